@@ -1,0 +1,492 @@
+/*
+ * tcl_oracle.c -- plain, slow, obviously-correct fp64 CPU oracle of TCL's Mamba cost model.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_2604_12891_b200/) never links, imports or calls it, and shares no code,
+ * header or constant with it.
+ *
+ * Citations: "P:n" = PAPER.md line n (section given); "S:n" = SPEC.md line n;
+ * "Rk" = reading k of SURVEY.md §8(c) / DESIGN.md §3.
+ *
+ * Everything is computed in double precision from the fp32 weight blob and fp32 features
+ * (promoted on read).  No blocking, no fusion, no SIMD, no BLAS: every loop is the formula.
+ *
+ * Forward pass of one candidate (§5.2 "Model Architecture"):
+ *   encoder  : three linears with output widths enc_dims (64,128,128 in the paper),
+ *              SiLU after the first two (R1)
+ *   per layer: h <- h + Mixer(LN_l(h))   (R3; pre-norm residual Mamba block)
+ *              Mixer = in_proj -> causal depthwise conv1d (d_conv taps) -> SiLU (R4)
+ *                      -> x_proj [dt_r | B | C] -> Delta = softplus(dt_proj(dt_r) + b_dt) (R7)
+ *                      -> selective scan with ZOH discretisation (Eqs. 4-5, R5, R6)
+ *                      -> D-skip -> gate y * SiLU(z) -> out_proj
+ *   final    : LN_f ("normalized again"), masked mean over the T real tokens (R9),
+ *              decoder three linears 64,32,1 with SiLU after the first two (R1).
+ *
+ * Parity-pin status of each function: see the header of tests/test_oracle_pins.py and
+ * DESIGN.md §4.  Absolute agreement with the paper's trained model is "parity unpinned"
+ * (no weights were released); the pins fix every step's arithmetic instead.
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* Same field order as tcl_dims in include/tcl.h (an interface, declared independently). */
+typedef struct {
+    int32_t d_in, max_len, d_model, n_layer, d_state, d_conv, expand, dt_rank;
+    int32_t enc_dims[3];
+    int32_t dec_dims[3];
+    float ln_eps;
+    float dropout_p;
+    int32_t precision, disc;
+} tclo_dims;
+
+enum { TCLO_DISC_ZOH = 0, TCLO_DISC_EULER_B = 1 };
+
+/* ------------------------------------------------------------------ elementary functions */
+
+/* SiLU(v) = v * sigmoid(v) = v / (1 + e^{-v})  (R1; Mamba's activation) */
+double tclo_silu(double v) { return v / (1.0 + exp(-v)); }
+
+/* softplus(v) = log(1 + e^v) (R13).  For v > 0 the algebraically identical
+ * v + log1p(e^{-v}) is used so that e^v cannot overflow. */
+double tclo_softplus(double v) {
+    if (v > 0.0) return v + log1p(exp(-v));
+    return log1p(exp(v));
+}
+
+/* y = W x + b, W row-major [out][in] (PyTorch nn.Linear layout). b may be NULL. */
+static void linear(const float* W, const float* b, int out, int in, const double* x, double* y) {
+    for (int o = 0; o < out; ++o) {
+        double acc = b ? (double)b[o] : 0.0;
+        for (int i = 0; i < in; ++i) acc += (double)W[(size_t)o * in + i] * x[i];
+        y[o] = acc;
+    }
+}
+
+/* LayerNorm over one row of width d (R2): (x - mean) / sqrt(var + eps) * g + b, biased var. */
+void tclo_layernorm_row(const double* x, int d, const float* g, const float* b, double eps,
+                        double* y) {
+    double mean = 0.0;
+    for (int i = 0; i < d; ++i) mean += x[i];
+    mean /= d;
+    double var = 0.0;
+    for (int i = 0; i < d; ++i) var += (x[i] - mean) * (x[i] - mean);
+    var /= d;
+    double rstd = 1.0 / sqrt(var + eps);
+    for (int i = 0; i < d; ++i) {
+        double v = (x[i] - mean) * rstd;
+        y[i] = g ? v * (double)g[i] + (double)b[i] : v;
+    }
+}
+
+/* Causal depthwise conv1d + SiLU over one candidate ("lightweight depthwise
+ * one-dimensional convolution"; R4 conv then SiLU):
+ *   c[t][d] = SiLU( b[d] + sum_{k<dc} w[d][k] * x[t-(dc-1)+k][d] ),  x[t'<0] = 0.
+ * x, c: [T][di] row-major; w: [di][dc]; tap dc-1 multiplies the current token. */
+void tclo_causal_conv_silu(const double* x, int T, int di, int dc, const float* w,
+                           const float* b, double* c) {
+    for (int t = 0; t < T; ++t)
+        for (int d = 0; d < di; ++d) {
+            double acc = b ? (double)b[d] : 0.0;
+            for (int k = 0; k < dc; ++k) {
+                int ts = t - (dc - 1) + k;
+                if (ts >= 0) acc += (double)w[(size_t)d * dc + k] * x[(size_t)ts * di + d];
+            }
+            c[(size_t)t * di + d] = tclo_silu(acc);
+        }
+}
+
+/* Selective scan over one candidate (Eqs. 4-5 discretised; R5, R6):
+ *   s_{-1} = 0;  for t < T, d < di, n < N:
+ *     Abar = exp(delta[t][d] * A[d][n])
+ *     Bbar = (exp(delta*A) - 1) / A * B[t][n]      (ZOH, default)  |  delta * B[t][n]  (Euler-B)
+ *     s[d][n] = Abar * s[d][n] + Bbar * u[t][d]
+ *   y[t][d] = sum_n C[t][n] * s[d][n] + Dv[d] * u[t][d]
+ * u, delta, y: [T][di]; B, C: [T][N]; A: [di][N] (strictly negative); Dv: [di].
+ * (e^{x}-1) is evaluated with expm1, i.e. exactly the definition without cancellation. */
+void tclo_ssm_scan(int T, int di, int N, const double* u, const double* delta,
+                   const double* A, const double* B, const double* C, const double* Dv,
+                   int disc, double* y) {
+    double* s = (double*)calloc((size_t)di * N, sizeof(double));
+    for (int t = 0; t < T; ++t) {
+        for (int d = 0; d < di; ++d) {
+            double dt = delta[(size_t)t * di + d];
+            double ut = u[(size_t)t * di + d];
+            double acc = 0.0;
+            for (int n = 0; n < N; ++n) {
+                double a = A[(size_t)d * N + n];
+                double Abar = exp(dt * a);
+                double Bbar = (disc == TCLO_DISC_EULER_B) ? dt * B[(size_t)t * N + n]
+                                                          : expm1(dt * a) / a * B[(size_t)t * N + n];
+                s[(size_t)d * N + n] = Abar * s[(size_t)d * N + n] + Bbar * ut;
+                acc += C[(size_t)t * N + n] * s[(size_t)d * N + n];
+            }
+            y[(size_t)t * di + d] = acc + Dv[d] * ut;
+        }
+    }
+    free(s);
+}
+
+/* ------------------------------------------------------------------ Philox4x32-10 (R17) */
+/* Salmon et al. 2011 ("Parallel random numbers: as easy as 1, 2, 3"), the Random123
+ * Philox4x32 with 10 rounds: multipliers 0xD2511F53, 0xCD9E8D57; Weyl key increments
+ * 0x9E3779B9, 0xBB67AE85.  Pinned by the published known-answer vectors (tests). */
+void tclo_philox4x32_10(const uint32_t ctr_in[4], const uint32_t key_in[2], uint32_t out[4]) {
+    uint32_t c0 = ctr_in[0], c1 = ctr_in[1], c2 = ctr_in[2], c3 = ctr_in[3];
+    uint32_t k0 = key_in[0], k1 = key_in[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0;
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0;
+        uint32_t n1 = lo1;
+        uint32_t n2 = hi0 ^ c3 ^ k1;
+        uint32_t n3 = lo0;
+        c0 = n0; c1 = n1; c2 = n2; c3 = n3;
+        k0 += 0x9E3779B9u;
+        k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+/* Inverted-dropout multiplier for hidden unit `unit` of `site` (R17):
+ *   counter = (unit>>2, token<<2 | site, pass, global index), key = (seed lo, seed hi);
+ *   keep iff word[unit & 3] >= floor(p * 2^32); kept units are scaled by 1/(1-p). */
+static double dropout_mult(uint64_t seed, double p, uint32_t thr, int unit, int token, int site,
+                           int pass, int64_t gidx) {
+    uint32_t ctr[4] = {(uint32_t)unit >> 2, ((uint32_t)token << 2) | (uint32_t)site,
+                       (uint32_t)pass, (uint32_t)gidx};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t w[4];
+    tclo_philox4x32_10(ctr, key, w);
+    return (w[unit & 3] >= thr) ? 1.0 / (1.0 - p) : 0.0;
+}
+
+/* ------------------------------------------------------------------ weight blob */
+typedef struct {
+    const float *W1, *b1, *W2, *b2, *W3, *b3;
+} mlp_w;
+typedef struct {
+    const float *ln_w, *ln_b, *W_in, *w_conv, *b_conv, *W_x, *W_dt, *b_dt, *A_log, *Dv, *W_out;
+} layer_w;
+
+/* Canonical order of SURVEY §8(b); returns number of floats consumed. */
+static int64_t parse_blob(const tclo_dims* d, const float* w, mlp_w* enc, layer_w* L, const float** lnf_w,
+                          const float** lnf_b, mlp_w* dec) {
+    const int dm = d->d_model, di = d->expand * d->d_model, N = d->d_state, R = d->dt_rank;
+    const float* p = w;
+#define TAKE(dst, cnt) do { dst = p; p += (cnt); } while (0)
+    TAKE(enc->W1, (int64_t)d->enc_dims[0] * d->d_in); TAKE(enc->b1, d->enc_dims[0]);
+    TAKE(enc->W2, (int64_t)d->enc_dims[1] * d->enc_dims[0]); TAKE(enc->b2, d->enc_dims[1]);
+    TAKE(enc->W3, (int64_t)d->enc_dims[2] * d->enc_dims[1]); TAKE(enc->b3, d->enc_dims[2]);
+    for (int l = 0; l < d->n_layer; ++l) {
+        layer_w* q = L ? &L[l] : NULL;
+        layer_w dummy;
+        if (!q) q = &dummy;
+        TAKE(q->ln_w, dm); TAKE(q->ln_b, dm);
+        TAKE(q->W_in, (int64_t)2 * di * dm);
+        TAKE(q->w_conv, (int64_t)di * d->d_conv); TAKE(q->b_conv, di);
+        TAKE(q->W_x, (int64_t)(R + 2 * N) * di);
+        TAKE(q->W_dt, (int64_t)di * R); TAKE(q->b_dt, di);
+        TAKE(q->A_log, (int64_t)di * N); TAKE(q->Dv, di);
+        TAKE(q->W_out, (int64_t)dm * di);
+    }
+    TAKE(*lnf_w, dm); TAKE(*lnf_b, dm);
+    TAKE(dec->W1, (int64_t)d->dec_dims[0] * dm); TAKE(dec->b1, d->dec_dims[0]);
+    TAKE(dec->W2, (int64_t)d->dec_dims[1] * d->dec_dims[0]); TAKE(dec->b2, d->dec_dims[1]);
+    TAKE(dec->W3, (int64_t)d->dec_dims[2] * d->dec_dims[1]); TAKE(dec->b3, d->dec_dims[2]);
+#undef TAKE
+    return (int64_t)(p - w);
+}
+
+/* Number of fp32 weights in the canonical blob: the sizes parse_blob walks, summed. */
+int64_t tclo_weights_count(const tclo_dims* d) {
+    const int64_t dm = d->d_model, di = (int64_t)d->expand * d->d_model, N = d->d_state,
+                  R = d->dt_rank, din = d->d_in;
+    int64_t enc = d->enc_dims[0] * din + d->enc_dims[0] + (int64_t)d->enc_dims[1] * d->enc_dims[0] +
+                  d->enc_dims[1] + (int64_t)d->enc_dims[2] * d->enc_dims[1] + d->enc_dims[2];
+    int64_t layer = 2 * dm + 2 * di * dm + di * d->d_conv + di + (R + 2 * N) * di + di * R + di +
+                    di * N + di + dm * di;
+    int64_t dec = d->dec_dims[0] * dm + d->dec_dims[0] + (int64_t)d->dec_dims[1] * d->dec_dims[0] +
+                  d->dec_dims[1] + (int64_t)d->dec_dims[2] * d->dec_dims[1] + d->dec_dims[2];
+    return enc + d->n_layer * layer + 2 * dm + dec;
+}
+
+static int dims_ok(const tclo_dims* d) {
+    if (d->d_in < 1 || d->max_len < 1 || d->d_model < 1 || d->n_layer < 0 || d->d_state < 1 ||
+        d->d_conv < 1 || d->expand < 1 || d->dt_rank < 1) return 0;
+    if (d->enc_dims[2] != d->d_model || d->dec_dims[2] != 1) return 0;
+    for (int i = 0; i < 3; ++i) if (d->enc_dims[i] < 1 || d->dec_dims[i] < 1) return 0;
+    return 1;
+}
+
+/* ------------------------------------------------------------------ forward, one candidate */
+/* Dump layout (doubles), written when dump != NULL (per-stage parity checks):
+ *   h_enc [T][dm]
+ *   per layer l: a [T][dm], x [T][di], z [T][di], u [T][di], dtr [T][R], B [T][N], C [T][N],
+ *                delta [T][di], y [T][di], g [T][di], h [T][dm]
+ *   pooled [dm], dec_h1 [h1], dec_h2 [h2]
+ * Dropout (MC mode) is applied when mc_pass >= 0. */
+typedef struct {
+    int mc_pass;          /* -1: deterministic forward */
+    uint64_t seed;
+    int64_t gidx;
+} mc_ctx;
+
+static double forward_one(const tclo_dims* d, const float* wblob, const float* x_in, int T,
+                          const mc_ctx* mc, double* dump) {
+    const int dm = d->d_model, di = d->expand * d->d_model, N = d->d_state, R = d->dt_rank;
+    const int e1 = d->enc_dims[0], e2 = d->enc_dims[1];
+    const int h1 = d->dec_dims[0], h2 = d->dec_dims[1];
+    const double eps = (double)d->ln_eps;
+    const double p = (double)d->dropout_p;
+    const uint32_t thr = (uint32_t)floor(p * 4294967296.0);
+    mlp_w enc, dec;
+    const float *lnf_w, *lnf_b;
+    layer_w* L = (layer_w*)calloc((size_t)(d->n_layer > 0 ? d->n_layer : 1), sizeof(layer_w));
+    parse_blob(d, wblob, &enc, L, &lnf_w, &lnf_b, &dec);
+
+    double* h = (double*)calloc((size_t)T * dm, sizeof(double));
+    double* xin = (double*)calloc((size_t)d->d_in, sizeof(double));
+    double* t1 = (double*)calloc((size_t)(e1 > h1 ? e1 : h1) + 1, sizeof(double));
+    double* t2 = (double*)calloc((size_t)(e2 > h2 ? e2 : h2) + 1, sizeof(double));
+    double* dp = dump;
+
+    /* encoder */
+    for (int t = 0; t < T; ++t) {
+        for (int i = 0; i < d->d_in; ++i) xin[i] = (double)x_in[(size_t)t * d->d_in + i];
+        linear(enc.W1, enc.b1, e1, d->d_in, xin, t1);
+        for (int i = 0; i < e1; ++i) {
+            t1[i] = tclo_silu(t1[i]);
+            if (mc && mc->mc_pass >= 0) t1[i] *= dropout_mult(mc->seed, p, thr, i, t, 0, mc->mc_pass, mc->gidx);
+        }
+        linear(enc.W2, enc.b2, e2, e1, t1, t2);
+        for (int i = 0; i < e2; ++i) {
+            t2[i] = tclo_silu(t2[i]);
+            if (mc && mc->mc_pass >= 0) t2[i] *= dropout_mult(mc->seed, p, thr, i, t, 1, mc->mc_pass, mc->gidx);
+        }
+        linear(enc.W3, enc.b3, dm, e2, t2, &h[(size_t)t * dm]);
+    }
+    if (dp) { memcpy(dp, h, sizeof(double) * T * dm); dp += (size_t)T * dm; }
+
+    double* a = (double*)calloc((size_t)T * dm, sizeof(double));
+    double* xz = (double*)calloc((size_t)2 * di, sizeof(double));
+    double* x = (double*)calloc((size_t)T * di, sizeof(double));
+    double* z = (double*)calloc((size_t)T * di, sizeof(double));
+    double* u = (double*)calloc((size_t)T * di, sizeof(double));
+    double* dbc = (double*)calloc((size_t)(R + 2 * N), sizeof(double));
+    double* dtr = (double*)calloc((size_t)T * R, sizeof(double));
+    double* Bm = (double*)calloc((size_t)T * N, sizeof(double));
+    double* Cm = (double*)calloc((size_t)T * N, sizeof(double));
+    double* delta = (double*)calloc((size_t)T * di, sizeof(double));
+    double* A = (double*)calloc((size_t)di * N, sizeof(double));
+    double* Dv = (double*)calloc((size_t)di, sizeof(double));
+    double* y = (double*)calloc((size_t)T * di, sizeof(double));
+    double* g = (double*)calloc((size_t)T * di, sizeof(double));
+    double* o = (double*)calloc((size_t)dm, sizeof(double));
+
+    for (int l = 0; l < d->n_layer; ++l) {
+        const layer_w* q = &L[l];
+        /* pre-norm (R2, R3) and in_proj */
+        for (int t = 0; t < T; ++t) {
+            tclo_layernorm_row(&h[(size_t)t * dm], dm, q->ln_w, q->ln_b, eps, &a[(size_t)t * dm]);
+            linear(q->W_in, NULL, 2 * di, dm, &a[(size_t)t * dm], xz);
+            for (int i = 0; i < di; ++i) { x[(size_t)t * di + i] = xz[i]; z[(size_t)t * di + i] = xz[di + i]; }
+        }
+        /* causal depthwise conv + SiLU (R4) */
+        tclo_causal_conv_silu(x, T, di, d->d_conv, q->w_conv, q->b_conv, u);
+        /* selection: x_proj -> [dt_r | B | C]; Delta = softplus(W_dt dt_r + b_dt) (R7) */
+        for (int t = 0; t < T; ++t) {
+            linear(q->W_x, NULL, R + 2 * N, di, &u[(size_t)t * di], dbc);
+            for (int r = 0; r < R; ++r) dtr[(size_t)t * R + r] = dbc[r];
+            for (int n = 0; n < N; ++n) { Bm[(size_t)t * N + n] = dbc[R + n]; Cm[(size_t)t * N + n] = dbc[R + N + n]; }
+            linear(q->W_dt, q->b_dt, di, R, &dtr[(size_t)t * R], &delta[(size_t)t * di]);
+            for (int i = 0; i < di; ++i) delta[(size_t)t * di + i] = tclo_softplus(delta[(size_t)t * di + i]);
+        }
+        /* A = -exp(A_log) (R8) */
+        for (int i = 0; i < di * N; ++i) A[i] = -exp((double)q->A_log[i]);
+        for (int i = 0; i < di; ++i) Dv[i] = (double)q->Dv[i];
+        tclo_ssm_scan(T, di, N, u, delta, A, Bm, Cm, Dv, d->disc, y);
+        /* gate y * SiLU(z); out_proj; residual */
+        for (int t = 0; t < T; ++t) {
+            for (int i = 0; i < di; ++i) g[(size_t)t * di + i] = y[(size_t)t * di + i] * tclo_silu(z[(size_t)t * di + i]);
+            linear(q->W_out, NULL, dm, di, &g[(size_t)t * di], o);
+            for (int i = 0; i < dm; ++i) h[(size_t)t * dm + i] += o[i];
+        }
+        if (dp) {
+#define DUMP(src, cnt) do { memcpy(dp, src, sizeof(double) * (size_t)(cnt)); dp += (cnt); } while (0)
+            DUMP(a, (size_t)T * dm); DUMP(x, (size_t)T * di); DUMP(z, (size_t)T * di); DUMP(u, (size_t)T * di);
+            DUMP(dtr, (size_t)T * R); DUMP(Bm, (size_t)T * N); DUMP(Cm, (size_t)T * N);
+            DUMP(delta, (size_t)T * di); DUMP(y, (size_t)T * di); DUMP(g, (size_t)T * di); DUMP(h, (size_t)T * dm);
+        }
+    }
+
+    /* final norm, masked mean over the T real tokens (R9), decoder */
+    double* pooled = (double*)calloc((size_t)dm, sizeof(double));
+    double* f = (double*)calloc((size_t)dm, sizeof(double));
+    for (int t = 0; t < T; ++t) {
+        tclo_layernorm_row(&h[(size_t)t * dm], dm, lnf_w, lnf_b, eps, f);
+        for (int i = 0; i < dm; ++i) pooled[i] += f[i];
+    }
+    for (int i = 0; i < dm; ++i) pooled[i] /= (double)T;
+    linear(dec.W1, dec.b1, h1, dm, pooled, t1);
+    for (int i = 0; i < h1; ++i) {
+        t1[i] = tclo_silu(t1[i]);
+        if (mc && mc->mc_pass >= 0) t1[i] *= dropout_mult(mc->seed, p, thr, i, 0, 2, mc->mc_pass, mc->gidx);
+    }
+    linear(dec.W2, dec.b2, h2, h1, t1, t2);
+    for (int i = 0; i < h2; ++i) {
+        t2[i] = tclo_silu(t2[i]);
+        if (mc && mc->mc_pass >= 0) t2[i] *= dropout_mult(mc->seed, p, thr, i, 0, 3, mc->mc_pass, mc->gidx);
+    }
+    double score;
+    linear(dec.W3, dec.b3, 1, h2, t2, &score);
+    if (dp) { DUMP(pooled, dm); DUMP(t1, h1); DUMP(t2, h2); }
+#undef DUMP
+
+    free(pooled); free(f); free(o); free(g); free(y); free(Dv); free(A); free(delta); free(Cm);
+    free(Bm); free(dtr); free(dbc); free(u); free(z); free(x); free(xz); free(a); free(t2);
+    free(t1); free(xin); free(h); free(L);
+    return score;
+}
+
+/* Size of the dump of forward_one, in doubles. */
+int64_t tclo_dump_size(const tclo_dims* d, int T) {
+    const int64_t dm = d->d_model, di = (int64_t)d->expand * d->d_model, N = d->d_state, R = d->dt_rank;
+    /* a, x, z, u, dtr, B, C, delta, y, g, h */
+    int64_t per_layer = T * dm + 3 * T * di + T * R + 2 * T * N + 3 * T * di + T * dm;
+    return T * dm + d->n_layer * per_layer + dm + d->dec_dims[0] + d->dec_dims[1];
+}
+
+/* One candidate with the per-stage dump (dump may be NULL). Returns 0 on success. */
+int tclo_forward_one(const tclo_dims* d, const float* w, const float* feats_one, int T, double* dump,
+                     double* score) {
+    if (!dims_ok(d) || T < 1 || T > d->max_len) return -1;
+    *score = forward_one(d, w, feats_one, T, NULL, dump);
+    return 0;
+}
+
+/* ------------------------------------------------------------------ batched, threaded */
+typedef struct {
+    const tclo_dims* d;
+    const float* w;
+    const float* feats;
+    const int32_t* lens;
+    int64_t n, begin, step;
+    int mc_passes;
+    uint64_t seed;
+    int64_t index_base;
+    double* scores;   /* deterministic mode */
+    double* mean;     /* MC mode */
+    double* var;
+} job_t;
+
+static void* worker(void* arg) {
+    job_t* j = (job_t*)arg;
+    const size_t stride = (size_t)j->d->max_len * j->d->d_in;
+    for (int64_t i = j->begin; i < j->n; i += j->step) {
+        int T = j->lens[i];
+        const float* xf = j->feats + (size_t)i * stride;
+        if (T < 1 || T > j->d->max_len) {  /* R16: invalid length -> NaN score */
+            if (j->scores) j->scores[i] = NAN;
+            if (j->mean) { j->mean[i] = NAN; j->var[i] = NAN; }
+            continue;
+        }
+        if (j->mc_passes <= 0) {
+            j->scores[i] = forward_one(j->d, j->w, xf, T, NULL, NULL);
+        } else {
+            /* Welford over passes; population variance (divide by the number of passes) (R17) */
+            double m = 0.0, M2 = 0.0;
+            for (int ps = 0; ps < j->mc_passes; ++ps) {
+                mc_ctx mc = {ps, j->seed, j->index_base + i};
+                double v = forward_one(j->d, j->w, xf, T, &mc, NULL);
+                double delta = v - m;
+                m += delta / (double)(ps + 1);
+                M2 += delta * (v - m);
+            }
+            j->mean[i] = m;
+            j->var[i] = M2 / (double)j->mc_passes;
+        }
+    }
+    return NULL;
+}
+
+static int run_threads(job_t* proto, int nthreads) {
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 256) nthreads = 256;
+    pthread_t th[256];
+    job_t jobs[256];
+    for (int k = 0; k < nthreads; ++k) {
+        jobs[k] = *proto;
+        jobs[k].begin = k;
+        jobs[k].step = nthreads;
+        if (nthreads == 1) { worker(&jobs[0]); return 0; }
+        pthread_create(&th[k], NULL, worker, &jobs[k]);
+    }
+    for (int k = 0; k < nthreads; ++k) pthread_join(th[k], NULL);
+    return 0;
+}
+
+/* scores[i] for candidates i < n; feats [n][max_len][d_in] fp32; lens [n]. */
+int tclo_score(const tclo_dims* d, const float* w, const float* feats, const int32_t* lens,
+               int64_t n, double* scores, int nthreads) {
+    if (!dims_ok(d) || n < 0) return -1;
+    job_t j = {d, w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL};
+    return run_threads(&j, nthreads);
+}
+
+/* MC-dropout (R17; north-star addition, absent from the paper): mean and population variance
+ * of the score over n_passes dropout passes. */
+int tclo_score_mc(const tclo_dims* d, const float* w, const float* feats, const int32_t* lens,
+                  int64_t n, int32_t n_passes, uint64_t seed, int64_t index_base, double* mean,
+                  double* var, int nthreads) {
+    if (!dims_ok(d) || n < 0 || n_passes < 1) return -1;
+    job_t j = {d, w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var};
+    return run_threads(&j, nthreads);
+}
+
+/* ------------------------------------------------------------------ top-k (R15) */
+/* The k best candidates under the total order (score desc, index asc), NaN treated as -inf.
+ * Selection by repeated linear scans (obviously correct, O(n k)); k is clamped to n and the
+ * slots >= n are filled with (idx -1, score -inf). */
+static int better(double a, int64_t ia, double b, int64_t ib) {
+    if (isnan(a)) a = -INFINITY;
+    if (isnan(b)) b = -INFINITY;
+    if (a != b) return a > b;
+    return ia < ib;
+}
+
+int tclo_topk_f64(const double* scores, int64_t n, int32_t k, int64_t index_base, int64_t* idx,
+                  double* top) {
+    if (k <= 0 || n < 0) return -1;
+    unsigned char* taken = (unsigned char*)calloc((size_t)(n > 0 ? n : 1), 1);
+    for (int32_t r = 0; r < k; ++r) {
+        int64_t best = -1;
+        for (int64_t i = 0; i < n; ++i) {
+            if (taken[i]) continue;
+            if (best < 0 || better(scores[i], i, scores[best], best)) best = i;
+        }
+        if (best < 0) { idx[r] = -1; top[r] = -INFINITY; continue; }
+        taken[best] = 1;
+        idx[r] = index_base + best;
+        top[r] = isnan(scores[best]) ? -INFINITY : scores[best];
+    }
+    free(taken);
+    return 0;
+}
+
+int tclo_topk_f32(const float* scores, int64_t n, int32_t k, int64_t index_base, int64_t* idx,
+                  float* top) {
+    if (k <= 0 || n < 0) return -1;
+    double* s = (double*)malloc(sizeof(double) * (size_t)(n > 0 ? n : 1));
+    double* t = (double*)malloc(sizeof(double) * (size_t)k);
+    for (int64_t i = 0; i < n; ++i) s[i] = (double)scores[i];
+    int rc = tclo_topk_f64(s, n, k, index_base, idx, t);
+    for (int32_t r = 0; r < k; ++r) top[r] = (float)t[r];
+    free(s); free(t);
+    return rc;
+}

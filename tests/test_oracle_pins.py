@@ -1,0 +1,413 @@
+"""Pins of the fp64 oracle (oracle/tcl_oracle.c) to things other than itself.
+
+Every test here runs on CPU (`-m "not gpu"`).  Each pin is one of: a value the paper prints
+(tests/golden/, cited), a closed form, a textbook/library routine (scipy expm, numpy convolve,
+torch layer_norm, scipy expit, np.logaddexp, numpy matmul), a brute-force evaluation on tiny
+inputs, or an invariant of the method.  They are chosen so that a plausible slip in the oracle
+(dropped term, wrong sign or index, transposed operand, swapped split) fails at least one:
+
+  function                 pinned by
+  -----------------------  ---------------------------------------------------------------
+  weights layout / count   paper model size 0.35 MB and KB+AC 0.7 MB
+  silu / softplus          scipy.special.expit, np.logaddexp (library)
+  layernorm_row            torch.nn.functional.layer_norm fp64 (library); mean 0 / var 1
+  causal_conv_silu         np.convolve per channel (library); identity kernel; causality
+  ssm_scan (ZOH)           brute-force O(T^2) unroll with Bbar from scipy.linalg.expm (Van Loan)
+                           closed-form special cases (u=0, C=0, A->-inf, Delta->0, constant input
+                           geometric sum, B*c / C/c invariance)
+  ssm_scan (Euler-B)       brute-force unroll with Bbar = Delta*B; A->-inf collapse
+  forward_one (stages)     every dumped stage re-derived from the previous one with library
+                           primitives (matmul, convolve, expit, logaddexp) + brute-force scan
+  forward (backbone off)   W_out == 0 reduces the model to MLP -> LN_f -> mean -> MLP:
+                           independent 15-line numpy implementation
+  score (batch)            padding invariance (random / NaN padded slots), permutation
+                           equivariance, batch-size invariance -- all exact
+  score_mc                 p = 0 => mean == score, var == 0 exactly; passes = 1 => var == 0;
+                           Philox KAT vectors (Random123); keep rate within 4 sigma of 1 - p
+  topk                     np.lexsort full stable sort; top-k of shard top-ks == global top-k
+
+Parity of absolute scores with the paper's trained model: parity unpinned (no weights released).
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+import scipy.linalg
+import scipy.special
+import torch
+
+import inputs
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+# ----------------------------------------------------------------------------- paper values
+def test_param_count_matches_paper_model_size(oracle):
+    g = json.load(open(os.path.join(GOLDEN, "paper_model_size.json")))
+    d = inputs.config("paper")["dims"]
+    assert (d.d_model, d.d_in, d.max_len, d.n_layer, d.d_state, d.expand, d.d_conv) == \
+        (g["d_model"], g["d_in"], g["max_len"], g["n_layer"], g["d_state"], g["expand"], g["d_conv"])
+    assert list(d.enc_dims) == g["enc_dims"] and list(d.dec_dims) == g["dec_dims"]
+    n = oracle.weights_count(d)
+    assert n == inputs.weights_count(d) == 92353
+    mib = n * g["bytes_per_param"] / 2 ** 20
+    assert round(mib, 2) == g["model_size_MB"]                    # 0.3523 MiB -> "0.35 MB"
+    assert round(2 * mib, 1) == g["kb_ac_size_MB"]                # KB + AC columns -> "0.7 MB"
+    # the alternative readings the pin excludes
+    assert round(oracle.weights_count(d.replace(expand=2)) * 4 / 2 ** 20, 2) != 0.35
+    assert round(oracle.weights_count(d.replace(d_state=32)) * 4 / 2 ** 20, 2) != 0.35
+
+
+@pytest.mark.parametrize("name", ["tiny", "tuning", "rdu", "large", "long"])
+def test_param_counts_of_configs(oracle, name):
+    d = inputs.config(name)["dims"]
+    expect = {"tiny": 26209, "tuning": 147777, "rdu": 147777, "large": 1021057, "long": 1021057}[name]
+    assert oracle.weights_count(d) == inputs.weights_count(d) == expect
+
+
+# ----------------------------------------------------------------------------- elementwise
+def test_silu_softplus_against_library(oracle):
+    for v in [-50.0, -5.0, -1.0, -1e-3, 0.0, 1e-3, 0.5, 3.0, 30.0, 800.0, -800.0]:
+        assert oracle.silu(v) == pytest.approx(v * scipy.special.expit(v), rel=1e-14, abs=1e-300)
+        assert oracle.softplus(v) == pytest.approx(np.logaddexp(0.0, v), rel=1e-14, abs=1e-300)
+
+
+def test_layernorm_against_torch(oracle):
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((7, 48)) * 3 + 1.5
+    g = rng.uniform(0.8, 1.2, 48).astype(np.float32)
+    b = rng.uniform(-0.1, 0.1, 48).astype(np.float32)
+    y = oracle.layernorm(x, g, b, eps=1e-5)
+    ref = torch.nn.functional.layer_norm(torch.from_numpy(x), (48,), torch.from_numpy(g.astype(np.float64)),
+                                         torch.from_numpy(b.astype(np.float64)), eps=1e-5).numpy()
+    np.testing.assert_allclose(y, ref, rtol=1e-12, atol=1e-12)
+    y0 = oracle.layernorm(x, eps=0.0)             # row mean 0, variance 1 before the affine
+    np.testing.assert_allclose(y0.mean(1), 0, atol=1e-12)
+    np.testing.assert_allclose(y0.var(1), 1, atol=1e-9)
+
+
+# ----------------------------------------------------------------------------- conv
+def test_conv_against_numpy_convolve(oracle):
+    rng = np.random.default_rng(1)
+    T, di, dc = 9, 5, 4
+    x = rng.standard_normal((T, di))
+    w = rng.standard_normal((di, dc)).astype(np.float32)
+    b = rng.standard_normal(di).astype(np.float32)
+    c = oracle.causal_conv_silu(x, w, b)
+    for d in range(di):
+        pre = np.convolve(x[:, d], w[d, ::-1].astype(np.float64))[:T] + b[d]
+        np.testing.assert_allclose(c[:, d], pre * scipy.special.expit(pre), rtol=1e-13, atol=1e-14)
+
+
+def test_conv_identity_kernel_and_causality(oracle):
+    rng = np.random.default_rng(2)
+    T, di, dc = 8, 3, 4
+    x = rng.standard_normal((T, di))
+    w = np.zeros((di, dc), np.float32)
+    w[:, -1] = 1.0                                 # kernel [0,...,0,1] is the identity
+    c = oracle.causal_conv_silu(x, w, np.zeros(di, np.float32))
+    np.testing.assert_allclose(c, x * scipy.special.expit(x), rtol=1e-14)
+    w = rng.standard_normal((di, dc)).astype(np.float32)
+    c0 = oracle.causal_conv_silu(x, w, None)
+    x2 = x.copy()
+    x2[5] += 10.0
+    c1 = oracle.causal_conv_silu(x2, w, None)
+    assert np.array_equal(c0[:5], c1[:5]) and not np.allclose(c0[5:], c1[5:])
+
+
+# ----------------------------------------------------------------------------- scan
+def _rand_scan(rng, T=5, di=3, N=4):
+    u = rng.standard_normal((T, di))
+    delta = np.exp(rng.uniform(np.log(1e-3), np.log(2.0), (T, di)))
+    A = -np.exp(rng.uniform(-1, 2.5, (di, N)))
+    B = rng.standard_normal((T, N))
+    C = rng.standard_normal((T, N))
+    Dv = rng.uniform(0.5, 1.5, di)
+    return u, delta, A, B, C, Dv
+
+
+def _vanloan_zoh(dt, a, b):
+    """ZOH from the matrix exponential: expm([[dt a, dt b],[0, 0]]) = [[Abar, Bbar],[0, 1]]."""
+    M = np.array([[dt * a, dt * b], [0.0, 0.0]])
+    E = scipy.linalg.expm(M)
+    return E[0, 0], E[0, 1]
+
+
+def _brute_scan(u, delta, A, B, C, Dv, disc):
+    """s_t = sum_{sigma<=t} (prod_{r=sigma+1..t} Abar_r) Bbar_sigma u_sigma ; y_t = C_t.s_t + D u_t."""
+    T, di = u.shape
+    N = A.shape[1]
+    y = np.zeros((T, di))
+    for t in range(T):
+        for d in range(di):
+            acc = 0.0
+            for n in range(N):
+                s = 0.0
+                for sg in range(t + 1):
+                    prod = 1.0
+                    for r in range(sg + 1, t + 1):
+                        prod *= _vanloan_zoh(delta[r, d], A[d, n], 0.0)[0]
+                    if disc == inputs.DISC_ZOH:
+                        bbar = _vanloan_zoh(delta[sg, d], A[d, n], B[sg, n])[1]
+                    else:
+                        bbar = delta[sg, d] * B[sg, n]
+                    s += prod * bbar * u[sg, d]
+                acc += C[t, n] * s
+            y[t, d] = acc + Dv[d] * u[t, d]
+    return y
+
+
+@pytest.mark.parametrize("disc", [inputs.DISC_ZOH, inputs.DISC_EULER_B])
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_scan_against_bruteforce_unroll(oracle, disc, seed):
+    rng = np.random.default_rng(10 + seed)
+    args = _rand_scan(rng, T=6, di=3, N=4)
+    y = oracle.ssm_scan(*args, disc=disc)
+    np.testing.assert_allclose(y, _brute_scan(*args, disc), rtol=1e-10, atol=1e-12)
+
+
+def test_zoh_coefficients_vanloan(oracle):
+    """T=1 with C=e_n, u=1, D=0 exposes Bbar; T=2 with u_1=0 exposes Abar*Bbar."""
+    rng = np.random.default_rng(3)
+    for _ in range(20):
+        dt = float(np.exp(rng.uniform(np.log(1e-4), np.log(3.0))))
+        a = -float(np.exp(rng.uniform(-2, 3)))
+        b = float(rng.standard_normal())
+        Ab, Bb = _vanloan_zoh(dt, a, b)
+        y1 = oracle.ssm_scan(np.ones((1, 1)), np.full((1, 1), dt), np.array([[a]]), np.array([[b]]),
+                             np.ones((1, 1)), np.zeros(1))
+        assert y1[0, 0] == pytest.approx(Bb, rel=1e-12)
+        y2 = oracle.ssm_scan(np.array([[1.0], [0.0]]), np.full((2, 1), dt), np.array([[a]]),
+                             np.array([[b], [b]]), np.ones((2, 1)), np.zeros(1))
+        assert y2[1, 0] == pytest.approx(Ab * Bb, rel=1e-12)
+        # Euler-B is the first-order limit of ZOH: difference O(dt^2)
+        ye = oracle.ssm_scan(np.ones((1, 1)), np.full((1, 1), dt), np.array([[a]]), np.array([[b]]),
+                             np.ones((1, 1)), np.zeros(1), disc=inputs.DISC_EULER_B)
+        assert abs(ye[0, 0] - y1[0, 0]) <= abs(b) * (dt * dt * abs(a)) * 0.5 * 1.0001 + 1e-15
+
+
+def test_scan_special_cases(oracle):
+    rng = np.random.default_rng(4)
+    u, delta, A, B, C, Dv = _rand_scan(rng, T=7, di=4, N=5)
+    # u = 0 -> y = 0
+    assert np.all(oracle.ssm_scan(np.zeros_like(u), delta, A, B, C, Dv) == 0.0)
+    # C = 0 -> y = D u
+    np.testing.assert_allclose(oracle.ssm_scan(u, delta, A, B, np.zeros_like(C), Dv), Dv * u, rtol=1e-15)
+    # Delta -> 0 -> y -> D u
+    y = oracle.ssm_scan(u, np.full_like(delta, 1e-12), A, B, C, Dv)
+    np.testing.assert_allclose(y, Dv * u, atol=1e-9)
+    # A -> -inf: ZOH gives Abar = 0 and Bbar = (0-1)/A * B -> 0, so y = D u;
+    # Euler-B gives y_t = <C_t, Delta_t B_t> u_t + D u_t -- discriminates reading R5.
+    Ainf = np.full_like(A, -1e300)
+    np.testing.assert_allclose(oracle.ssm_scan(u, delta, Ainf, B, C, Dv), Dv * u, rtol=1e-15)
+    ye = oracle.ssm_scan(u, delta, Ainf, B, C, Dv, disc=inputs.DISC_EULER_B)
+    np.testing.assert_allclose(ye, (C * B).sum(1)[:, None] * delta * u + Dv * u, rtol=1e-13)
+    # B*c and C/c leave y unchanged
+    np.testing.assert_allclose(oracle.ssm_scan(u, delta, A, B * 8.0, C / 8.0, Dv),
+                               oracle.ssm_scan(u, delta, A, B, C, Dv), rtol=1e-13)
+
+
+def test_scan_constant_input_geometric_sum(oracle):
+    """Time-invariant Delta/B/C and constant u: s_t = Bbar u (1 - Abar^{t+1}) / (1 - Abar)
+    (S4's convolutional view)."""
+    T, dt, a, b, c, u0 = 12, 0.3, -0.7, 1.3, -0.4, 0.9
+    Ab, Bb = _vanloan_zoh(dt, a, b)
+    y = oracle.ssm_scan(np.full((T, 1), u0), np.full((T, 1), dt), np.array([[a]]), np.full((T, 1), b),
+                        np.full((T, 1), c), np.zeros(1))
+    t = np.arange(T)
+    np.testing.assert_allclose(y[:, 0], c * Bb * u0 * (1 - Ab ** (t + 1)) / (1 - Ab), rtol=1e-12)
+
+
+# ----------------------------------------------------------------------------- whole model
+def _model(name, n, seed_off=1, **featkw):
+    c = inputs.config(name)
+    d = c["dims"]
+    w = inputs.make_weights(d, c["seed"])
+    f, l = inputs.make_features(d, n, c["seed"] + seed_off, **featkw)
+    return d, w, f, l
+
+
+def _silu(v):
+    return v * scipy.special.expit(v)
+
+
+def _ln(x, g, b, eps):
+    t = torch.from_numpy(np.atleast_2d(x))
+    return torch.nn.functional.layer_norm(t, (t.shape[-1],), torch.from_numpy(g.astype(np.float64)),
+                                          torch.from_numpy(b.astype(np.float64)), eps=eps).numpy()
+
+
+@pytest.mark.parametrize("name,disc", [("tiny", inputs.DISC_ZOH), ("paper", inputs.DISC_ZOH),
+                                       ("tiny", inputs.DISC_EULER_B)])
+def test_forward_stages_chain(oracle, name, disc):
+    """Each dumped stage re-derived from the previous with library primitives."""
+    d, w, f, l = _model(name, 4)
+    d = d.replace(disc=disc)
+    W = {k: v.astype(np.float64) for k, v in inputs.split_weights(d, w).items()}
+    T = 5
+    score, st = oracle.forward_one(d, w, f[0], T)
+    x = f[0, :T].astype(np.float64)
+    e1 = _silu(x @ W["enc.W1"].T + W["enc.b1"])
+    e2 = _silu(e1 @ W["enc.W2"].T + W["enc.b2"])
+    h = e2 @ W["enc.W3"].T + W["enc.b3"]
+    np.testing.assert_allclose(st["h_enc"], h, rtol=1e-11, atol=1e-12)
+    di, R, N = d.d_inner, d.dt_rank, d.d_state
+    for li in range(d.n_layer):
+        p = f"layer{li}."
+        g = lambda k: st[p + k]
+        np.testing.assert_allclose(g("a"), _ln(h, W[p + "ln_w"], W[p + "ln_b"], d.ln_eps), rtol=1e-11, atol=1e-12)
+        xz = g("a") @ W[p + "W_in"].T
+        np.testing.assert_allclose(g("x"), xz[:, :di], rtol=1e-11, atol=1e-12)
+        np.testing.assert_allclose(g("z"), xz[:, di:], rtol=1e-11, atol=1e-12)
+        for ch in range(di):
+            pre = np.convolve(g("x")[:, ch], W[p + "w_conv"][ch, ::-1])[:T] + W[p + "b_conv"][ch]
+            np.testing.assert_allclose(g("u")[:, ch], _silu(pre), rtol=1e-11, atol=1e-12)
+        dbc = g("u") @ W[p + "W_x"].T
+        np.testing.assert_allclose(g("dtr"), dbc[:, :R], rtol=1e-11, atol=1e-12)
+        np.testing.assert_allclose(g("B"), dbc[:, R:R + N], rtol=1e-11, atol=1e-12)
+        np.testing.assert_allclose(g("C"), dbc[:, R + N:], rtol=1e-11, atol=1e-12)
+        np.testing.assert_allclose(g("delta"), np.logaddexp(0, g("dtr") @ W[p + "W_dt"].T + W[p + "b_dt"]),
+                                   rtol=1e-11, atol=1e-14)
+        A = -np.exp(W[p + "A_log"])
+        y = _brute_scan(g("u"), g("delta"), A, g("B"), g("C"), W[p + "Dv"], disc)
+        np.testing.assert_allclose(g("y"), y, rtol=1e-9, atol=1e-11)
+        np.testing.assert_allclose(g("g"), g("y") * _silu(g("z")), rtol=1e-12, atol=1e-14)
+        h = h + g("g") @ W[p + "W_out"].T
+        np.testing.assert_allclose(g("h"), h, rtol=1e-10, atol=1e-11)
+    pooled = _ln(h, W["lnf_w"], W["lnf_b"], d.ln_eps).mean(0)
+    np.testing.assert_allclose(st["pooled"], pooled, rtol=1e-11, atol=1e-12)
+    d1 = _silu(pooled @ W["dec.W1"].T + W["dec.b1"])
+    d2 = _silu(d1 @ W["dec.W2"].T + W["dec.b2"])
+    assert score == pytest.approx(float(d2 @ W["dec.W3"][0] + W["dec.b3"][0]), rel=1e-11, abs=1e-12)
+
+
+def test_backbone_off_reduces_to_mlp(oracle):
+    """W_out == 0 in every layer => model == MLP -> LN_f -> masked mean -> MLP (independent numpy)."""
+    d, w, f, l = _model("tuning", 24)
+    names = inputs.manifest(d)
+    w = w.copy()
+    for m in names:
+        if m["name"].endswith("W_out"):
+            w[m["offset"]:m["offset"] + int(np.prod(m["shape"]))] = 0.0
+    W = {k: v.astype(np.float64) for k, v in inputs.split_weights(d, w).items()}
+    got = oracle.score(d, w, f, l)
+    for i in range(len(l)):
+        x = f[i, :l[i]].astype(np.float64)
+        h = _silu(_silu(x @ W["enc.W1"].T + W["enc.b1"]) @ W["enc.W2"].T + W["enc.b2"]) @ W["enc.W3"].T + W["enc.b3"]
+        mu = h.mean(1, keepdims=True)
+        var = ((h - mu) ** 2).mean(1, keepdims=True)
+        p = (((h - mu) / np.sqrt(var + d.ln_eps)) * W["lnf_w"] + W["lnf_b"]).mean(0)
+        s = _silu(_silu(p @ W["dec.W1"].T + W["dec.b1"]) @ W["dec.W2"].T + W["dec.b2"]) @ W["dec.W3"][0] + W["dec.b3"][0]
+        assert got[i] == pytest.approx(s, rel=1e-11, abs=1e-12)
+
+
+def test_padding_invariance_exact(oracle):
+    """Padded slots are ignored whatever they hold (R16; S:318 '< 1e-12', exact here)."""
+    d, w, f, l = _model("tiny", 64)
+    s0 = oracle.score(d, w, f, l)
+    _, _, fr, lr = _model("tiny", 64, pad_value="random")
+    _, _, fn, ln = _model("tiny", 64, pad_value=np.nan)
+    assert np.array_equal(lr, l) and np.array_equal(ln, l)
+    assert np.array_equal(oracle.score(d, w, fr, lr), s0)
+    assert np.array_equal(oracle.score(d, w, fn, ln), s0)
+    # appending a masked token: a longer max_len with the extra slot padded
+    d2 = d.replace(max_len=d.max_len + 1)
+    f2 = np.concatenate([f, np.full((f.shape[0], 1, f.shape[2]), 7.0, np.float32)], axis=1)
+    assert np.array_equal(oracle.score(d2, w, f2, l), s0)
+
+
+def test_permutation_and_batch_invariance(oracle):
+    d, w, f, l = _model("tiny", 50)
+    s = oracle.score(d, w, f, l)
+    perm = np.random.default_rng(5).permutation(50)
+    assert np.array_equal(oracle.score(d, w, f[perm], l[perm]), s[perm])
+    assert np.array_equal(oracle.score(d, w, f[:7], l[:7]), s[:7])
+    assert np.array_equal(oracle.score(d, w, f[30:], l[30:], nthreads=1), s[30:])
+
+
+def test_all_zero_features_constant(oracle):
+    """all-zero features give a deterministic constant (per length)."""
+    d, w, _, _ = _model("tiny", 2)
+    f = np.zeros((6, d.max_len, d.d_in), np.float32)
+    l = np.array([5, 5, 5, 9, 9, 9], np.int32)
+    s = oracle.score(d, w, f, l)
+    assert s[0] == s[1] == s[2] and s[3] == s[4] == s[5] and np.isfinite(s).all()
+
+
+def test_invalid_length_is_nan(oracle):
+    d, w, f, l = _model("tiny", 4)
+    l = l.copy()
+    l[1] = 0
+    l[2] = d.max_len + 1
+    s = oracle.score(d, w, f, l)
+    assert np.isnan(s[1]) and np.isnan(s[2]) and np.isfinite(s[0]) and np.isfinite(s[3])
+
+
+# ----------------------------------------------------------------------------- MC dropout
+def test_philox_known_answers(oracle):
+    for line in open(os.path.join(GOLDEN, "philox4x32_10_kat.txt")):
+        if line.startswith("#") or not line.strip():
+            continue
+        v = [int(t, 16) for t in line.split()]
+        assert list(oracle.philox4x32_10(v[0:4], v[4:6])) == v[6:10]
+
+
+def test_mc_p0_equals_score_exactly(oracle):
+    d, w, f, l = _model("tiny", 16)
+    s = oracle.score(d, w, f, l)
+    m, v = oracle.score_mc(d.replace(dropout_p=0.0), w, f, l, n_passes=3, seed=7)
+    assert np.array_equal(m, s) and np.all(v == 0.0)
+    m1, v1 = oracle.score_mc(d, w, f, l, n_passes=1, seed=7)
+    assert np.all(v1 == 0.0) and not np.array_equal(m1, s)
+
+
+def test_mc_keep_rate_and_determinism(oracle):
+    """Empirical keep rate of the R17 mask within 4 sigma of 1 - p; shard-independent keys."""
+    p = 0.1
+    thr = int(math.floor(p * 2 ** 32))
+    n_units, kept = 0, 0
+    for gidx in range(20):
+        for unit in range(0, 64, 4):
+            wds = oracle.philox4x32_10([unit >> 2, (3 << 2) | 1, 2, gidx], [7, 0])
+            kept += int((wds >= thr).sum())
+            n_units += 4
+    sigma = math.sqrt(n_units * p * (1 - p))
+    assert abs(kept - n_units * (1 - p)) <= 4 * sigma
+    d, w, f, l = _model("tiny", 12)
+    m, v = oracle.score_mc(d, w, f, l, n_passes=4, seed=11, index_base=100)
+    m2, v2 = oracle.score_mc(d, w, f[6:], l[6:], n_passes=4, seed=11, index_base=106)
+    assert np.array_equal(m[6:], m2) and np.array_equal(v[6:], v2)
+    assert np.all(v > 0)
+
+
+# ----------------------------------------------------------------------------- top-k
+def test_topk_against_lexsort(oracle):
+    rng = np.random.default_rng(6)
+    s = rng.standard_normal(300).astype(np.float32)
+    s[10] = s[20] = s[30] = s.max()              # ties -> index ascending
+    s[40] = np.nan                               # NaN -> -inf
+    for k in (1, 5, 64, 300, 310):
+        idx, top = oracle.topk(s, k, index_base=1000)
+        key = np.where(np.isnan(s), -np.inf, s)
+        order = np.lexsort((np.arange(300), -key))[:min(k, 300)]
+        assert np.array_equal(idx[:len(order)], order + 1000)
+        assert np.array_equal(top[:len(order)], key[order])
+        if k > 300:
+            assert np.all(idx[300:] == -1) and np.all(np.isneginf(top[300:]))
+
+
+def test_topk_of_shard_topks_is_global(oracle):
+    rng = np.random.default_rng(7)
+    s = np.round(rng.standard_normal(1000), 2)   # many ties
+    k = 37
+    gi, gt = oracle.topk(s, k)
+    parts = []
+    for lo in range(0, 1000, 250):
+        li, lt = oracle.topk(s[lo:lo + 250], k, index_base=lo)
+        parts.append((li, lt))
+    cat_i = np.concatenate([p[0] for p in parts])
+    cat_t = np.concatenate([p[1] for p in parts])
+    order = np.lexsort((cat_i, -cat_t))[:k]
+    assert np.array_equal(cat_i[order], gi) and np.array_equal(cat_t[order], gt)
