@@ -1,0 +1,184 @@
+/*
+ * tcl.h -- C ABI of libtcl.so, the B200 (sm_100a) batched scorer of TCL's Mamba cost model.
+ *
+ * The operation (§3.2): an auto-tuning round proposes candidate tensor
+ * programs; the cost model predicts each one's performance and the best K are selected for
+ * measurement on the hardware.  Each candidate is a sequence of schedule-primitive feature
+ * vectors, L x D with D = 22 on CPU targets (§5.1), padded at the tail to
+ * `max_len`, plus its real length T.  The model is the Mamba-based cost
+ * model of PAPER.md §5.2 (lines 429-451, Fig. 5): encoder (3 linears) -> norm -> Mamba
+ * block(s) -> norm -> masked mean over the T real tokens -> decoder (3 linears) -> one score.
+ * Higher score = better predicted performance.  The readings where the
+ * paper is silent are listed in DESIGN.md §3 (R1-R20).
+ *
+ * Conventions
+ *   - Every function returns tcl_status (0 = TCL_OK); nothing throws across the ABI.
+ *   - "_dev" pointers are CUDA device pointers on the model's device; "_host" pointers are host
+ *     memory (pinned or pageable).  The caller owns every pointer it passes in.
+ *   - Compute calls enqueue work on `stream` (a cudaStream_t passed as void*; NULL = legacy
+ *     default stream) and return after host-side validation; outputs are valid once the stream
+ *     has synchronised.  The *_host variants synchronise before returning.
+ *   - Host-detectable errors return immediately (TCL_EINVAL, TCL_ESHAPE); a per-thread message
+ *     is available from tcl_last_error().
+ *   - Device-detected errors are sticky: a candidate length outside [1, max_len] produces a NaN
+ *     score for that candidate, sets a device flag, and is reported as TCL_ELEN by
+ *     tcl_sync_error() (or by the next *_host call).
+ *   - Padded slots (t >= T_i) are ignored whatever they contain, including NaN/Inf.
+ *   - A model is not thread-safe: one host thread (one stream) per model at a time.  Create one
+ *     model per stream for concurrent scoring (weights are only ~4 MB).
+ */
+#ifndef TCL_H_
+#define TCL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    TCL_OK = 0,
+    TCL_EINVAL = -1, /* null pointer, n < 0, k <= 0, n_passes < 1, dropout_p not in [0,1) ...  */
+    TCL_ESHAPE = -2, /* inconsistent dims (e.g. enc_dims[2] != d_model), unsupported size      */
+    TCL_ELEN = -3,   /* a candidate length outside [1, max_len] was seen on the device          */
+    TCL_ECUDA = -4,  /* CUDA runtime/driver error                                               */
+    TCL_ENOMEM = -5, /* device allocation failed                                                */
+    TCL_ENCCL = -6,  /* NCCL error                                                              */
+    TCL_ESTATE = -7  /* call out of order (e.g. tcl_topk_global before tcl_comm_init)           */
+} tcl_status;
+
+/* Arithmetic of the projections (in_proj, out_proj, encoder linears 2-3).
+ *   FP32:      every GEMM in fp32 on the CUDA cores (FFMA); score within 1e-4*max(1,|ref|).
+ *   BF16_PROJ: bf16 operands on the tcgen05 tensor cores with fp32 accumulation (TMEM);
+ *              residual stream, norms, conv, scan and head stay fp32; within 2e-2*max(1,|ref|). */
+typedef enum { TCL_PREC_FP32 = 0, TCL_PREC_BF16_PROJ = 1 } tcl_precision;
+
+/* Discretisation of B ("a discretization method", reading R5):
+ *   ZOH:     Abar = exp(Delta*A), Bbar = (exp(Delta*A) - 1)/A * B   (default)
+ *   EULER_B: Abar = exp(Delta*A), Bbar = Delta*B                      (Mamba's reference code) */
+typedef enum { TCL_DISC_ZOH = 0, TCL_DISC_EULER_B = 1 } tcl_disc;
+
+/* Model dimensions.  Paper model ([n_layer,d_state,expand,d_conv] = [1,8,1,4], PAPER.md:586;
+ * encoder 64,128,128 / decoder 64,32,1) is d_model = 128, enc_dims = {64,128,128},
+ * dec_dims = {64,32,1}, dt_rank = 8, d_in = 22.
+ * Supported by this build: d_in <= 32; d_model, enc_dims in {multiples of 32} <= 256;
+ * d_inner = expand*d_model <= 512 (multiple of 32); d_state in {8, 16}; dt_rank <= 32;
+ * d_conv <= 8; dec_dims[0] <= 256, dec_dims[1] <= 256, dec_dims[2] == 1; max_len <= 256. */
+typedef struct {
+    int32_t d_in;        /* feature width D per token (22 on CPU targets)          */
+    int32_t max_len;     /* L: padded sequence length of the feature tensor                       */
+    int32_t d_model;     /* residual width                                                        */
+    int32_t n_layer;     /* number of Mamba blocks (pre-norm residual, reading R3)                */
+    int32_t d_state;     /* N: SSM state size per channel                          */
+    int32_t d_conv;      /* depthwise causal conv width                            */
+    int32_t expand;      /* d_inner = expand * d_model                              */
+    int32_t dt_rank;     /* R: rank of the Delta projection (reading R7: ceil(d_model/16))         */
+    int32_t enc_dims[3]; /* encoder output widths; enc_dims[2] == d_model                         */
+    int32_t dec_dims[3]; /* decoder output widths; dec_dims[2] == 1                               */
+    float ln_eps;        /* LayerNorm epsilon (reading R2: 1e-5, biased variance)                 */
+    float dropout_p;     /* inverted-dropout rate, used only by tcl_score_mc (reading R17)        */
+    int32_t precision;   /* tcl_precision                                                          */
+    int32_t disc;        /* tcl_disc                                                               */
+} tcl_dims;
+
+typedef struct tcl_model tcl_model;
+
+/* Number of fp32 values in the canonical weight blob for `dims` (0 if dims are invalid).
+ * Blob order (fp32 little-endian, PyTorch [out][in] row-major):
+ *   enc: W1[e1][d_in] b1[e1] W2[e2][e1] b2[e2] W3[dm][e2] b3[dm]
+ *   per layer: ln_w[dm] ln_b[dm] W_in[2di][dm] (rows 0..di-1 -> x, di.. -> z)
+ *              w_conv[di][d_conv] (tap d_conv-1 = current token) b_conv[di]
+ *              W_x[R+2N][di] (rows: dt_r, then B, then C) W_dt[di][R] b_dt[di]
+ *              A_log[di][N] (A = -exp(A_log), reading R8) Dv[di] W_out[dm][di]
+ *   lnf_w[dm] lnf_b[dm]
+ *   dec: W1[h1][dm] b1[h1] W2[h2][h1] b2[h2] W3[1][h2] b3[1]                               */
+size_t tcl_weights_count(const tcl_dims* dims);
+
+/* Validate dims, copy the weights to `cuda_device` (converting/pre-splitting for the chosen
+ * precision and pre-scaling A by log2(e)), allocate the workspace lazily.  The host buffer may be
+ * freed on return.  *out receives the model handle. */
+tcl_status tcl_model_create(const float* weights_host, size_t n_floats, const tcl_dims* dims,
+                            int cuda_device, tcl_model** out);
+tcl_status tcl_model_destroy(tcl_model* model);
+
+/* Optional pre-allocation of the workspace for batches of up to n_max candidates (no allocation
+ * happens in later calls with n <= n_max).  mc_passes_max is accepted for API symmetry. */
+tcl_status tcl_reserve(tcl_model* model, int64_t n_max, int32_t mc_passes_max);
+
+/* Score n candidates.
+ *   feats_dev  [n][max_len][d_in] fp32 row-major (padded slots ignored)
+ *   lens_dev   [n] int32, each in [1, max_len]
+ *   scores_dev [n] fp32 output.
+ * n == 0 is a no-op.  Scores are batch-invariant: a candidate's score does not depend on n, on
+ * its position in the batch, or on the other candidates (bit-identical). */
+tcl_status tcl_score(tcl_model* model, const float* feats_dev, const int32_t* lens_dev, int64_t n,
+                     float* scores_dev, void* stream);
+
+/* MC-dropout uncertainty (north-star addition for the RDU sampler; the paper's
+ * own uncertainty is Eqs. 2-3): n_passes forward passes with inverted dropout (rate
+ * dims.dropout_p) after the SiLU of encoder layers 1-2 and decoder layers 1-2; mask bits from
+ * Philox4x32-10 keyed by `seed`, counter (unit>>2, token<<2|site, pass, index_base+i) (reading
+ * R17).  mean_dev/var_dev [n] fp32: mean and population variance (divide by n_passes). */
+tcl_status tcl_score_mc(tcl_model* model, const float* feats_dev, const int32_t* lens_dev, int64_t n,
+                        int32_t n_passes, uint64_t seed, int64_t index_base, float* mean_dev,
+                        float* var_dev, void* stream);
+
+/* Top-k ("selects the best K"): the k largest scores under the total order
+ * (score desc, index asc), NaN treated as -inf.  idx_dev [k] int64 receives index_base + i,
+ * topscore_dev [k] fp32 the scores.  If k > n, slots >= n get idx -1 and score -inf.
+ * Requires index_base + n <= 2^32 - 1.  1 <= k <= 4096. */
+tcl_status tcl_topk(tcl_model* model, const float* scores_dev, int64_t n, int32_t k,
+                    int64_t index_base, int64_t* idx_dev, float* topscore_dev, void* stream);
+
+/* Multi-GPU (one process per GPU).  Rank 0 calls tcl_comm_unique_id, broadcasts the 128 bytes
+ * (e.g. through torch.distributed), every rank calls tcl_comm_init (collective). */
+tcl_status tcl_comm_unique_id(uint8_t id_out[128]);
+tcl_status tcl_comm_init(tcl_model* model, const uint8_t id[128], int32_t nranks, int32_t rank);
+
+/* Global top-k across ranks: local top-k of this rank's n_local scores (indices index_base + i),
+ * ncclAllGather of the k packed (score, index) keys over NVLink, merge -> the identical
+ * (idx, score)[k] on every rank.  Collective: every rank must call it with the same k. */
+tcl_status tcl_topk_global(tcl_model* model, const float* local_scores_dev, int64_t n_local,
+                           int64_t index_base, int32_t k, int64_t* idx_dev, float* topscore_dev,
+                           void* stream);
+
+/* End-to-end host variant (the call a user without device buffers makes): copies feats/lens
+ * host->device (pipelined in sub-chunks with the scoring on a second stream), scores, selects the
+ * top-k (k > 0) and copies the results device->host.  Candidate i gets index index_base + i.  If
+ * tcl_comm_init was called with nranks > 1 the top-k is the global one (tcl_topk_global, a
+ * collective: every rank must call).  Synchronises; returns TCL_ELEN if a length was invalid.
+ * idx_host/topscore_host may be NULL when k == 0. */
+tcl_status tcl_score_host(tcl_model* model, const float* feats_host, const int32_t* lens_host,
+                          int64_t n, int64_t index_base, float* scores_host, int32_t k,
+                          int64_t* idx_host, float* topscore_host, void* stream);
+
+/* Synchronise `stream`, then return (and clear) the sticky device error of the model. */
+tcl_status tcl_sync_error(tcl_model* model, void* stream);
+
+/* Number of kernels this model launched so far (instrumentation for bench.py). */
+int64_t tcl_launch_count(const tcl_model* model);
+
+/* Per-stage device-time instrumentation: when enabled, every launch is bracketed by CUDA events
+ * recorded on the launching stream.  tcl_profile_read synchronises the device, adds the elapsed
+ * times per stage kind into ms_out[TCL_PROF_NKINDS] and launch counts into launches_out, and
+ * clears the record list if reset != 0. */
+typedef enum {
+    TCL_PROF_PACK = 0, TCL_PROF_ENCODER, TCL_PROF_LAYERNORM, TCL_PROF_IN_PROJ, TCL_PROF_CONV,
+    TCL_PROF_X_PROJ, TCL_PROF_DT_PROJ, TCL_PROF_SCAN, TCL_PROF_OUT_PROJ, TCL_PROF_HEAD,
+    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_NKINDS
+} tcl_prof_kind;
+tcl_status tcl_profile_enable(tcl_model* model, int enable);
+tcl_status tcl_profile_read(tcl_model* model, double* ms_out, int64_t* launches_out, int reset);
+const char* tcl_profile_name(int kind);
+
+/* Thread-local message describing the last error returned on this thread ("" if none). */
+const char* tcl_last_error(void);
+
+/* Build information (compile target, version). */
+const char* tcl_build_info(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCL_H_ */

@@ -1,0 +1,106 @@
+// internal.h -- the model object behind the opaque tcl_model handle (host side only).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/tcl.h"
+
+#define TCL_STR_(x) #x
+#define TCL_STR(x) TCL_STR_(x)
+
+namespace tcl {
+
+constexpr int kXld = 32;  // packed feature row width (d_in <= 32, zero-padded -> 16-byte rows)
+
+struct LayerPtrs {
+    const float *ln_w, *ln_b, *W_in, *w_conv, *b_conv, *W_x, *W_dt, *b_dt, *A_log, *Dv, *W_out;
+};
+
+struct WeightPtrs {  // device pointers into the fp32 blob (canonical order, include/tcl.h)
+    const float *enc_W1, *enc_b1, *enc_W2, *enc_b2, *enc_W3, *enc_b3;
+    std::vector<LayerPtrs> layers;
+    const float *lnf_w, *lnf_b;
+    const float *dec_W1, *dec_b1, *dec_W2, *dec_b2, *dec_W3, *dec_b3;
+};
+
+struct Workspace {
+    int64_t cap_n = 0, rows = 0;
+    int32_t* cu = nullptr;        // [cap_n + 1]
+    int32_t* row_cand = nullptr;  // [rows]
+    float* X = nullptr;           // [rows][kXld]
+    float* H = nullptr;           // [rows][dm]   residual stream
+    float* A = nullptr;           // [rows][dm]   LN_l(H)
+    float* XZ = nullptr;          // [rows][2 di] in_proj output
+    float* U = nullptr;           // [rows][max(di, e1)]  conv output / encoder hidden 1
+    float* Delta = nullptr;       // [rows][max(di, e2)]  softplus(dt) / encoder hidden 2
+    float* G = nullptr;           // [rows][di]   gated scan output
+    float* DBC = nullptr;         // [rows][ldbc] x_proj output
+    float* m2 = nullptr;          // [cap_n] MC Welford M2
+    std::vector<void*> allocs;
+};
+
+tcl_status set_error(tcl_status st, const std::string& msg);
+tcl_status cuda_error(cudaError_t e, const char* where);
+
+}  // namespace tcl
+
+struct tcl_model {
+    tcl_dims dims{};
+    int device = 0;
+    int ldbc = 0;
+    float* w_dev = nullptr;
+    tcl::WeightPtrs wp{};
+    float* W1p = nullptr;   // [e1][kXld]
+    float* A2 = nullptr;    // [n_layer][di][N]  A * log2(e)
+    float* invA = nullptr;  // [n_layer][di][N]  1 / A
+    int* d_err = nullptr;
+    tcl::Workspace ws;
+    unsigned long long* topk_tmp = nullptr;
+    size_t topk_tmp_cap = 0;
+    // multi-GPU
+    void* comm = nullptr;   // ncclComm_t
+    int nranks = 1, rank = 0;
+    unsigned long long* keys_send = nullptr;  // [4096]
+    unsigned long long* keys_recv = nullptr;  // [nranks * 4096]
+    // end-to-end host path staging
+    int64_t stage_cap = 0;
+    float* stage_feats = nullptr;
+    int32_t* stage_lens = nullptr;
+    float* stage_scores = nullptr;
+    int64_t* stage_idx = nullptr;
+    float* stage_top = nullptr;
+    cudaStream_t copy_stream = nullptr;
+    std::vector<cudaEvent_t> chunk_events;
+    int64_t launches = 0;
+    // per-stage instrumentation (tcl_profile_enable)
+    int prof_on = 0;
+    struct ProfRec { int kind; cudaEvent_t a, b; };
+    std::vector<ProfRec> prof_recs;
+    std::vector<cudaEvent_t> prof_pool;
+    double prof_ms[TCL_PROF_NKINDS] = {};
+    int64_t prof_n[TCL_PROF_NKINDS] = {};
+};
+
+namespace tcl {
+void comm_destroy(tcl_model* m);
+
+// Brackets the launches issued in its scope with CUDA events when profiling is on.
+struct ProfScope {
+    tcl_model* m; int kind; cudaStream_t s; cudaEvent_t a = nullptr;
+    static cudaEvent_t get(tcl_model* m) {
+        if (!m->prof_pool.empty()) { cudaEvent_t e = m->prof_pool.back(); m->prof_pool.pop_back(); return e; }
+        cudaEvent_t e; cudaEventCreate(&e); return e;
+    }
+    ProfScope(tcl_model* m_, int k, cudaStream_t s_) : m(m_), kind(k), s(s_) {
+        if (m->prof_on) { a = get(m); cudaEventRecord(a, s); }
+    }
+    ~ProfScope() {
+        if (!a) return;
+        cudaEvent_t b = get(m);
+        cudaEventRecord(b, s);
+        m->prof_recs.push_back({kind, a, b});
+    }
+};
+}

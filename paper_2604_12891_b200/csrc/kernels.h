@@ -1,0 +1,95 @@
+// kernels.h -- internal launchers of libtcl (not part of the C ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace tcl {
+
+// Device error bits (sticky, tcl_sync_error).
+enum : int { ERR_LEN = 1 };
+
+// ---- pack ------------------------------------------------------------------
+// cu[n+1] exclusive prefix of the valid lengths (invalid lengths count as 0 rows and raise
+// ERR_LEN); cu[n] = P.  n <= 1<<20 per launch.
+void launch_lens_prefix(const int32_t* lens, int64_t n, int32_t max_len, int32_t* cu, int* err,
+                        cudaStream_t s);
+// Gather the real rows of feats [n][L][d_in] into X [P][ldx] (columns d_in..ldx-1 zeroed) and
+// write row_cand[P].  If x_bf16 != nullptr, also writes a bf16 copy [P][ldx].
+void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int64_t n, int L,
+                 int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s);
+
+// ---- SIMT fp32 GEMM with fused epilogues ------------------------------------------------------
+enum Epi : int { EPI_NONE = 0, EPI_SILU = 1, EPI_SOFTPLUS = 2, EPI_RESID = 3 };
+struct GemmArgs {
+    const float* X; int ldx;        // [M][K]
+    const float* W; int ldw;        // [N][K] (PyTorch [out][in])
+    const float* bias;              // [N] or nullptr
+    float* Y; int ldy;              // [M][N]
+    int K, N;
+    int max_rows;                   // grid extent (rows)
+    const int32_t* p_rows;          // device: actual row count (cu[n]); rows >= *p_rows skipped
+    int epi;
+    // dropout (EPI_SILU only): per-row candidate and token
+    DropoutCtx drop; int site;
+    const int32_t* row_cand; const int32_t* cu;
+};
+void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
+
+// ---- LayerNorm rows (fp32 in, fp32 out and/or bf16 out) ---------------------------------------
+void launch_layernorm(const float* H, int ldh, int dm, const float* g, const float* b, float eps,
+                      float* Y, void* Ybf16, int ldy, int max_rows, const int32_t* p_rows,
+                      cudaStream_t s);
+
+// ---- causal depthwise conv + SiLU (a5) --------------------------------------------------------
+// X [P][ldx] (x part = first di columns) -> U [P][di]
+void launch_conv_silu(const float* X, int ldx, const float* w, const float* b, int di, int dc,
+                      float* U, const int32_t* row_cand, const int32_t* cu, int max_rows,
+                      const int32_t* p_rows, cudaStream_t s);
+
+// ---- selective scan + D skip + gate (a7) ------------------------------------------------------
+struct ScanArgs {
+    const float* U;      // [P][di]
+    const float* Delta;  // [P][di]
+    const float* Z; int ldz;  // z at Z[row*ldz + d]
+    const float* BC; int ldbc; int b_off, c_off;  // B at BC[row*ldbc + b_off + n]
+    const float* A2;     // [di][N]  A * log2(e)
+    const float* invA;   // [di][N]  1 / A
+    const float* Dv;     // [di]
+    float* G;            // [P][di]  y * SiLU(z)
+    const int32_t* cu; const int32_t* lens;
+    int64_t n; int di, N, disc, accurate, max_len;
+};
+void launch_scan(const ScanArgs& a, cudaStream_t s);
+
+// ---- head: LN_f, masked mean, decoder (a9) ----------------------------------------------------
+struct HeadArgs {
+    const float* H; int ldh; int dm;
+    const float* lnf_w; const float* lnf_b; float eps;
+    const float* W1; const float* b1; int h1;
+    const float* W2; const float* b2; int h2;
+    const float* W3; const float* b3;
+    const int32_t* cu; const int32_t* lens; int max_len;
+    int64_t n;
+    float* scores;
+    DropoutCtx drop;
+    // MC accumulation (Welford) when mean != nullptr: pass index = drop.pass
+    float* mean; float* m2;
+};
+void launch_head(const HeadArgs& a, cudaStream_t s);
+void launch_mc_finalize(const float* m2, int64_t n, int passes, float* var, cudaStream_t s);
+
+// ---- top-k ------------------------------------------------------------------------------------
+// Local top-k keys: k keys (descending, sentinel 0 padded) of scores[0..n) with index_base.
+// tmp must hold >= 2 * ceil(n / kTopkChunk) * k + 2 * kTopkChunk keys.
+constexpr int kTopkChunk = 8192;
+size_t topk_tmp_keys(int64_t n, int k);
+// Both return the number of kernels launched.
+int launch_topk_keys(const float* scores, int64_t n, int k, int64_t index_base,
+                     unsigned long long* out_keys, unsigned long long* tmp, cudaStream_t s);
+// Top-k of `count` keys -> decoded (idx, score) [k].  tmp: k + topk_tmp_keys(count, k) keys.
+int launch_topk_merge(const unsigned long long* keys, int64_t count, int k, int64_t* idx,
+                      float* score, unsigned long long* tmp, cudaStream_t s);
+
+}  // namespace tcl

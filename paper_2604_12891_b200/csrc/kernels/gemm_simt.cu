@@ -1,0 +1,92 @@
+// gemm_simt.cu -- fp32 CUDA-core GEMM Y = epi(X W^T + b) for the FP32 precision mode.
+//
+// Used for every linear of the fp32 path (encoder P:451, in_proj / x_proj / dt_proj / out_proj
+// of the Mamba block P:446) and for the small projections of the bf16 path.  Exact fp32
+// FFMA accumulation in a fixed k order: a row's result never depends on the other rows of the
+// tile, so scores are batch-invariant (reading R19).
+// Tile 64x64x16, 256 threads, 4x4 outputs per thread, operands staged k-major in shared memory.
+#include "../kernels.h"
+
+namespace tcl {
+
+constexpr int BM = 64, BN = 64, BK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
+    __shared__ __align__(16) float As[BK][BM + 4];
+    __shared__ __align__(16) float Ws[BK][BN + 4];
+    const int rows = *a.p_rows;
+    const int m0 = blockIdx.x * BM;
+    if (m0 >= rows) return;
+    const int n0 = blockIdx.y * BN;
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    // loader mapping: 64 rows x 16 k = 1024 floats = 256 threads x float4
+    const int lr = tid >> 2, lk = (tid & 3) * 4;
+    float acc[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+
+    for (int k0 = 0; k0 < a.K; k0 += BK) {
+        {
+            const int gm = m0 + lr, gk = k0 + lk;
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gm < rows && gk < a.K) v = *reinterpret_cast<const float4*>(a.X + (int64_t)gm * a.ldx + gk);
+            As[lk + 0][lr] = v.x; As[lk + 1][lr] = v.y; As[lk + 2][lr] = v.z; As[lk + 3][lr] = v.w;
+            const int gn = n0 + lr;
+            float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gn < a.N && gk < a.K) w = __ldg(reinterpret_cast<const float4*>(a.W + (int64_t)gn * a.ldw + gk));
+            Ws[lk + 0][lr] = w.x; Ws[lk + 1][lr] = w.y; Ws[lk + 2][lr] = w.z; Ws[lk + 3][lr] = w.w;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < BK; ++kk) {
+            float4 av = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+            float4 wv = *reinterpret_cast<const float4*>(&Ws[kk][tx * 4]);
+            float ar[4] = {av.x, av.y, av.z, av.w}, wr[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(ar[i], wr[j], acc[i][j]);
+        }
+        __syncthreads();
+    }
+
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int gm = m0 + ty * 4 + i;
+        if (gm >= rows) continue;
+        int cand = 0, token = 0;
+        if (a.epi == EPI_SILU && a.drop.enabled) {
+            cand = a.row_cand[gm];
+            token = gm - a.cu[cand];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int gn = n0 + tx * 4 + j;
+            if (gn >= a.N) continue;
+            float v = acc[i][j] + (a.bias ? __ldg(a.bias + gn) : 0.0f);
+            float* dst = a.Y + (int64_t)gm * a.ldy + gn;
+            switch (a.epi) {
+                case EPI_SILU:
+                    v = silu(v);
+                    if (a.drop.enabled)
+                        v = dropout_keep(a.drop, gn, token, a.site, cand) ? v * a.drop.scale : 0.0f;
+                    break;
+                case EPI_SOFTPLUS: v = softplus(v); break;
+                case EPI_RESID: v = *dst + v; break;
+                default: break;
+            }
+            *dst = v;
+        }
+    }
+}
+
+void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
+    if (a.max_rows <= 0) return;
+    dim3 grid((a.max_rows + BM - 1) / BM, (a.N + BN - 1) / BN);
+    k_gemm_simt<<<grid, 256, 0, s>>>(a);
+}
+
+}  // namespace tcl

@@ -1,0 +1,126 @@
+// mixer.cu -- the Mamba mixer's sequence ops on the fp32 path:
+//   causal depthwise conv1d + SiLU (reading R4) and the selective scan with ZOH
+//   discretisation, D skip and SiLU(z) gate (Eqs. 4-5; readings R5, R6).
+#include "../kernels.h"
+
+namespace tcl {
+
+// u[t][d] = SiLU(b[d] + sum_{k<dc} w[d][k] * x[t-(dc-1)+k][d]),  x[t'<0] = 0 within a candidate.
+__global__ void __launch_bounds__(256) k_conv_silu(const float* __restrict__ X, int ldx,
+                                                   const float* __restrict__ w,
+                                                   const float* __restrict__ b, int di, int dc,
+                                                   float* __restrict__ U,
+                                                   const int32_t* __restrict__ row_cand,
+                                                   const int32_t* __restrict__ cu,
+                                                   const int32_t* __restrict__ p_rows) {
+    const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t row = idx / di;
+    const int d = (int)(idx - row * di);
+    if (row >= *p_rows) return;
+    const int t = (int)(row - cu[row_cand[row]]);
+    float acc = __ldg(b + d);
+    for (int k = 0; k < dc; ++k) {
+        const int back = dc - 1 - k;
+        if (t >= back) acc = fmaf(__ldg(w + d * dc + k), X[(row - back) * ldx + d], acc);
+    }
+    U[row * di + d] = silu(acc);
+}
+
+void launch_conv_silu(const float* X, int ldx, const float* w, const float* b, int di, int dc,
+                      float* U, const int32_t* row_cand, const int32_t* cu, int max_rows,
+                      const int32_t* p_rows, cudaStream_t s) {
+    int64_t total = (int64_t)max_rows * di;
+    if (total == 0) return;
+    k_conv_silu<<<(unsigned)((total + 255) / 256), 256, 0, s>>>(X, ldx, w, b, di, dc, U, row_cand, cu,
+                                                                p_rows);
+}
+
+// Accurate e^x - 1 for the fp32 path: series where Ab - 1 would cancel.  x2 = x * log2(e).
+__device__ __forceinline__ float expm1_from(float x2, float Ab) {
+    if (fabsf(x2) < 0.25f) {
+        const float x = x2 * kLn2;
+        return x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720, 1.0f / 120), 1.0f / 24),
+                                          1.0f / 6), 0.5f), 1.0f);
+    }
+    return Ab - 1.0f;
+}
+
+// One thread per (candidate, channel d); the N states live in registers across t < T_i.
+// B_t, C_t of the candidate are staged in shared memory (broadcast to all channels).
+template <int N, bool ACC, int DISC>
+__global__ void __launch_bounds__(128) k_scan(ScanArgs a) {
+    extern __shared__ float sBC[];  // [T][2N]
+    const int64_t i = blockIdx.x;
+    const int d = blockIdx.y * blockDim.x + threadIdx.x;
+    const int T = a.lens[i];
+    if (T < 1 || T > a.max_len) return;
+    const int64_t base = a.cu[i];
+    for (int idx = threadIdx.x; idx < T * 2 * N; idx += blockDim.x) {
+        const int t = idx / (2 * N), j = idx - t * 2 * N;
+        sBC[idx] = a.BC[(base + t) * a.ldbc + (j < N ? a.b_off + j : a.c_off + j - N)];
+    }
+    __syncthreads();
+    if (d >= a.di) return;
+    float A2[N], iA[N], s[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        A2[n] = __ldg(a.A2 + d * N + n);
+        iA[n] = __ldg(a.invA + d * N + n);
+        s[n] = 0.0f;
+    }
+    const float Dv = __ldg(a.Dv + d);
+    for (int t = 0; t < T; ++t) {
+        const int64_t row = base + t;
+        const float u = a.U[row * a.di + d];
+        const float dl = a.Delta[row * a.di + d];
+        const float z = a.Z[row * a.ldz + d];
+        const float* Bt = sBC + t * 2 * N;
+        const float* Ct = Bt + N;
+        float y = 0.0f;
+        if (DISC == 1) {  // Euler-B: Bbar = Delta * B
+            const float du = dl * u;
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                const float Ab = ex2(dl * A2[n]);
+                s[n] = fmaf(Ab, s[n], du * Bt[n]);
+                y = fmaf(Ct[n], s[n], y);
+            }
+        } else {          // ZOH: Bbar = (Ab - 1) / A * B
+#pragma unroll
+            for (int n = 0; n < N; ++n) {
+                const float x2 = dl * A2[n];
+                const float Ab = ex2(x2);
+                const float v = (Bt[n] * u) * iA[n];
+                if (ACC) {
+                    s[n] = fmaf(Ab, s[n], expm1_from(x2, Ab) * v);
+                } else {
+                    s[n] = fmaf(Ab, s[n] + v, -v);
+                }
+                y = fmaf(Ct[n], s[n], y);
+            }
+        }
+        y = fmaf(Dv, u, y);
+        a.G[row * a.di + d] = y * silu(z);
+    }
+}
+
+template <int N>
+static void scan_dispatch(const ScanArgs& a, cudaStream_t s) {
+    const int bx = a.di < 128 ? a.di : 128;
+    dim3 grid((unsigned)a.n, (a.di + bx - 1) / bx);
+    size_t smem = (size_t)a.max_len * 2 * N * sizeof(float);
+    if (a.disc == 1)
+        k_scan<N, false, 1><<<grid, bx, smem, s>>>(a);
+    else if (a.accurate)
+        k_scan<N, true, 0><<<grid, bx, smem, s>>>(a);
+    else
+        k_scan<N, false, 0><<<grid, bx, smem, s>>>(a);
+}
+
+void launch_scan(const ScanArgs& a, cudaStream_t s) {
+    if (a.n == 0) return;
+    if (a.N == 8) scan_dispatch<8>(a, s);
+    else if (a.N == 16) scan_dispatch<16>(a, s);
+}
+
+}  // namespace tcl

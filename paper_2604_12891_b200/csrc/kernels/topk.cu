@@ -1,0 +1,124 @@
+// topk.cu -- SURVEY §8(a) a11: "selects the best K".
+//
+// Total order (score desc, index asc) with NaN -> -inf (reading R15) is encoded in one uint64 key:
+//   key = orderable_u32(score) << 32 | (0xFFFFFFFF - global_index)
+// so the k largest keys are exactly the top-k.  Key 0 never encodes a real candidate (the
+// smallest real high word is orderable(-inf) = 0x007FFFFF) and is used as the padding sentinel.
+// Selection is a tournament: each CTA bitonic-sorts a chunk of 8192 keys in shared memory and
+// keeps its best k; rounds repeat until one chunk remains.  Integer-only -> bit-exact.
+#include <math.h>
+
+#include "../kernels.h"
+
+namespace tcl {
+
+typedef unsigned long long u64;
+
+__device__ __forceinline__ u64 make_key(float f, uint32_t gidx) {
+    if (isnan(f)) f = -INFINITY;
+    if (f == 0.0f) f = 0.0f;  // -0 == +0 in the score order
+    uint32_t b = __float_as_uint(f);
+    uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return ((u64)ord << 32) | (u64)(0xFFFFFFFFu - gidx);
+}
+
+template <bool FROM_SCORES>
+__global__ void __launch_bounds__(1024) k_topk_chunk(const float* __restrict__ scores,
+                                                     const u64* __restrict__ keys_in, int64_t count,
+                                                     int64_t index_base, int k, u64* __restrict__ out) {
+    extern __shared__ u64 sk[];
+    constexpr int C = kTopkChunk;
+    const int64_t lo = (int64_t)blockIdx.x * C;
+    const int64_t m = min((int64_t)C, count - lo);
+    for (int j = threadIdx.x; j < C; j += blockDim.x) {
+        u64 v = 0;
+        if (j < m) v = FROM_SCORES ? make_key(scores[lo + j], (uint32_t)(index_base + lo + j)) : keys_in[lo + j];
+        sk[j] = v;
+    }
+    __syncthreads();
+    for (int size = 2; size <= C; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int j = threadIdx.x; j < C / 2; j += blockDim.x) {
+                const int a = 2 * stride * (j / stride) + (j % stride);
+                const int b = a + stride;
+                const bool desc = (a & size) == 0;
+                const u64 x = sk[a], y = sk[b];
+                if ((x < y) == desc) { sk[a] = y; sk[b] = x; }
+            }
+            __syncthreads();
+        }
+    }
+    for (int j = threadIdx.x; j < k; j += blockDim.x) out[(int64_t)blockIdx.x * k + j] = sk[j];
+}
+
+__global__ void k_topk_decode(const u64* __restrict__ keys, int k, int64_t* __restrict__ idx,
+                              float* __restrict__ score) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    const u64 key = keys[j];
+    if (key == 0) { idx[j] = -1; score[j] = -INFINITY; return; }
+    const uint32_t ord = (uint32_t)(key >> 32);
+    const uint32_t b = (ord & 0x80000000u) ? (ord & 0x7FFFFFFFu) : ~ord;
+    idx[j] = (int64_t)(0xFFFFFFFFu - (uint32_t)key);
+    score[j] = __uint_as_float(b);
+}
+
+size_t topk_tmp_keys(int64_t n, int k) {
+    const int64_t blocks = (n + kTopkChunk - 1) / kTopkChunk;
+    return (size_t)(2 * blocks * k + 2 * kTopkChunk);
+}
+
+static void set_smem_once() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(k_topk_chunk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTopkChunk * (int)sizeof(u64));
+    cudaFuncSetAttribute(k_topk_chunk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kTopkChunk * (int)sizeof(u64));
+    done = true;
+}
+
+// Rounds of the tournament; writes exactly k keys (descending, 0-padded) to `out`.
+static int tournament(const float* scores, const u64* keys, int64_t count, int k,
+                      int64_t index_base, u64* out, u64* tmp, cudaStream_t s) {
+    int launched = 0;
+    set_smem_once();
+    const size_t smem = kTopkChunk * sizeof(u64);
+    const int64_t blocks0 = (count + kTopkChunk - 1) / kTopkChunk;
+    u64* buf[2] = {tmp, tmp + blocks0 * k + kTopkChunk};
+    int which = 0;
+    const u64* src = keys;
+    bool from_scores = scores != nullptr;
+    int64_t cur = count;
+    for (;;) {
+        int64_t blocks = (cur + kTopkChunk - 1) / kTopkChunk;
+        if (blocks < 1) blocks = 1;
+        u64* dst = blocks == 1 ? out : buf[which];
+        if (from_scores)
+            k_topk_chunk<true><<<(unsigned)blocks, 1024, smem, s>>>(scores, nullptr, cur, index_base, k, dst);
+        else
+            k_topk_chunk<false><<<(unsigned)blocks, 1024, smem, s>>>(nullptr, src, cur, 0, k, dst);
+        ++launched;
+        if (blocks == 1) break;
+        cur = blocks * k;
+        src = dst;
+        which ^= 1;
+        from_scores = false;
+    }
+    return launched;
+}
+
+int launch_topk_keys(const float* scores, int64_t n, int k, int64_t index_base, u64* out_keys,
+                     u64* tmp, cudaStream_t s) {
+    return tournament(scores, nullptr, n, k, index_base, out_keys, tmp, s);
+}
+
+int launch_topk_merge(const u64* keys, int64_t count, int k, int64_t* idx, float* score, u64* tmp,
+                      cudaStream_t s) {
+    u64* fin = tmp;  // k keys, then the tournament scratch
+    int launched = tournament(nullptr, keys, count, k, 0, fin, tmp + k, s);
+    k_topk_decode<<<(k + 255) / 256, 256, 0, s>>>(fin, k, idx, score);
+    return launched + 1;
+}
+
+}  // namespace tcl

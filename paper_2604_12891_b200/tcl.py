@@ -1,0 +1,214 @@
+"""Thin ctypes binding of libtcl.so (include/tcl.h).  Argument marshalling only.
+
+Every step of the scoring path runs in libtcl's CUDA kernels; this module converts torch
+tensors / numpy arrays into pointers and status codes into exceptions.  There is no CPU
+fallback: if libtcl.so is missing or no CUDA device is present the calls raise.
+PyTorch is used only for device memory, streams and (in bench.py) process groups.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import Optional, Tuple
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libtcl.so")
+
+STATUS = {0: "TCL_OK", -1: "TCL_EINVAL", -2: "TCL_ESHAPE", -3: "TCL_ELEN", -4: "TCL_ECUDA",
+          -5: "TCL_ENOMEM", -6: "TCL_ENCCL", -7: "TCL_ESTATE"}
+TCL_PREC_FP32, TCL_PREC_BF16_PROJ = 0, 1
+TCL_DISC_ZOH, TCL_DISC_EULER_B = 0, 1
+
+
+class TclError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class tcl_dims(ctypes.Structure):
+    _fields_ = [("d_in", ctypes.c_int32), ("max_len", ctypes.c_int32), ("d_model", ctypes.c_int32),
+                ("n_layer", ctypes.c_int32), ("d_state", ctypes.c_int32), ("d_conv", ctypes.c_int32),
+                ("expand", ctypes.c_int32), ("dt_rank", ctypes.c_int32),
+                ("enc_dims", ctypes.c_int32 * 3), ("dec_dims", ctypes.c_int32 * 3),
+                ("ln_eps", ctypes.c_float), ("dropout_p", ctypes.c_float),
+                ("precision", ctypes.c_int32), ("disc", ctypes.c_int32)]
+
+    @classmethod
+    def of(cls, d) -> "tcl_dims":
+        return cls(d.d_in, d.max_len, d.d_model, d.n_layer, d.d_state, d.d_conv, d.expand, d.dt_rank,
+                   (ctypes.c_int32 * 3)(*d.enc_dims), (ctypes.c_int32 * 3)(*d.dec_dims),
+                   d.ln_eps, d.dropout_p, d.precision, d.disc)
+
+
+EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score",
+           "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
+           "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
+           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name"]
+PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
+              "head", "topk", "mixer", "allgather", "mc"]
+
+_lib: Optional[ctypes.CDLL] = None
+
+
+def load(path: str = LIB_PATH) -> ctypes.CDLL:
+    """Load libtcl.so (import torch first so its NCCL is the one the library binds to)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} is missing: build it with `python -m paper_2604_12891_b200.build` "
+                           "(there is no CPU fallback)")
+    try:
+        import torch  # noqa: F401  (loads libnccl.so.2 / the CUDA driver first)
+    except Exception:
+        pass
+    L = ctypes.CDLL(path)
+    P, vp = ctypes.POINTER, ctypes.c_void_p
+    i32, i64, u64, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_size_t
+    L.tcl_weights_count.restype = sz
+    L.tcl_weights_count.argtypes = [P(tcl_dims)]
+    L.tcl_model_create.argtypes = [vp, sz, P(tcl_dims), ctypes.c_int, P(vp)]
+    L.tcl_model_destroy.argtypes = [vp]
+    L.tcl_reserve.argtypes = [vp, i64, i32]
+    L.tcl_score.argtypes = [vp, vp, vp, i64, vp, vp]
+    L.tcl_score_mc.argtypes = [vp, vp, vp, i64, i32, u64, i64, vp, vp, vp]
+    L.tcl_topk.argtypes = [vp, vp, i64, i32, i64, vp, vp, vp]
+    L.tcl_comm_unique_id.argtypes = [vp]
+    L.tcl_comm_init.argtypes = [vp, vp, i32, i32]
+    L.tcl_topk_global.argtypes = [vp, vp, i64, i64, i32, vp, vp, vp]
+    L.tcl_score_host.argtypes = [vp, vp, vp, i64, i64, vp, i32, vp, vp, vp]
+    L.tcl_sync_error.argtypes = [vp, vp]
+    L.tcl_launch_count.restype = i64
+    L.tcl_launch_count.argtypes = [vp]
+    L.tcl_last_error.restype = ctypes.c_char_p
+    L.tcl_last_error.argtypes = []
+    L.tcl_build_info.restype = ctypes.c_char_p
+    L.tcl_build_info.argtypes = []
+    L.tcl_profile_enable.argtypes = [vp, ctypes.c_int]
+    L.tcl_profile_read.argtypes = [vp, P(ctypes.c_double), P(i64), ctypes.c_int]
+    L.tcl_profile_name.restype = ctypes.c_char_p
+    L.tcl_profile_name.argtypes = [ctypes.c_int]
+    for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
+               "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
+               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read"):
+        getattr(L, fn).restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(code: int):
+    if code != 0:
+        raise TclError(code, load().tcl_last_error().decode())
+
+
+def _ptr(t) -> int:
+    """Device/host address of a torch tensor or numpy array (no copy, must be contiguous)."""
+    if isinstance(t, np.ndarray):
+        assert t.flags["C_CONTIGUOUS"]
+        return t.ctypes.data
+    assert t.is_contiguous()
+    return t.data_ptr()
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        import torch
+        return torch.cuda.current_stream().cuda_stream
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream
+
+
+def tcl_weights_count(dims) -> int:
+    return int(load().tcl_weights_count(ctypes.byref(tcl_dims.of(dims))))
+
+
+def tcl_comm_unique_id() -> bytes:
+    buf = (ctypes.c_uint8 * 128)()
+    _check(load().tcl_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Model:
+    """Owns one tcl_model handle (weights on one device + workspace)."""
+
+    def __init__(self, weights: np.ndarray, dims, device: int = 0):
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        self.dims = dims
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(load().tcl_model_create(w.ctypes.data, w.size, ctypes.byref(tcl_dims.of(dims)), device,
+                                       ctypes.byref(h)))
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            load().tcl_model_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    def reserve(self, n_max: int, mc_passes_max: int = 0):
+        _check(load().tcl_reserve(self._h, n_max, mc_passes_max))
+
+    # -- device-buffer calls (torch CUDA tensors) --------------------------------------------
+    def tcl_score(self, feats, lens, scores, stream=None):
+        n = lens.shape[0]
+        _check(load().tcl_score(self._h, _ptr(feats), _ptr(lens), n, _ptr(scores), _stream(stream)))
+
+    def tcl_score_mc(self, feats, lens, n_passes: int, seed: int, index_base: int, mean, var, stream=None):
+        n = lens.shape[0]
+        _check(load().tcl_score_mc(self._h, _ptr(feats), _ptr(lens), n, n_passes, seed, index_base,
+                                   _ptr(mean), _ptr(var), _stream(stream)))
+
+    def tcl_topk(self, scores, k: int, index_base: int, idx, top, n: Optional[int] = None, stream=None):
+        n = scores.shape[0] if n is None else n
+        _check(load().tcl_topk(self._h, _ptr(scores), n, k, index_base, _ptr(idx), _ptr(top), _stream(stream)))
+
+    def tcl_comm_init(self, uid: bytes, nranks: int, rank: int):
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
+        _check(load().tcl_comm_init(self._h, buf, nranks, rank))
+
+    def tcl_topk_global(self, scores, index_base: int, k: int, idx, top, stream=None):
+        _check(load().tcl_topk_global(self._h, _ptr(scores), scores.shape[0], index_base, k, _ptr(idx),
+                                      _ptr(top), _stream(stream)))
+
+    def tcl_sync_error(self, stream=None):
+        _check(load().tcl_sync_error(self._h, _stream(stream)))
+
+    def launch_count(self) -> int:
+        return int(load().tcl_launch_count(self._h))
+
+    def profile_enable(self, on: bool = True):
+        _check(load().tcl_profile_enable(self._h, 1 if on else 0))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{stage: (total_ms, launches)} accumulated since the last reset (synchronises)."""
+        n = len(PROF_KINDS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_int64 * n)()
+        _check(load().tcl_profile_read(self._h, ms, cnt, 1 if reset else 0))
+        return {load().tcl_profile_name(i).decode(): (ms[i], cnt[i]) for i in range(n) if cnt[i] > 0}
+
+    # -- host-buffer call (end to end) -----------------------------------------------------------
+    def tcl_score_host(self, feats: np.ndarray, lens: np.ndarray, k: int = 0, index_base: int = 0,
+                       scores: np.ndarray = None, idx: np.ndarray = None, top: np.ndarray = None,
+                       stream=None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+        n = lens.shape[0]
+        scores = np.empty(n, np.float32) if scores is None else scores
+        idx = np.empty(max(k, 1), np.int64) if idx is None else idx
+        top = np.empty(max(k, 1), np.float32) if top is None else top
+        _check(load().tcl_score_host(self._h, _ptr(feats), _ptr(lens), n, index_base, _ptr(scores), k,
+                                     _ptr(idx), _ptr(top), _stream(stream)))
+        return scores, idx[:k], top[:k]
