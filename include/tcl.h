@@ -172,6 +172,13 @@ tcl_status tcl_profile_enable(tcl_model* model, int enable);
 tcl_status tcl_profile_read(tcl_model* model, double* ms_out, int64_t* launches_out, int reset);
 const char* tcl_profile_name(int kind);
 
+/* Debugging aid (per-stage parity tests): copy the current contents of a workspace buffer, as
+ * fp32, to host memory.  name: "H" (residual stream [P][d_model]), "A" (LayerNorm output
+ * [P][d_model]), "XZ" (in_proj output [P][2 d_inner]), "G" (gated scan output [P][d_inner]),
+ * "U" (conv output, fp32 path only), "DELTA" (fp32 path only).  Rows are the packed tokens of the
+ * last chunk scored; buffers hold the values of the LAST layer that wrote them.  Synchronises. */
+tcl_status tcl_debug_read(tcl_model* model, const char* name, float* host_out, int64_t rows, int64_t cols);
+
 /* Thread-local message describing the last error returned on this thread ("" if none). */
 const char* tcl_last_error(void);
 

@@ -16,6 +16,8 @@
 #include "../../include/tcl.h"
 #include "internal.h"
 #include "kernels.h"
+#include "kernels_mixer.h"
+#include "kernels_tc.h"
 
 using namespace tcl;
 
@@ -81,9 +83,6 @@ static tcl_status validate_dims(const tcl_dims* d) {
     return TCL_OK;
 }
 
-static int round_up(int v, int m) { return (v + m - 1) / m * m; }
-
-// ------------------------------------------------------------------------------ workspace
 template <typename T>
 static tcl_status dev_alloc(T** p, size_t count) {
     if (count == 0) count = 1;
@@ -94,6 +93,102 @@ static tcl_status dev_alloc(T** p, size_t count) {
     }
     return TCL_OK;
 }
+
+static int round_up(int v, int m) { return (v + m - 1) / m * m; }
+
+static uint16_t f2bf(float f) {  // round to nearest even (weights are finite)
+    uint32_t u;
+    memcpy(&u, &f, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+
+// Upload a bf16 copy of W [rows][cols] into a zero-padded [rows_p][cols_p] device matrix.
+static tcl_status upload_bf16(tcl_model* m, const float* W, int rows, int cols, int rows_p, int cols_p,
+                              __nv_bfloat16** out) {
+    std::vector<uint16_t> h((size_t)rows_p * cols_p, 0);
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) h[(size_t)r * cols_p + c] = f2bf(W[(size_t)r * cols + c]);
+    tcl_status st = dev_alloc(out, h.size());
+    if (st != TCL_OK) return st;
+    m->bf_allocs.push_back(*out);
+    cudaError_t e = cudaMemcpy(*out, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? TCL_OK : cuda_error(e, "upload_bf16");
+}
+
+// Host offsets of the canonical blob (include/tcl.h), for the bf16 copies.
+struct HostW {
+    const float *W1, *W2, *W3;
+    std::vector<const float*> Win, Wx, Wdt, Wout;
+};
+static HostW host_offsets(const tcl_dims& d, const float* w) {
+    const int dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
+    HostW h;
+    const float* p = w;
+    h.W1 = p; p += (size_t)d.enc_dims[0] * d.d_in + d.enc_dims[0];
+    h.W2 = p; p += (size_t)d.enc_dims[1] * d.enc_dims[0] + d.enc_dims[1];
+    h.W3 = p; p += (size_t)d.enc_dims[2] * d.enc_dims[1] + d.enc_dims[2];
+    for (int l = 0; l < d.n_layer; ++l) {
+        p += 2 * dm;
+        h.Win.push_back(p); p += (size_t)2 * di * dm;
+        p += (size_t)di * d.d_conv + di;
+        h.Wx.push_back(p); p += (size_t)(R + 2 * N) * di;
+        h.Wdt.push_back(p); p += (size_t)di * R + di;
+        p += (size_t)di * N + di;
+        h.Wout.push_back(p); p += (size_t)dm * di;
+    }
+    return h;
+}
+
+static tcl_status validate_tc(const tcl_dims& d) {
+    const int dm = d.d_model, di = d.expand * d.d_model;
+    auto bad = [](const char* msg) { return set_error(TCL_ESHAPE, msg); };
+    if (dm != 64 && dm != 128 && dm != 256) return bad("bf16 path: d_model must be 64, 128 or 256");
+    if (di != 64 && di != 128 && di != 256) return bad("bf16 path: d_inner must be 64, 128 or 256");
+    for (int i = 0; i < 2; ++i)
+        if (d.enc_dims[i] > 256) return bad("bf16 path: enc_dims[0..1] must be <= 256");
+    if (d.dt_rank > 32) return bad("bf16 path: dt_rank must be <= 32");
+    if (d.d_conv < 2 || d.d_conv > 4) return bad("bf16 path: d_conv must be in [2, 4]");
+    if (round_up(d.dt_rank + 2 * d.d_state, 8) > 64) return bad("bf16 path: dt_rank + 2 d_state must be <= 64");
+    return TCL_OK;
+}
+
+static tcl_status setup_tc(tcl_model* m, const float* wh) {
+    const tcl_dims& d = m->dims;
+    tcl_status st = validate_tc(d);
+    if (st != TCL_OK) return st;
+    const int dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+    m->use_tc = 1;
+    cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
+    m->nxp = round_up(R + 2 * N, 8);
+    m->rp = R <= 16 ? 16 : 32;
+    m->bn_in = std::min(256, 2 * di);
+    HostW h = host_offsets(d, wh);
+    if ((st = upload_bf16(m, h.W1, e1, d.d_in, e1, kXld, &m->W1b)) != TCL_OK) return st;
+    if ((st = upload_bf16(m, h.W2, e2, e1, e2, e1, &m->W2b)) != TCL_OK) return st;
+    if ((st = upload_bf16(m, h.W3, dm, e2, dm, e2, &m->W3b)) != TCL_OK) return st;
+    bool ok = make_tmap_bf16(&m->tmW1, m->W1b, kXld, e1, kXld * 2, 64, e1) &&
+              make_tmap_bf16(&m->tmW2, m->W2b, e1, e2, (uint64_t)e1 * 2, 64, e2) &&
+              make_tmap_bf16(&m->tmW3, m->W3b, e2, dm, (uint64_t)e2 * 2, 64, dm);
+    for (int l = 0; l < d.n_layer && ok; ++l) {
+        __nv_bfloat16 *win, *wout, *wx, *wdt;
+        if ((st = upload_bf16(m, h.Win[l], 2 * di, dm, 2 * di, dm, &win)) != TCL_OK) return st;
+        if ((st = upload_bf16(m, h.Wout[l], dm, di, dm, di, &wout)) != TCL_OK) return st;
+        if ((st = upload_bf16(m, h.Wx[l], R + 2 * N, di, m->nxp, di, &wx)) != TCL_OK) return st;
+        if ((st = upload_bf16(m, h.Wdt[l], di, R, di, m->rp, &wdt)) != TCL_OK) return st;
+        m->Winb.push_back(win); m->Woutb.push_back(wout); m->Wxb.push_back(wx); m->Wdtb.push_back(wdt);
+        CUtensorMap a, b;
+        ok = make_tmap_bf16(&a, win, dm, 2 * di, (uint64_t)dm * 2, 64, m->bn_in) &&
+             make_tmap_bf16(&b, wout, di, dm, (uint64_t)di * 2, 64, dm);
+        m->tmWin.push_back(a);
+        m->tmWout.push_back(b);
+    }
+    if (!ok) return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (weights)");
+    return TCL_OK;
+}
+
+// ------------------------------------------------------------------------------ workspace
 
 static void free_workspace(tcl_model* m) {
     Workspace& w = m->ws;
@@ -131,6 +226,22 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     TAKE(G, rows * di);
     TAKE(DBC, rows * m->ldbc);
     TAKE(m2, chunk_n);
+    if (m->use_tc) {
+        const int64_t xzw = std::max<int64_t>(2 * di, (int64_t)d.enc_dims[0] + d.enc_dims[1]);
+        TAKE(Xb, rows * kXld);
+        TAKE(XZb, rows * xzw);
+        TAKE(Ab, rows * dm);
+        TAKE(Gb, rows * di);
+        const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+        __nv_bfloat16* E1b = w.XZb;
+        __nv_bfloat16* E2b = w.XZb + rows * e1;
+        bool ok = make_tmap_bf16(&w.tmXb, w.Xb, kXld, rows, kXld * 2, 64, 128) &&
+                  make_tmap_bf16(&w.tmE1b, E1b, e1, rows, (uint64_t)e1 * 2, 64, 128) &&
+                  make_tmap_bf16(&w.tmE2b, E2b, e2, rows, (uint64_t)e2 * 2, 64, 128) &&
+                  make_tmap_bf16(&w.tmAb, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128) &&
+                  make_tmap_bf16(&w.tmGb, w.Gb, di, rows, (uint64_t)di * 2, 64, 128);
+        if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
+    }
 #undef TAKE
     w.cap_n = chunk_n;
     w.rows = rows;
@@ -225,6 +336,126 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     launch_head(h, s); ++nl;
 }
 
+static tcl_status debug_sync(const char* where, cudaStream_t s) {
+    static int on = -1;
+    if (on < 0) { const char* e = getenv("TCL_DEBUG_SYNC"); on = (e && e[0] == '1') ? 1 : 0; }
+    if (!on) return TCL_OK;
+    cudaError_t e = cudaStreamSynchronize(s);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, where);
+    fprintf(stderr, "[tcl] %s ok\n", where);
+    return TCL_OK;
+}
+
+// The bf16 projection path (precision == TCL_PREC_BF16_PROJ): tcgen05 GEMMs with fused
+// epilogues for the encoder / in_proj / out_proj(+LN), one fused mixer kernel per layer.
+static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
+                                   float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+    const tcl_dims& d = m->dims;
+    Workspace& w = m->ws;
+    const int L = d.max_len, dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+    const int32_t* P = w.cu + n;
+    int64_t& nl = m->launches;
+    const int64_t rows = w.rows;
+    __nv_bfloat16* E1b = w.XZb;
+    __nv_bfloat16* E2b = w.XZb + rows * e1;
+    cudaError_t e;
+    {
+        ProfScope ps(m, TCL_PROF_PACK, s);
+        launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++nl;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, nullptr, w.Xb, w.row_cand, s); ++nl;
+    }
+    if (debug_sync("pack", s) != TCL_OK) return TCL_ECUDA;
+    auto base = [&]() {
+        TcGemmParams p{};
+        p.n_tiles = 1; p.p_rows = P; p.drop = drop; p.drop.enabled = 0; p.row_cand = w.row_cand; p.cu = w.cu;
+        p.eps = d.ln_eps;
+        return p;
+    };
+    auto kb_of = [](int K) { return (K + 63) / 64; };
+    {
+        ProfScope ps(m, TCL_PROF_ENCODER, s);
+        TcGemmParams p = base();
+        p.epi = TC_EPI_BF16; p.bias = m->wp.enc_b1; p.act_silu = 1; p.out = E1b; p.ldo = e1;
+        p.drop.enabled = drop.enabled; p.site = 0;
+        if ((e = launch_gemm_tc(w.tmXb, m->tmW1, p, e1, 1, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc1");
+        ++nl;
+        if (debug_sync("enc1", s) != TCL_OK) return TCL_ECUDA;
+        p.bias = m->wp.enc_b2; p.out = E2b; p.ldo = e2; p.site = 1;
+        if ((e = launch_gemm_tc(w.tmE1b, m->tmW2, p, e2, kb_of(e1), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc2");
+        ++nl;
+        if (debug_sync("enc2", s) != TCL_OK) return TCL_ECUDA;
+        TcGemmParams q = base();
+        q.epi = TC_EPI_RESID_LN; q.bias = m->wp.enc_b3; q.residual = 0; q.H = w.H; q.ldh = dm;
+        q.out = d.n_layer > 0 ? w.Ab : nullptr; q.ldo = dm;
+        q.ln_g = d.n_layer > 0 ? m->wp.layers[0].ln_w : m->wp.lnf_w;
+        q.ln_b = d.n_layer > 0 ? m->wp.layers[0].ln_b : m->wp.lnf_b;
+        if ((e = launch_gemm_tc(w.tmE2b, m->tmW3, q, dm, kb_of(e2), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc3");
+        ++nl;
+        if (debug_sync("enc3", s) != TCL_OK) return TCL_ECUDA;
+    }
+    for (int l = 0; l < d.n_layer; ++l) {
+        const LayerPtrs& q = m->wp.layers[l];
+        {
+            ProfScope ps(m, TCL_PROF_IN_PROJ, s);
+            TcGemmParams p = base();
+            p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
+            if ((e = launch_gemm_tc(w.tmAb, m->tmWin[l], p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
+                return cuda_error(e, "in_proj");
+            ++nl;
+            if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;
+        }
+        {
+            ProfScope ps(m, TCL_PROF_MIXER, s);
+            MixerArgs a{};
+            a.XZ = w.XZb; a.ldxz = 2 * di; a.G = w.Gb; a.ldg = di;
+            a.A2 = m->A2 + (size_t)l * di * N; a.invA = m->invA + (size_t)l * di * N; a.Dv = q.Dv;
+            a.w_conv = q.w_conv; a.b_conv = q.b_conv; a.b_dt = q.b_dt;
+            a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
+            a.cu = w.cu; a.lens = lens; a.n = n;
+            a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
+            if ((e = launch_mixer_fused(a, s)) != cudaSuccess) return cuda_error(e, "mixer");
+            ++nl;
+            if (debug_sync("mixer", s) != TCL_OK) return TCL_ECUDA;
+        }
+        {
+            ProfScope ps(m, TCL_PROF_OUT_PROJ, s);
+            TcGemmParams p = base();
+            p.epi = TC_EPI_RESID_LN; p.residual = 1; p.H = w.H; p.ldh = dm;
+            const bool last = l + 1 == d.n_layer;
+            p.out = last ? nullptr : w.Ab; p.ldo = dm;
+            p.ln_g = last ? m->wp.lnf_w : m->wp.layers[l + 1].ln_w;
+            p.ln_b = last ? m->wp.lnf_b : m->wp.layers[l + 1].ln_b;
+            if ((e = launch_gemm_tc(w.tmGb, m->tmWout[l], p, dm, kb_of(di), m->num_sms, s)) != cudaSuccess)
+                return cuda_error(e, "out_proj");
+            ++nl;
+            if (debug_sync("out_proj", s) != TCL_OK) return TCL_ECUDA;
+        }
+    }
+    HeadArgs h{};
+    h.H = w.H; h.ldh = dm; h.dm = dm; h.lnf_w = m->wp.lnf_w; h.lnf_b = m->wp.lnf_b; h.eps = d.ln_eps;
+    h.W1 = m->wp.dec_W1; h.b1 = m->wp.dec_b1; h.h1 = d.dec_dims[0];
+    h.W2 = m->wp.dec_W2; h.b2 = m->wp.dec_b2; h.h2 = d.dec_dims[1];
+    h.W3 = m->wp.dec_W3; h.b3 = m->wp.dec_b3;
+    h.cu = w.cu; h.lens = lens; h.max_len = L; h.n = n; h.scores = scores; h.drop = drop;
+    h.mean = mc_mean; h.m2 = w.m2;
+    ProfScope ps(m, TCL_PROF_HEAD, s);
+    launch_head(h, s); ++nl;
+    return TCL_OK;
+}
+
+static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, float* scores,
+                              const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+    if (m->use_tc) {
+        tcl_status st = forward_chunk_tc(m, feats, lens, n, scores, drop, mc_mean, s);
+        if (st != TCL_OK) return st;
+        return debug_sync("forward_chunk_tc", s);
+    }
+    forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s);
+    return debug_sync("forward_chunk", s);
+}
+
 static int64_t chunk_cap(const tcl_model* m) {
     // bound the activation arena: <= 4M packed rows per chunk (>= 1 candidate)
     int64_t c = (int64_t)(4 << 20) / m->dims.max_len;
@@ -314,6 +545,9 @@ tcl_status tcl_model_create(const float* weights_host, size_t n_floats, const tc
         cudaMemcpy(m->A2, a2.data(), a2.size() * sizeof(float), cudaMemcpyHostToDevice);
         cudaMemcpy(m->invA, ia.data(), ia.size() * sizeof(float), cudaMemcpyHostToDevice);
     }
+    if (d.precision == TCL_PREC_BF16_PROJ) {
+        if ((st = setup_tc(m, weights_host)) != TCL_OK) { tcl_model_destroy(m); return st; }
+    }
     if ((st = dev_alloc(&m->d_err, 1)) != TCL_OK) { tcl_model_destroy(m); return st; }
     CUDA_TRY(cudaMemset(m->d_err, 0, sizeof(int)));
     if ((st = dev_alloc(&m->keys_send, 4096)) != TCL_OK) { tcl_model_destroy(m); return st; }
@@ -336,6 +570,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
         if (q) cudaFree(q);
     if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     for (auto ev : m->chunk_events) cudaEventDestroy(ev);
+    for (void* q : m->bf_allocs) cudaFree(q);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
     delete m;
@@ -362,7 +597,8 @@ tcl_status tcl_score(tcl_model* m, const float* feats, const int32_t* lens, int6
     const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
     for (int64_t off = 0; off < n; off += cap) {
         const int64_t nc = std::min(cap, n - off);
-        forward_chunk(m, feats + off * stride, lens + off, nc, scores + off, nodrop, nullptr, s);
+        st = forward_any(m, feats + off * stride, lens + off, nc, scores + off, nodrop, nullptr, s);
+        if (st != TCL_OK) return st;
     }
     CUDA_TRY(cudaGetLastError());
     return TCL_OK;
@@ -392,7 +628,8 @@ tcl_status tcl_score_mc(tcl_model* m, const float* feats, const int32_t* lens, i
         drop.index_base = index_base + off;
         for (int ps = 0; ps < n_passes; ++ps) {
             drop.pass = ps;
-            forward_chunk(m, feats + off * stride, lens + off, nc, nullptr, drop, mean + off, s);
+            st = forward_any(m, feats + off * stride, lens + off, nc, nullptr, drop, mean + off, s);
+            if (st != TCL_OK) return st;
         }
         ProfScope ps(m, TCL_PROF_MC, s);
         launch_mc_finalize(m->ws.m2, nc, n_passes, var + off, s);
@@ -432,6 +669,36 @@ tcl_status tcl_sync_error(tcl_model* m, void* stream) {
 }
 
 int64_t tcl_launch_count(const tcl_model* m) { return m ? m->launches : 0; }
+
+tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t rows, int64_t cols) {
+    if (!m || !name || !out || rows < 0 || cols < 1) return set_error(TCL_EINVAL, "bad argument");
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const Workspace& w = m->ws;
+    if (rows > w.rows) return set_error(TCL_EINVAL, "rows exceed the workspace");
+    const std::string nm(name);
+    const void* src = nullptr;
+    bool bf = false;
+    if (nm == "H") src = w.H;
+    else if (nm == "A") { src = m->use_tc ? (const void*)w.Ab : (const void*)w.A; bf = m->use_tc; }
+    else if (nm == "XZ") { src = m->use_tc ? (const void*)w.XZb : (const void*)w.XZ; bf = m->use_tc; }
+    else if (nm == "G") { src = m->use_tc ? (const void*)w.Gb : (const void*)w.G; bf = m->use_tc; }
+    else if (nm == "U" && !m->use_tc) src = w.U;
+    else if (nm == "DELTA" && !m->use_tc) src = w.Delta;
+    if (!src) return set_error(TCL_EINVAL, "unknown buffer name");
+    const size_t cnt = (size_t)rows * cols;
+    if (!bf) {
+        CUDA_TRY(cudaMemcpy(out, src, cnt * sizeof(float), cudaMemcpyDeviceToHost));
+    } else {
+        std::vector<uint16_t> h(cnt);
+        CUDA_TRY(cudaMemcpy(h.data(), src, cnt * 2, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < cnt; ++i) {
+            uint32_t u = (uint32_t)h[i] << 16;
+            memcpy(&out[i], &u, 4);
+        }
+    }
+    return TCL_OK;
+}
 
 tcl_status tcl_profile_enable(tcl_model* m, int enable) {
     if (!m) return set_error(TCL_EINVAL, "null model");

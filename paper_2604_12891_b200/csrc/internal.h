@@ -1,5 +1,7 @@
 // internal.h -- the model object behind the opaque tcl_model handle (host side only).
 #pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -38,6 +40,12 @@ struct Workspace {
     float* G = nullptr;           // [rows][di]   gated scan output
     float* DBC = nullptr;         // [rows][ldbc] x_proj output
     float* m2 = nullptr;          // [cap_n] MC Welford M2
+    // bf16 tensor-core path
+    __nv_bfloat16* Xb = nullptr;   // [rows][kXld]  packed features
+    __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden
+    __nv_bfloat16* Ab = nullptr;   // [rows][dm]    LN_l(H)
+    __nv_bfloat16* Gb = nullptr;   // [rows][di]    gated scan output
+    CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;
     std::vector<void*> allocs;
 };
 
@@ -74,6 +82,13 @@ struct tcl_model {
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> chunk_events;
     int64_t launches = 0;
+    // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)
+    int use_tc = 0, num_sms = 148, nxp = 0, rp = 0, bn_in = 0;
+    std::vector<void*> bf_allocs;
+    __nv_bfloat16 *W1b = nullptr, *W2b = nullptr, *W3b = nullptr;
+    std::vector<__nv_bfloat16*> Winb, Woutb, Wxb, Wdtb;
+    CUtensorMap tmW1, tmW2, tmW3;
+    std::vector<CUtensorMap> tmWin, tmWout;
     // per-stage instrumentation (tcl_profile_enable)
     int prof_on = 0;
     struct ProfRec { int kind; cudaEvent_t a, b; };

@@ -1,0 +1,305 @@
+// gemm_tc.cu -- the projections of the bf16 path on the 5th-generation tensor cores (tcgen05).
+//
+//   in_proj   [x|z] = LN_l(H) W_in^T
+//   out_proj  H <- H + g W_out^T, then LN_{l+1}(H)   (a8 + a3 of the next layer, fused epilogue)
+//   encoder   SiLU(X W1^T + b1), SiLU(. W2^T + b2), . W3^T + b3 (+ LN_0)   (a2)
+//
+// Design (B200-first): persistent, warp-specialised, weight-stationary.  Each CTA keeps its
+// [BN x K] slice of the weight matrix resident in shared memory for the whole launch (loaded once
+// by TMA), and streams 128-row activation tiles through a 4-stage TMA ring (128B-swizzled,
+// K-major).  One elected thread issues tcgen05.mma (M=128, N=BN, K=16 per instruction) into a
+// double-buffered fp32 accumulator in TMEM (2 x BN columns), so the epilogue of tile i overlaps
+// the MMAs of tile i+1.  Four epilogue warps drain TMEM with tcgen05.ld (one row per thread) and
+// apply the fused epilogue (bias, SiLU, MC-dropout, bf16 pack; or residual add + LayerNorm of the
+// next layer computed in-thread from the full row).
+//
+// Roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + MMA issuer,
+// warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4) .. 32*(w%4)+31).
+#include <cuda_bf16.h>
+
+#include "../kernels_tc.h"
+#include "../tc_ptx.cuh"
+
+namespace tcl {
+
+constexpr int kStages = 4;
+constexpr int kBM = 128;
+constexpr int kABytes = kBM * 128;  // one 128 x 64 bf16 K-block of A
+
+template <int BN, int KB>
+struct TcSmem {
+    static constexpr int kBBytes = KB * BN * 128;
+    static constexpr int kOffB = 0;
+    static constexpr int kOffA = kOffB + kBBytes;
+    static constexpr int kOffBar = kOffA + kStages * kABytes;
+    static constexpr int kBytes = kOffBar + 256 + 1024;  // + barriers, + alignment slack
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+template <int BN, int KB>
+__global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
+                                                    const __grid_constant__ CUtensorMap tmB,
+                                                    const TcGemmParams p) {
+    using S = TcSmem<BN, KB>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sB = smem + S::kOffB;
+    uint8_t* sA = smem + S::kOffA;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
+    uint64_t* empty = full + kStages;
+    uint64_t* bfull = empty + kStages;
+    uint64_t* tfull = bfull + 1;      // [2]
+    uint64_t* tempty = tfull + 2;     // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int rows = *p.p_rows;
+    const int num_m = (rows + kBM - 1) / kBM;
+    const int n_tile = blockIdx.x % p.n_tiles;
+    const int m_first = blockIdx.x / p.n_tiles;
+    const int m_step = gridDim.x / p.n_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        tc::mbar_init(bfull, 1);
+        for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
+        tc::fence_mbar_init();
+    }
+    if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
+    tc::tc_fence_before();
+    __syncthreads();
+    tc::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer
+            tc::tma_prefetch(&tmA);
+            tc::tma_prefetch(&tmB);
+            tc::mbar_arrive_expect_tx(bfull, S::kBBytes);
+            for (int kb = 0; kb < KB; ++kb)
+                tc::tma_load_2d(sB + kb * BN * 128, &tmB, kb * 64, n_tile * BN, bfull);
+            const uint64_t pol = tc::policy_evict_first();
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int m = m_first; m < num_m; m += m_step) {
+                for (int kb = 0; kb < KB; ++kb) {
+                    tc::mbar_wait(&empty[stage], phase ^ 1);
+                    tc::mbar_arrive_expect_tx(&full[stage], kABytes);
+                    tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+        __syncwarp();
+    } else if (warp == 1) {
+        if (lane == 0) {
+            // ---------------- MMA issuer (single thread)
+            constexpr uint32_t idesc = tc::idesc_bf16_f32(kBM, BN);
+            tc::mbar_wait(bfull, 0);
+            tc::tc_fence_after();
+            const uint32_t sA_addr = tc::smem_u32(sA), sB_addr = tc::smem_u32(sB);
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int m = m_first; m < num_m; m += m_step) {
+                tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc::tc_fence_after();
+                const uint32_t d = tmem_base + acc * BN;
+                for (int kb = 0; kb < KB; ++kb) {
+                    tc::mbar_wait(&full[stage], phase);
+                    tc::tc_fence_after();
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const uint64_t ad = tc::sw128_kmajor_desc(sA_addr + stage * kABytes + k * 32);
+                        const uint64_t bd = tc::sw128_kmajor_desc(sB_addr + kb * BN * 128 + k * 32);
+                        tc::mma_bf16(d, ad, bd, idesc, (kb | k) != 0);
+                    }
+                    tc::mma_commit(&empty[stage]);
+                    if (++stage == kStages) { stage = 0; phase ^= 1; }
+                }
+                tc::mma_commit(&tfull[acc]);
+                if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+            }
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue warps
+        const int quarter = warp & 3;
+        const int rloc = quarter * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int m = m_first; m < num_m; m += m_step) {
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
+            const int row = m * kBM + rloc;
+            const bool valid = row < rows;
+            const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
+            if (p.epi == TC_EPI_BF16) {
+                int cand = 0, token = 0;
+                if (p.drop.enabled && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
+                __nv_bfloat16* orow = p.out + (int64_t)row * p.ldo + n_tile * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(tbase + c * 32, r);
+                    tc::tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const int n = n_tile * BN + c * 32 + j;
+                        float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+                        if (p.bias) { v0 += __ldg(p.bias + n); v1 += __ldg(p.bias + n + 1); }
+                        if (p.act_silu) { v0 = silu(v0); v1 = silu(v1); }
+                        if (p.drop.enabled) {
+                            v0 = dropout_keep(p.drop, n, token, p.site, cand) ? v0 * p.drop.scale : 0.0f;
+                            v1 = dropout_keep(p.drop, n + 1, token, p.site, cand) ? v1 * p.drop.scale : 0.0f;
+                        }
+                        pk[j / 2] = pack_bf16x2(v0, v1);
+                    }
+                    if (valid) {
+                        uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
+                }
+            } else {
+                // residual (+bias) into H (fp32), then LayerNorm of the full row -> bf16 A
+                float* hrow = p.H + (int64_t)row * p.ldh;
+                float sum = 0.f, sumsq = 0.f, shift = 0.f;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(tbase + c * 32, r);
+                    tc::tmem_ld_wait();
+                    float v[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
+                    if (p.bias) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) v[j] += __ldg(p.bias + c * 32 + j);
+                    }
+                    if (p.residual && valid) {
+                        const float4* h4 = reinterpret_cast<const float4*>(hrow + c * 32);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) {
+                            float4 h = h4[q];
+                            v[4 * q] += h.x; v[4 * q + 1] += h.y; v[4 * q + 2] += h.z; v[4 * q + 3] += h.w;
+                        }
+                    }
+                    if (valid) {
+                        float4* o4 = reinterpret_cast<float4*>(hrow + c * 32);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                    }
+                    if (c == 0) shift = v[0];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float t = v[j] - shift;
+                        sum += t;
+                        sumsq = fmaf(t, t, sumsq);
+                        r[j] = __float_as_uint(v[j]);
+                    }
+                    tc::tmem_st32(tbase + c * 32, r);  // keep the new row in TMEM for pass 2
+                }
+                tc::tmem_st_wait();
+                const float inv = 1.0f / (float)BN;
+                const float mean_s = sum * inv;
+                const float var = fmaxf(sumsq * inv - mean_s * mean_s, 0.0f);
+                const float mean = shift + mean_s;
+                const float rstd = rsqrtf(var + p.eps);
+                __nv_bfloat16* arow = p.out + (int64_t)row * p.ldo;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t r[32];
+                    tc::tmem_ld32(tbase + c * 32, r);
+                    tc::tmem_ld_wait();
+                    uint32_t pk[16];
+#pragma unroll
+                    for (int j = 0; j < 32; j += 2) {
+                        const int n = c * 32 + j;
+                        const float a0 = (__uint_as_float(r[j]) - mean) * rstd * __ldg(p.ln_g + n) + __ldg(p.ln_b + n);
+                        const float a1 = (__uint_as_float(r[j + 1]) - mean) * rstd * __ldg(p.ln_g + n + 1) + __ldg(p.ln_b + n + 1);
+                        pk[j / 2] = pack_bf16x2(a0, a1);
+                    }
+                    if (valid && p.out) {
+                        uint4* dst = reinterpret_cast<uint4*>(arow + c * 32);
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    }
+                }
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+            if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+        }
+    }
+    tc::tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc::tc_fence_after();
+        tc::tmem_dealloc(tmem_base, 2 * BN);
+    }
+}
+
+// ------------------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* f = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
+}
+
+bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                    uint32_t box_inner, uint32_t box_outer) {
+    auto fn = encode_fn();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t es[2] = {1, 1};
+    CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, int KB>
+static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int grid,
+                               cudaStream_t s) {
+    const int smem = TcSmem<BN, KB>::kBytes;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_gemm_tc<BN, KB><<<grid, 192, smem, s>>>(a, b, p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int bn, int kb,
+                           int num_sms, cudaStream_t s) {
+    // grid: one persistent CTA per SM, a multiple of the number of N tiles
+    const int grid = (num_sms / p.n_tiles) * p.n_tiles;
+#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_impl<BN_, KB_>(a, b, p, grid, s);
+    TCL_TC_CASE(256, 1) TCL_TC_CASE(256, 2) TCL_TC_CASE(256, 3) TCL_TC_CASE(256, 4)
+    TCL_TC_CASE(128, 1) TCL_TC_CASE(128, 2) TCL_TC_CASE(128, 3) TCL_TC_CASE(128, 4)
+    TCL_TC_CASE(64, 1) TCL_TC_CASE(64, 2) TCL_TC_CASE(64, 3) TCL_TC_CASE(64, 4)
+    TCL_TC_CASE(32, 1) TCL_TC_CASE(32, 2) TCL_TC_CASE(32, 3) TCL_TC_CASE(32, 4)
+#undef TCL_TC_CASE
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace tcl

@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
     const float* src = feats + slot * d_in;
     for (int c = lane; c < ldx; c += 32) {
         float v = c < d_in ? __ldg(src + c) : 0.0f;
-        X[row * ldx + c] = v;
+        if (X) X[row * ldx + c] = v;
         if (Xb) Xb[row * ldx + c] = __float2bfloat16_rn(v);
     }
     if (lane == 0) row_cand[row] = (int32_t)i;

@@ -1,0 +1,36 @@
+// kernels_tc.h -- launchers of the tcgen05 / TMA kernels (bf16 projection path).
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace tcl {
+
+enum TcEpi : int { TC_EPI_BF16 = 0, TC_EPI_RESID_LN = 1 };
+
+struct TcGemmParams {
+    int n_tiles;                 // N / BN (each CTA owns one N tile for the whole launch)
+    const int32_t* p_rows;       // device: number of valid rows (packed tokens)
+    int epi;
+    // TC_EPI_BF16: out[row][n] = bf16(dropout(act(acc + bias)))
+    const float* bias;           // [N] or nullptr
+    int act_silu;
+    __nv_bfloat16* out; int ldo; // bf16 output (EPI_BF16) / LayerNorm output (EPI_RESID_LN)
+    // TC_EPI_RESID_LN: H = (residual ? H : 0) + acc (+ bias); out = bf16(LN(H) * g + b)
+    float* H; int ldh; int residual;
+    const float* ln_g; const float* ln_b; float eps;
+    DropoutCtx drop; int site; const int32_t* row_cand; const int32_t* cu;
+};
+
+// 2-D bf16 tensor map, 128B swizzle, box {box_inner (<= 64), box_outer (<= 256)}.
+bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                    uint32_t box_inner, uint32_t box_outer);
+// A: [rows][K] (box {64, 128}); B: [N][K] weights (box {64, bn}); kb = ceil(K / 64).
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int bn, int kb,
+                           int num_sms, cudaStream_t s);
+
+}  // namespace tcl

@@ -46,7 +46,7 @@ class tcl_dims(ctypes.Structure):
 EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score",
            "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
-           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name"]
+           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read"]
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc"]
 
@@ -89,11 +89,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_build_info.argtypes = []
     L.tcl_profile_enable.argtypes = [vp, ctypes.c_int]
     L.tcl_profile_read.argtypes = [vp, P(ctypes.c_double), P(i64), ctypes.c_int]
+    L.tcl_debug_read.argtypes = [vp, ctypes.c_char_p, vp, i64, i64]
     L.tcl_profile_name.restype = ctypes.c_char_p
     L.tcl_profile_name.argtypes = [ctypes.c_int]
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
-               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read"):
+               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -189,6 +190,11 @@ class Model:
 
     def launch_count(self) -> int:
         return int(load().tcl_launch_count(self._h))
+
+    def debug_read(self, name: str, rows: int, cols: int) -> np.ndarray:
+        out = np.empty((rows, cols), np.float32)
+        _check(load().tcl_debug_read(self._h, name.encode(), out.ctypes.data, rows, cols))
+        return out
 
     def profile_enable(self, on: bool = True):
         _check(load().tcl_profile_enable(self._h, 1 if on else 0))

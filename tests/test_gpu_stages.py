@@ -1,0 +1,75 @@
+"""Per-stage GPU parity (SURVEY §4 tier T2): the workspace buffers of a 1-layer model, read back
+through tcl_debug_read, against the oracle's per-stage dumps of the same candidates.
+
+bf16 path: operands are rounded to bf16 (8-bit mantissa), so stage tolerances are relative to the
+stage's magnitude: |gpu - ref| <= rtol * max|ref| + rtol * |ref| with rtol = 2e-2 (the north-star
+bf16 bound); the fp32 path is checked at 1e-4.
+"""
+import numpy as np
+import pytest
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_12891_b200 import build
+    build.build()
+    return torch
+
+
+def _run(torch, name, prec, n=24):
+    from paper_2604_12891_b200 import Model
+    c = inputs.config(name)
+    d = c["dims"].replace(n_layer=1, precision=prec)
+    w = inputs.make_weights(d, c["seed"])
+    f, l = inputs.make_features(d, n, c["seed"] + 3, workload="large")
+    m = Model(w, d)
+    ft, lt = torch.from_numpy(f).cuda(), torch.from_numpy(l).cuda()
+    s = torch.empty(n, dtype=torch.float32, device="cuda")
+    m.tcl_score(ft, lt, s)
+    m.tcl_sync_error()
+    return d, w, f, l, m, s.cpu().numpy()
+
+
+def _close(got, ref, rtol, what):
+    scale = np.abs(ref).max() + 1e-12
+    err = np.abs(got - ref)
+    bad = err > rtol * scale + rtol * np.abs(ref)
+    assert not bad.any(), f"{what}: {bad.sum()} / {bad.size} out of tol; max err {err.max():.3e} (scale {scale:.3e})"
+    return err.max() / scale
+
+
+@pytest.mark.parametrize("name,prec", [("large", 1), ("paper", 1), ("large", 0), ("tiny", 0)])
+def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
+    d, w, f, l, m, scores = _run(torch_cuda, name, prec)
+    P = int(l.sum())
+    di, dm = d.d_inner, d.d_model
+    stages = {k: [] for k in ("a", "x", "z", "g", "h")}
+    ref_scores = []
+    for i in range(len(l)):
+        sc, st = oracle.forward_one(d, w, f[i], int(l[i]))
+        ref_scores.append(sc)
+        for k in stages:
+            stages[k].append(st[f"layer0.{k}"])
+    ref = {k: np.concatenate(v, 0) for k, v in stages.items()}
+    rtol = 2e-2 if prec == 1 else 1e-4
+    A = m.debug_read("A", P, dm)
+    XZ = m.debug_read("XZ", P, 2 * di)
+    G = m.debug_read("G", P, di)
+    H = m.debug_read("H", P, dm)
+    rep = {}
+    rep["A"] = _close(A, ref["a"], rtol, "LN_0(H_enc)")
+    rep["x"] = _close(XZ[:, :di], ref["x"], rtol, "in_proj x")
+    rep["z"] = _close(XZ[:, di:], ref["z"], rtol, "in_proj z")
+    rep["g"] = _close(G, ref["g"], rtol, "gated scan output")
+    rep["h"] = _close(H, ref["h"], rtol, "residual after layer 0")
+    ref_scores = np.array(ref_scores)
+    rep["score"] = float(np.abs(scores - ref_scores).max())
+    assert np.all(np.abs(scores - ref_scores) <= rtol * np.maximum(1, np.abs(ref_scores)))
+    print(name, "prec", prec, {k: f"{v:.2e}" for k, v in rep.items()})
