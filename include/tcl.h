@@ -64,7 +64,9 @@ typedef enum { TCL_DISC_ZOH = 0, TCL_DISC_EULER_B = 1 } tcl_disc;
  * dec_dims = {64,32,1}, dt_rank = 8, d_in = 22.
  * Supported by this build: d_in <= 32; d_model, enc_dims in {multiples of 32} <= 256;
  * d_inner = expand*d_model <= 512 (multiple of 32); d_state in {8, 16}; dt_rank <= 32;
- * d_conv <= 8; dec_dims[0] <= 256, dec_dims[1] <= 256, dec_dims[2] == 1; max_len <= 256. */
+ * d_conv <= 8; dec_dims[0..1] multiples of 4 <= 256, dec_dims[2] == 1; max_len <= 256.
+ * BF16_PROJ additionally needs d_model, d_inner in {64, 128, 256}, enc_dims[0..1] <= 256,
+ * d_conv == 4. */
 typedef struct {
     int32_t d_in;        /* feature width D per token (22 on CPU targets)          */
     int32_t max_len;     /* L: padded sequence length of the feature tensor                       */

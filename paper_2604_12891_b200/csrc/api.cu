@@ -74,8 +74,9 @@ static tcl_status validate_dims(const tcl_dims* d) {
     for (int i = 0; i < 2; ++i)
         if (d->enc_dims[i] < 32 || d->enc_dims[i] > 512 || d->enc_dims[i] % 32) return bad("enc_dims[0..1] must be multiples of 32 in [32, 512]");
     if (d->dec_dims[2] != 1) return bad("dec_dims[2] must be 1");
-    if (d->dec_dims[0] < 1 || d->dec_dims[0] > 256 || d->dec_dims[1] < 1 || d->dec_dims[1] > 256)
-        return bad("dec_dims[0..1] must be in [1, 256]");
+    if (d->dec_dims[0] < 4 || d->dec_dims[0] > 256 || d->dec_dims[1] < 4 || d->dec_dims[1] > 256 ||
+        d->dec_dims[0] % 4 || d->dec_dims[1] % 4)
+        return bad("dec_dims[0..1] must be multiples of 4 in [4, 256]");
     if (!(d->ln_eps > 0.0f)) return bad("ln_eps must be > 0");
     if (!(d->dropout_p >= 0.0f && d->dropout_p < 1.0f)) return set_error(TCL_EINVAL, "dropout_p must be in [0, 1)");
     if (d->precision != TCL_PREC_FP32 && d->precision != TCL_PREC_BF16_PROJ) return bad("unknown precision");
@@ -148,7 +149,7 @@ static tcl_status validate_tc(const tcl_dims& d) {
     for (int i = 0; i < 2; ++i)
         if (d.enc_dims[i] > 256) return bad("bf16 path: enc_dims[0..1] must be <= 256");
     if (d.dt_rank > 32) return bad("bf16 path: dt_rank must be <= 32");
-    if (d.d_conv < 2 || d.d_conv > 4) return bad("bf16 path: d_conv must be in [2, 4]");
+    if (d.d_conv != 4) return bad("bf16 path: d_conv must be 4");
     if (round_up(d.dt_rank + 2 * d.d_state, 8) > 64) return bad("bf16 path: dt_rank + 2 d_state must be <= 64");
     return TCL_OK;
 }
@@ -226,6 +227,10 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     TAKE(G, rows * di);
     TAKE(DBC, rows * m->ldbc);
     TAKE(m2, chunk_n);
+    TAKE(pooled, chunk_n * dm);
+    TAKE(dh1, chunk_n * d.dec_dims[0]);
+    TAKE(dh2, chunk_n * d.dec_dims[1]);
+    TAKE(dsc, chunk_n);
     if (m->use_tc) {
         const int64_t xzw = std::max<int64_t>(2 * di, (int64_t)d.enc_dims[0] + d.enc_dims[1]);
         TAKE(Xb, rows * kXld);
@@ -258,6 +263,37 @@ static tcl_status ensure_topk_tmp(tcl_model* m, int64_t n, int k) {
     if (st != TCL_OK) return st;
     m->topk_tmp_cap = need;
     return TCL_OK;
+}
+
+// ------------------------------------------------------------------------------ head
+// LN_f + masked mean (warp per candidate), then the decoder MLP as three small
+// fp32 GEMMs over the candidates (weights stream through shared memory once per 64 candidates);
+// MC passes fold each pass' score into (mean, M2) with Welford's update.
+static void run_head(tcl_model* m, const int32_t* lens, int64_t n, float* scores, const DropoutCtx& drop,
+                     float* mc_mean, cudaStream_t s) {
+    const tcl_dims& d = m->dims;
+    Workspace& w = m->ws;
+    const int dm = d.d_model, h1 = d.dec_dims[0], h2 = d.dec_dims[1];
+    int64_t& nl = m->launches;
+    ProfScope ps(m, TCL_PROF_HEAD, s);
+    launch_pool(w.H, dm, dm, m->wp.lnf_w, m->wp.lnf_b, d.ln_eps, w.cu, lens, d.max_len, n, w.pooled, s);
+    ++nl;
+    auto dec = [&](const float* X, int K, const float* W, const float* b, float* Y, int Nout, int epi, int site) {
+        GemmArgs g{};
+        g.X = X; g.ldx = K; g.W = W; g.ldw = K; g.bias = b; g.Y = Y; g.ldy = Nout; g.K = K; g.N = Nout;
+        g.max_rows = (int)n; g.p_rows = nullptr; g.rows_const = (int)n; g.rows_are_cands = 1; g.epi = epi;
+        g.drop = drop; g.site = site;
+        if (epi != EPI_SILU) g.drop.enabled = 0;
+        launch_gemm_simt(g, s);
+        ++nl;
+    };
+    dec(w.pooled, dm, m->wp.dec_W1, m->wp.dec_b1, w.dh1, h1, EPI_SILU, 2);
+    dec(w.dh1, h1, m->wp.dec_W2, m->wp.dec_b2, w.dh2, h2, EPI_SILU, 3);
+    float* out = mc_mean ? w.dsc : scores;
+    dec(w.dh2, h2, m->wp.dec_W3, m->wp.dec_b3, out, 1, EPI_NONE, -1);
+    if (mc_mean) launch_welford(w.dsc, lens, d.max_len, n, drop.pass, mc_mean, w.m2, s);
+    else launch_mask_invalid(lens, d.max_len, n, scores, s);
+    ++nl;
 }
 
 // ------------------------------------------------------------------------------ forward
@@ -325,15 +361,7 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
         gemm(w.G, di, q.W_out, di, nullptr, w.H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ);
     }
 
-    HeadArgs h{};
-    h.H = w.H; h.ldh = dm; h.dm = dm; h.lnf_w = m->wp.lnf_w; h.lnf_b = m->wp.lnf_b; h.eps = d.ln_eps;
-    h.W1 = m->wp.dec_W1; h.b1 = m->wp.dec_b1; h.h1 = d.dec_dims[0];
-    h.W2 = m->wp.dec_W2; h.b2 = m->wp.dec_b2; h.h2 = d.dec_dims[1];
-    h.W3 = m->wp.dec_W3; h.b3 = m->wp.dec_b3;
-    h.cu = w.cu; h.lens = lens; h.max_len = L; h.n = n; h.scores = scores; h.drop = drop;
-    h.mean = mc_mean; h.m2 = w.m2;
-    ProfScope ps(m, TCL_PROF_HEAD, s);
-    launch_head(h, s); ++nl;
+    run_head(m, lens, n, scores, drop, mc_mean, s);
 }
 
 static tcl_status debug_sync(const char* where, cudaStream_t s) {
@@ -415,7 +443,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
             a.cu = w.cu; a.lens = lens; a.n = n;
             a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
-            if ((e = launch_mixer_fused(a, s)) != cudaSuccess) return cuda_error(e, "mixer");
+            if ((e = launch_mixer_fused(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "mixer");
             ++nl;
             if (debug_sync("mixer", s) != TCL_OK) return TCL_ECUDA;
         }
@@ -433,15 +461,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             if (debug_sync("out_proj", s) != TCL_OK) return TCL_ECUDA;
         }
     }
-    HeadArgs h{};
-    h.H = w.H; h.ldh = dm; h.dm = dm; h.lnf_w = m->wp.lnf_w; h.lnf_b = m->wp.lnf_b; h.eps = d.ln_eps;
-    h.W1 = m->wp.dec_W1; h.b1 = m->wp.dec_b1; h.h1 = d.dec_dims[0];
-    h.W2 = m->wp.dec_W2; h.b2 = m->wp.dec_b2; h.h2 = d.dec_dims[1];
-    h.W3 = m->wp.dec_W3; h.b3 = m->wp.dec_b3;
-    h.cu = w.cu; h.lens = lens; h.max_len = L; h.n = n; h.scores = scores; h.drop = drop;
-    h.mean = mc_mean; h.m2 = w.m2;
-    ProfScope ps(m, TCL_PROF_HEAD, s);
-    launch_head(h, s); ++nl;
+    run_head(m, lens, n, scores, drop, mc_mean, s);
     return TCL_OK;
 }
 

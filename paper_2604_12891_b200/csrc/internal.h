@@ -40,6 +40,10 @@ struct Workspace {
     float* G = nullptr;           // [rows][di]   gated scan output
     float* DBC = nullptr;         // [rows][ldbc] x_proj output
     float* m2 = nullptr;          // [cap_n] MC Welford M2
+    float* pooled = nullptr;      // [cap_n][dm]  masked mean of LN_f(H)
+    float* dh1 = nullptr;         // [cap_n][h1]  decoder hidden 1
+    float* dh2 = nullptr;         // [cap_n][h2]  decoder hidden 2
+    float* dsc = nullptr;         // [cap_n]      per-pass score (MC)
     // bf16 tensor-core path
     __nv_bfloat16* Xb = nullptr;   // [rows][kXld]  packed features
     __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden

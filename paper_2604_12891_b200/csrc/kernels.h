@@ -30,6 +30,8 @@ struct GemmArgs {
     int K, N;
     int max_rows;                   // grid extent (rows)
     const int32_t* p_rows;          // device: actual row count (cu[n]); rows >= *p_rows skipped
+    int rows_const;                 // row count when p_rows == nullptr
+    int rows_are_cands;             // decoder: row = candidate, token 0 (dropout sites 2, 3)
     int epi;
     // dropout (EPI_SILU only): per-row candidate and token
     DropoutCtx drop; int site;
@@ -62,6 +64,16 @@ struct ScanArgs {
     int64_t n; int di, N, disc, accurate, max_len;
 };
 void launch_scan(const ScanArgs& a, cudaStream_t s);
+
+// ---- head: LN_f + masked mean pool (warp per candidate) -> pooled [n][dm] -----------------------
+void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const float* lnf_b, float eps,
+                 const int32_t* cu, const int32_t* lens, int max_len, int64_t n, float* pooled,
+                 cudaStream_t s);
+// MC: Welford update of (mean, m2) with this pass' scores; invalid lengths -> NaN.
+void launch_welford(const float* score, const int32_t* lens, int max_len, int64_t n, int pass,
+                    float* mean, float* m2, cudaStream_t s);
+// Scores of invalid candidates -> NaN (reading R16).
+void launch_mask_invalid(const int32_t* lens, int max_len, int64_t n, float* scores, cudaStream_t s);
 
 // ---- head: LN_f, masked mean, decoder (a9) ----------------------------------------------------
 struct HeadArgs {

@@ -14,7 +14,7 @@ constexpr int BM = 64, BN = 64, BK = 16;
 __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
     __shared__ __align__(16) float As[BK][BM + 4];
     __shared__ __align__(16) float Ws[BK][BN + 4];
-    const int rows = *a.p_rows;
+    const int rows = a.p_rows ? *a.p_rows : a.rows_const;
     const int m0 = blockIdx.x * BM;
     if (m0 >= rows) return;
     const int n0 = blockIdx.y * BN;
@@ -59,8 +59,8 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
         if (gm >= rows) continue;
         int cand = 0, token = 0;
         if (a.epi == EPI_SILU && a.drop.enabled) {
-            cand = a.row_cand[gm];
-            token = gm - a.cu[cand];
+            cand = a.rows_are_cands ? gm : a.row_cand[gm];
+            token = a.rows_are_cands ? 0 : gm - a.cu[cand];
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {

@@ -22,17 +22,22 @@
 
 namespace tcl {
 
-constexpr int kStages = 4;
 constexpr int kBM = 128;
 constexpr int kABytes = kBM * 128;  // one 128 x 64 bf16 K-block of A
+constexpr int kEpiWarps = 8;        // two warps per TMEM lane quarter (column halves)
+constexpr int kThreads = 64 + 32 * kEpiWarps;
 
 template <int BN, int KB>
 struct TcSmem {
     static constexpr int kBBytes = KB * BN * 128;
+    static constexpr int kStagesRaw = (200 * 1024 - kBBytes) / kABytes;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
     static constexpr int kOffB = 0;
     static constexpr int kOffA = kOffB + kBBytes;
-    static constexpr int kOffBar = kOffA + kStages * kABytes;
-    static constexpr int kBytes = kOffBar + 256 + 1024;  // + barriers, + alignment slack
+    static constexpr int kOffPar = kOffA + kStages * kABytes;         // bias, ln_g, ln_b  [3][BN] fp32
+    static constexpr int kOffRed = kOffPar + 3 * BN * 4;              // LN partials [2][128] float2
+    static constexpr int kOffBar = kOffRed + 2 * 128 * 8;
+    static constexpr int kBytes = kOffBar + 256 + 1024;               // + barriers, + alignment slack
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -40,15 +45,33 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <int BN, int KB>
-__global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
-                                                    const __grid_constant__ CUtensorMap tmB,
-                                                    const TcGemmParams p) {
+// MC-dropout keep test kept out of line: the hot epilogues stay small (no I-cache pressure).
+__device__ __noinline__ float drop_apply(const DropoutCtx& d, float v, int unit, int token, int site,
+                                         int64_t cand) {
+    return dropout_keep(d, unit, token, site, cand) ? v * d.scale : 0.0f;
+}
+
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// EPI: 0 = bf16 out; 1 = bf16 out of SiLU(acc + bias); 2 = same + MC dropout;
+//      3 = residual/bias into fp32 H, then LayerNorm(H) -> bf16 out (BN == full row)
+template <int BN, int KB, int EPI>
+__global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
+                                                         const __grid_constant__ CUtensorMap tmB,
+                                                         const TcGemmParams p) {
     using S = TcSmem<BN, KB>;
+    constexpr int kStages = S::kStages;
+    constexpr int NCH = BN / 32;  // 32-column chunks of the accumulator
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sB = smem + S::kOffB;
     uint8_t* sA = smem + S::kOffA;
+    float* s_bias = reinterpret_cast<float*>(smem + S::kOffPar);
+    float* s_g = s_bias + BN;
+    float* s_b = s_g + BN;
+    float2* s_red = reinterpret_cast<float2*>(smem + S::kOffRed);  // [2 halves][128 rows]
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::kOffBar);
     uint64_t* empty = full + kStages;
     uint64_t* bfull = empty + kStages;
@@ -64,10 +87,15 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUte
     const int m_step = gridDim.x / p.n_tiles;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) { tc::mbar_init(&full[s], 1); tc::mbar_init(&empty[s], 1); }
+        for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], 1); }
         tc::mbar_init(bfull, 1);
-        for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], 4); }
+        for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], kEpiWarps); }
         tc::fence_mbar_init();
+    }
+    for (int j = threadIdx.x; j < BN; j += kThreads) {
+        const int n = n_tile * BN + j;
+        s_bias[j] = p.bias ? __ldg(p.bias + n) : 0.0f;
+        if (EPI == 3) { s_g[j] = __ldg(p.ln_g + j); s_b[j] = __ldg(p.ln_b + j); }
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
     tc::tc_fence_before();
@@ -129,8 +157,9 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUte
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue warps
+        // ---------------- epilogue warps: warp w drains TMEM lanes 32*(w%4).., column half h
         const int quarter = warp & 3;
+        const int half = (warp - 2) >> 2;
         const int rloc = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -140,25 +169,27 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUte
             const int row = m * kBM + rloc;
             const bool valid = row < rows;
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
-            if (p.epi == TC_EPI_BF16) {
+            if constexpr (EPI != 3) {
                 int cand = 0, token = 0;
-                if (p.drop.enabled && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
+                if (EPI == 2 && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
                 __nv_bfloat16* orow = p.out + (int64_t)row * p.ldo + n_tile * BN;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = half; c < NCH; c += 2) {
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
                     tc::tmem_ld_wait();
                     uint32_t pk[16];
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) {
-                        const int n = n_tile * BN + c * 32 + j;
                         float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
-                        if (p.bias) { v0 += __ldg(p.bias + n); v1 += __ldg(p.bias + n + 1); }
-                        if (p.act_silu) { v0 = silu(v0); v1 = silu(v1); }
-                        if (p.drop.enabled) {
-                            v0 = dropout_keep(p.drop, n, token, p.site, cand) ? v0 * p.drop.scale : 0.0f;
-                            v1 = dropout_keep(p.drop, n + 1, token, p.site, cand) ? v1 * p.drop.scale : 0.0f;
+                        if (EPI >= 1) {
+                            v0 = silu(v0 + s_bias[c * 32 + j]);
+                            v1 = silu(v1 + s_bias[c * 32 + j + 1]);
+                        }
+                        if (EPI == 2) {
+                            const int n = n_tile * BN + c * 32 + j;
+                            v0 = drop_apply(p.drop, v0, n, token, p.site, cand);
+                            v1 = drop_apply(p.drop, v1, n + 1, token, p.site, cand);
                         }
                         pk[j / 2] = pack_bf16x2(v0, v1);
                     }
@@ -169,70 +200,86 @@ __global__ void __launch_bounds__(192, 1) k_gemm_tc(const __grid_constant__ CUte
                     }
                 }
             } else {
-                // residual (+bias) into H (fp32), then LayerNorm of the full row -> bf16 A
+                // pass 1: v = acc + bias (+ H_old); store H; keep v in TMEM; partial row sum
                 float* hrow = p.H + (int64_t)row * p.ldh;
-                float sum = 0.f, sumsq = 0.f, shift = 0.f;
+                float sum = 0.f;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = half; c < NCH; c += 2) {
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
-                    tc::tmem_ld_wait();
-                    float v[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
-                    if (p.bias) {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) v[j] += __ldg(p.bias + c * 32 + j);
-                    }
+                    float hv[32];
                     if (p.residual && valid) {
                         const float4* h4 = reinterpret_cast<const float4*>(hrow + c * 32);
 #pragma unroll
                         for (int q = 0; q < 8; ++q) {
-                            float4 h = h4[q];
-                            v[4 * q] += h.x; v[4 * q + 1] += h.y; v[4 * q + 2] += h.z; v[4 * q + 3] += h.w;
+                            const float4 h = h4[q];
+                            hv[4 * q] = h.x; hv[4 * q + 1] = h.y; hv[4 * q + 2] = h.z; hv[4 * q + 3] = h.w;
                         }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) hv[j] = 0.0f;
+                    }
+                    tc::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float v = __uint_as_float(r[j]) + s_bias[c * 32 + j] + hv[j];
+                        hv[j] = v;
+                        sum += v;
+                        r[j] = __float_as_uint(v);
                     }
                     if (valid) {
                         float4* o4 = reinterpret_cast<float4*>(hrow + c * 32);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) o4[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                        for (int q = 0; q < 8; ++q) o4[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
                     }
-                    if (c == 0) shift = v[0];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float t = v[j] - shift;
-                        sum += t;
-                        sumsq = fmaf(t, t, sumsq);
-                        r[j] = __float_as_uint(v[j]);
-                    }
-                    tc::tmem_st32(tbase + c * 32, r);  // keep the new row in TMEM for pass 2
+                    tc::tmem_st32(tbase + c * 32, r);
                 }
                 tc::tmem_st_wait();
-                const float inv = 1.0f / (float)BN;
-                const float mean_s = sum * inv;
-                const float var = fmaxf(sumsq * inv - mean_s * mean_s, 0.0f);
-                const float mean = shift + mean_s;
-                const float rstd = rsqrtf(var + p.eps);
-                __nv_bfloat16* arow = p.out + (int64_t)row * p.ldo;
+                // exchange the halves' partial sums (named barrier of the 2 warps of this quarter)
+                s_red[half * 128 + rloc].x = sum;
+                named_bar(1 + quarter, 64);
+                const float mean = (s_red[rloc].x + s_red[128 + rloc].x) * (1.0f / BN);
+                // pass 2: sum of squared deviations (two-pass variance, no cancellation)
+                float sq = 0.f;
 #pragma unroll 1
-                for (int c = 0; c < BN / 32; ++c) {
+                for (int c = half; c < NCH; c += 2) {
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
                     tc::tmem_ld_wait();
-                    uint32_t pk[16];
 #pragma unroll
-                    for (int j = 0; j < 32; j += 2) {
-                        const int n = c * 32 + j;
-                        const float a0 = (__uint_as_float(r[j]) - mean) * rstd * __ldg(p.ln_g + n) + __ldg(p.ln_b + n);
-                        const float a1 = (__uint_as_float(r[j + 1]) - mean) * rstd * __ldg(p.ln_g + n + 1) + __ldg(p.ln_b + n + 1);
-                        pk[j / 2] = pack_bf16x2(a0, a1);
-                    }
-                    if (valid && p.out) {
-                        uint4* dst = reinterpret_cast<uint4*>(arow + c * 32);
-#pragma unroll
-                        for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                    for (int j = 0; j < 32; ++j) {
+                        const float e = __uint_as_float(r[j]) - mean;
+                        sq = fmaf(e, e, sq);
                     }
                 }
+                s_red[half * 128 + rloc].y = sq;
+                named_bar(1 + quarter, 64);
+                const float var = (s_red[rloc].y + s_red[128 + rloc].y) * (1.0f / BN);
+                const float rstd = rsqrtf(var + p.eps);
+                // pass 3: normalise -> bf16
+                if (p.out) {
+                    __nv_bfloat16* arow = p.out + (int64_t)row * p.ldo;
+#pragma unroll 1
+                    for (int c = half; c < NCH; c += 2) {
+                        uint32_t r[32];
+                        tc::tmem_ld32(tbase + c * 32, r);
+                        tc::tmem_ld_wait();
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int j = 0; j < 32; j += 2) {
+                            const int n = c * 32 + j;
+                            const float a0 = (__uint_as_float(r[j]) - mean) * rstd * s_g[n] + s_b[n];
+                            const float a1 = (__uint_as_float(r[j + 1]) - mean) * rstd * s_g[n + 1] + s_b[n + 1];
+                            pk[j / 2] = pack_bf16x2(a0, a1);
+                        }
+                        if (valid) {
+                            uint4* dst = reinterpret_cast<uint4*>(arow + c * 32);
+#pragma unroll
+                            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                        }
+                    }
+                }
+                named_bar(1 + quarter, 64);  // s_red reuse guard for the next tile
             }
             tc::tc_fence_before();
             __syncwarp();
@@ -275,25 +322,35 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int KB>
+template <int BN, int KB, int EPI>
 static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int grid,
                                cudaStream_t s) {
     const int smem = TcSmem<BN, KB>::kBytes;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, KB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_gemm_tc<BN, KB><<<grid, 192, smem, s>>>(a, b, p);
+    k_gemm_tc<BN, KB, EPI><<<grid, kThreads, smem, s>>>(a, b, p);
     return cudaGetLastError();
+}
+
+template <int BN, int KB>
+static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int grid,
+                              cudaStream_t s) {
+    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, p, grid, s);
+    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, p, grid, s);
+    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, p, grid, s);
+    return launch_impl<BN, KB, 0>(a, b, p, grid, s);
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int bn, int kb,
                            int num_sms, cudaStream_t s) {
     // grid: one persistent CTA per SM, a multiple of the number of N tiles
     const int grid = (num_sms / p.n_tiles) * p.n_tiles;
-#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_impl<BN_, KB_>(a, b, p, grid, s);
+    if (p.epi == TC_EPI_BF16 && p.act_silu == 0 && p.bias) return cudaErrorInvalidValue;  // unsupported combo
+#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, p, grid, s);
     TCL_TC_CASE(256, 1) TCL_TC_CASE(256, 2) TCL_TC_CASE(256, 3) TCL_TC_CASE(256, 4)
     TCL_TC_CASE(128, 1) TCL_TC_CASE(128, 2) TCL_TC_CASE(128, 3) TCL_TC_CASE(128, 4)
     TCL_TC_CASE(64, 1) TCL_TC_CASE(64, 2) TCL_TC_CASE(64, 3) TCL_TC_CASE(64, 4)

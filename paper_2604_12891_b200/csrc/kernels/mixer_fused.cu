@@ -1,4 +1,5 @@
-// mixer_fused.cu -- the Mamba mixer of the bf16 path in ONE kernel:
+// mixer_fused.cu -- the Mamba mixer of the bf16 path in ONE persistent kernel
+// (SURVEY §8(a) a5-a7):
 //
 //   u   = SiLU(b_conv + causal depthwise conv_{d_conv}(x))            (R4)
 //   [dt_r | B | C] = u W_x^T                                           (input-dependent selection; R7)
@@ -6,21 +7,27 @@
 //   s_t = exp(Delta A) s_{t-1} + (exp(Delta A) - 1)/A * B_t u_t        (Eqs. 4-5 with ZOH; R5)
 //   y_t = C_t . s_t + D u_t ;  g_t = y_t * SiLU(z_t)                   (R6; gate)
 //
-// One CTA per candidate, one thread per channel d (the N states of channel d live in registers
-// for the whole sequence, never in memory).  The candidate is walked in chunks of 16 tokens:
-//   1. conv + SiLU from a register window of the last d_conv-1 inputs (coalesced bf16 loads of x
-//      and z from the in_proj output), u kept fp32 in shared memory + a bf16 copy for the MMA;
-//   2. x_proj on the tensor cores: mma.sync m16n8k16 (bf16 in, fp32 out) of the 16 x DI chunk
-//      by W_x^T (these contractions are 16 x 48 x 256 and 16 x 256 x 16 per chunk: far too small
-//      for a TMEM accumulator round trip, so the warp-level MMA is the right unit here);
-//   3. dt_proj on the tensor cores, softplus epilogue -> Delta in shared memory;
-//   4. the selective scan (ex2.approx on MUFU, exp(Delta A) = 2^(Delta * A log2 e) with A
-//      pre-scaled at model creation) + D skip + SiLU(z) gate, g written as bf16 for out_proj.
-// Nothing but x, z (in) and g (out) touches HBM.
+// Work decomposition: a persistent CTA of DI threads walks candidates (grid-stride); thread d owns
+// channel d and keeps its N SSM states in registers for the whole sequence.  Each candidate is
+// processed in chunks of 16 tokens:
+//   0. the chunk's 16 rows of the in_proj output [x | z] (bf16, contiguous in the packed layout)
+//      arrive by one TMA bulk copy (cp.async.bulk) into a double buffer; the copy of the NEXT
+//      chunk is issued before this chunk is computed, so HBM latency is hidden;
+//   1. causal conv + SiLU from a register window of the previous d_conv-1 inputs -> u (smem);
+//   2. x_proj on the tensor cores: mma.sync m16n8k16 (bf16 in, fp32 accumulate) of the 16 x DI
+//      chunk by W_x^T (weights staged once per CTA in padded shared memory);
+//   3. dt_proj on the tensor cores (B fragments held in registers for the whole launch) with the
+//      softplus epilogue -> Delta (smem);
+//   4. the selective scan: exp(Delta A) = 2^(Delta * A log2 e) on MUFU.EX2 (A pre-scaled at model
+//      creation); all other arithmetic in packed fp32x2 (FFMA2/FMUL2/FADD2) so that the SFU, not
+//      instruction issue, bounds the loop; D skip; SiLU(z) gate; g stored as bf16.
+// The 16 x 48 x 256 and 16 x 256 x 16 contractions per chunk are far too small for a TMEM
+// accumulator round trip, so the warp-level MMA is the right unit here.
 #include <cuda_bf16.h>
 
 #include "../kernels.h"
 #include "../kernels_mixer.h"
+#include "../tc_ptx.cuh"
 
 namespace tcl {
 
@@ -28,14 +35,17 @@ constexpr int kTC = 16;  // tokens per chunk (= MMA M)
 
 template <int DI, int NXP>
 struct MixerSmem {
-    static constexpr int kUbld = DI + 8;   // bf16 row stride (+16 B: conflict-free fragment loads)
+    static constexpr int kWxld = DI + 8;   // bf16 row stride of W_x (+16 B: conflict-free B fragments)
     static constexpr int kDbcld = NXP + 4;
-    static constexpr int kU = 0;                                   // float [16][DI]
-    static constexpr int kDl = kU + kTC * DI * 4;                  // float [16][DI]
-    static constexpr int kZ = kDl + kTC * DI * 4;                  // bf16  [16][DI]
-    static constexpr int kUb = kZ + kTC * DI * 2;                  // bf16  [16][DI + 8]
-    static constexpr int kDbc = kUb + kTC * kUbld * 2;             // float [16][NXP + 4]
-    static constexpr int kBytes = kDbc + kTC * kDbcld * 4;
+    static constexpr int kUld = DI + 4;
+    static constexpr int kXZ = 0;                                  // bf16 [2][16][2 DI] (TMA bulk dst)
+    static constexpr int kU = kXZ + 2 * kTC * 2 * DI * 2;          // float [16][DI + 4]
+    static constexpr int kDl = kU + kTC * kUld * 4;                // float [16][DI]
+    static constexpr int kDbc = kDl + kTC * DI * 4;                // float [16][NXP + 4]
+    static constexpr int kUb = kDbc + kTC * kDbcld * 4;            // bf16  [16][DI + 8] (MMA A operand)
+    static constexpr int kWx = kUb + kTC * kWxld * 2;              // bf16  [NXP][DI + 8]
+    static constexpr int kBar = kWx + NXP * kWxld * 2;             // 2 mbarriers
+    static constexpr int kBytes = kBar + 16;
 };
 
 __device__ __forceinline__ uint32_t pk_bf16(float a, float b) {
@@ -51,85 +61,159 @@ __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4],
         : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
-template <int DI, int N, int RP, int NXP, int DC>
-__global__ void __launch_bounds__(DI) k_mixer_fused(MixerArgs a) {
+// bf16-path activations: SiLU(v) = v * (0.5 + 0.5 tanh(v/2)) -> one MUFU.TANH.
+__device__ __forceinline__ float silu_fast(float v) {
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
+    return v * fmaf(0.5f, t, 0.5f);
+}
+// softplus(v) = max(v, 0) + log(1 + e^{-|v|}): branch-free, two MUFU ops.
+__device__ __forceinline__ float softplus_fast(float v) {
+    return fmaxf(v, 0.0f) + __logf(1.0f + __expf(-fabsf(v)));
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            tc::smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+        : "memory");
+}
+
+template <int DI, int N, int RP, int NXP, int DC, int DISC>
+__global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
     constexpr int NW = DI / 32;
     using L = MixerSmem<DI, NXP>;
-    extern __shared__ __align__(16) uint8_t msm[];
-    float (*u_s)[DI] = reinterpret_cast<float (*)[DI]>(msm + L::kU);
-    float (*dl_s)[DI] = reinterpret_cast<float (*)[DI]>(msm + L::kDl);
-    __nv_bfloat16 (*z_s)[DI] = reinterpret_cast<__nv_bfloat16 (*)[DI]>(msm + L::kZ);
-    __nv_bfloat16 (*u_b)[L::kUbld] = reinterpret_cast<__nv_bfloat16 (*)[L::kUbld]>(msm + L::kUb);
-    float (*dbc_s)[L::kDbcld] = reinterpret_cast<float (*)[L::kDbcld]>(msm + L::kDbc);
+    extern __shared__ __align__(128) uint8_t msm[];
+    __nv_bfloat16* xz_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kXZ);   // [2][16][2 DI]
+    float* u_s = reinterpret_cast<float*>(msm + L::kU);                       // [16][DI + 4]
+    float* dl_s = reinterpret_cast<float*>(msm + L::kDl);                     // [16][DI]
+    float* dbc_s = reinterpret_cast<float*>(msm + L::kDbc);                   // [16][NXP + 4]
+    __nv_bfloat16* wx_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kWx);    // [NXP][DI + 8]
+    __nv_bfloat16* u_b = reinterpret_cast<__nv_bfloat16*>(msm + L::kUb);     // [16][DI + 8]
+    uint64_t* bar = reinterpret_cast<uint64_t*>(msm + L::kBar);
 
-    const int64_t i = blockIdx.x;
     const int d = threadIdx.x;
     const int warp = d >> 5, lane = d & 31;
     const int g = lane >> 2, tq = lane & 3;
-    const int T = a.lens[i];
-    if (T < 1 || T > a.max_len) return;
-    const int64_t base = a.cu[i];
 
-    // per-channel constants
-    float A2[N], iA[N], s[N];
+    // ---- once per CTA: W_x into padded smem, W_dt fragments into registers, per-channel constants
+    for (int idx = d; idx < NXP * DI / 8; idx += DI) {
+        const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
+        *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
+            __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
+    }
+    constexpr int NT_DT = DI / 8 / NW;  // dt_proj n-tiles per warp
+    uint32_t wdt[NT_DT][RP / 16][2];
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-        A2[n] = __ldg(a.A2 + d * N + n);
-        iA[n] = __ldg(a.invA + d * N + n);
-        s[n] = 0.0f;
+    for (int j = 0; j < NT_DT; ++j) {
+        const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
+#pragma unroll
+        for (int ks = 0; ks < RP / 16; ++ks) {
+            wdt[j][ks][0] = __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 2 * tq));
+            wdt[j][ks][1] = __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 8 + 2 * tq));
+        }
+    }
+    float2 A2[N / 2], iA[N / 2];
+#pragma unroll
+    for (int n = 0; n < N / 2; ++n) {
+        A2[n] = __ldg(reinterpret_cast<const float2*>(a.A2 + d * N) + n);
+        iA[n] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + n);
     }
     const float Dv = __ldg(a.Dv + d);
     const float bconv = __ldg(a.b_conv + d);
     float wc[DC];
 #pragma unroll
     for (int k = 0; k < DC; ++k) wc[k] = __ldg(a.w_conv + d * DC + k);
-    float win[DC];  // x[t-1], x[t-2], ... (window of previous inputs, zero before the candidate)
-#pragma unroll
-    for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+    if (d == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
 
-    for (int t0 = 0; t0 < T; t0 += kTC) {
-        const int tc = min(kTC, T - t0);
-        // ---- 1. conv + SiLU, z staging
+    // ---- chunk iterator over (candidate, t0) for this CTA (grid-stride over candidates)
+    auto first_valid = [&](int64_t i) -> int64_t {
+        for (; i < a.n; i += gridDim.x) {
+            const int T = a.lens[i];
+            if (T >= 1 && T <= a.max_len) return i;
+        }
+        return i;
+    };
+    // issue the copy of chunk (i, t0) into buffer b
+    auto issue = [&](int64_t i, int t0, int b) {
+        if (d == 0 && i < a.n) {
+            const int T = a.lens[i];
+            const int tc = min(kTC, T - t0);
+            const uint32_t bytes = (uint32_t)tc * 2 * DI * 2;
+            tc::mbar_arrive_expect_tx(&bar[b], bytes);
+            bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + (a.cu[i] + t0) * (int64_t)a.ldxz, bytes, &bar[b]);
+        }
+    };
+    int64_t cur_i = first_valid(blockIdx.x);
+    int cur_t0 = 0;
+    issue(cur_i, 0, 0);
+    uint32_t parity = 0;  // bit b = phase parity of buffer b
+    int buf = 0;
+
+    float2 s[N / 2];
+    float win[DC];
+    while (cur_i < a.n) {
+        const int T = a.lens[cur_i];
+        const int64_t base = a.cu[cur_i];
+        if (cur_t0 == 0) {
+#pragma unroll
+            for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+        }
+        const int tc = min(kTC, T - cur_t0);
+        // next chunk in this CTA's sequence -> prefetch into the other buffer
+        int64_t nxt_i = cur_i;
+        int nxt_t0 = cur_t0 + kTC;
+        if (nxt_t0 >= T) { nxt_i = first_valid(cur_i + gridDim.x); nxt_t0 = 0; }
+        issue(nxt_i, nxt_t0, buf ^ 1);
+
+        tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
+        parity ^= 1u << buf;
+        const __nv_bfloat16* xz = xz_s + buf * kTC * 2 * DI;
+
+        // ---- 1. causal conv + SiLU
+#pragma unroll 4
         for (int tt = 0; tt < kTC; ++tt) {
-            float u = 0.0f, z = 0.0f;
+            float u = 0.0f;
             if (tt < tc) {
-                const __nv_bfloat16* xr = a.XZ + (base + t0 + tt) * a.ldxz;
-                const float x = __bfloat162float(xr[d]);
-                z = __bfloat162float(xr[DI + d]);
-                // c = b + sum_k w[k] * x[t - (dc-1) + k]; tap dc-1 is the current token
+                const float x = __bfloat162float(xz[tt * 2 * DI + d]);
                 float acc = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
                 for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
 #pragma unroll
                 for (int k = DC - 1; k > 0; --k) win[k] = win[k - 1];
                 win[0] = x;
-                u = silu(acc);
+                u = silu_fast(acc);
             }
-            u_s[tt][d] = u;
-            z_s[tt][d] = __float2bfloat16_rn(z);
-            u_b[tt][d] = __float2bfloat16_rn(u);
+            u_s[tt * L::kUld + d] = u;
+            u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
         }
         __syncthreads();
-        // ---- 2. x_proj: dbc[16][NXP] = u_b[16][DI] . W_x^T   (warp w -> n-tiles w, w+NW, ...)
+        // ---- 2. x_proj on the tensor cores: dbc[16][NXP] = u[16][DI] . W_x^T
         for (int nt = warp; nt < NXP / 8; nt += NW) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const __nv_bfloat16* wrow = a.Wx_b + (int64_t)(nt * 8 + g) * DI;
+            const __nv_bfloat16* wrow = wx_s + (nt * 8 + g) * L::kWxld;
 #pragma unroll 4
             for (int k0 = 0; k0 < DI; k0 += 16) {
                 uint32_t af[4];
-                af[0] = *reinterpret_cast<const uint32_t*>(&u_b[g][k0 + 2 * tq]);
-                af[1] = *reinterpret_cast<const uint32_t*>(&u_b[g + 8][k0 + 2 * tq]);
-                af[2] = *reinterpret_cast<const uint32_t*>(&u_b[g][k0 + 8 + 2 * tq]);
-                af[3] = *reinterpret_cast<const uint32_t*>(&u_b[g + 8][k0 + 8 + 2 * tq]);
-                const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 2 * tq));
-                const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 8 + 2 * tq));
+                af[0] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 2 * tq);
+                af[1] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 2 * tq);
+                af[2] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 8 + 2 * tq);
+                af[3] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 8 + 2 * tq);
+                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 2 * tq);
+                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 8 + 2 * tq);
                 mma_16816(acc, af, b0, b1);
             }
             const int c = nt * 8 + 2 * tq;
-            dbc_s[g][c] = acc[0];
-            dbc_s[g][c + 1] = acc[1];
-            dbc_s[g + 8][c] = acc[2];
-            dbc_s[g + 8][c + 1] = acc[3];
+            *reinterpret_cast<float2*>(dbc_s + g * L::kDbcld + c) = make_float2(acc[0], acc[1]);
+            *reinterpret_cast<float2*>(dbc_s + (g + 8) * L::kDbcld + c) = make_float2(acc[2], acc[3]);
         }
         __syncthreads();
         // ---- 3. dt_proj + softplus: dl[16][DI] = softplus(dt_r[16][RP] . W_dt^T + b_dt)
@@ -139,8 +223,8 @@ __global__ void __launch_bounds__(DI) k_mixer_fused(MixerArgs a) {
             for (int ks = 0; ks < RP / 16; ++ks) {
                 const int k0 = ks * 16;
                 auto ld2 = [&](int r, int k) -> uint32_t {
-                    const float v0 = (k < a.R) ? dbc_s[r][k] : 0.0f;
-                    const float v1 = (k + 1 < a.R) ? dbc_s[r][k + 1] : 0.0f;
+                    const float v0 = (k < a.R) ? dbc_s[r * L::kDbcld + k] : 0.0f;
+                    const float v1 = (k + 1 < a.R) ? dbc_s[r * L::kDbcld + k + 1] : 0.0f;
                     return pk_bf16(v0, v1);
                 };
                 af[ks][0] = ld2(g, k0 + 2 * tq);
@@ -148,98 +232,117 @@ __global__ void __launch_bounds__(DI) k_mixer_fused(MixerArgs a) {
                 af[ks][2] = ld2(g, k0 + 8 + 2 * tq);
                 af[ks][3] = ld2(g + 8, k0 + 8 + 2 * tq);
             }
-            for (int nt = warp; nt < DI / 8; nt += NW) {
-                float acc[4] = {0.f, 0.f, 0.f, 0.f};
-                const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)(nt * 8 + g) * RP;
 #pragma unroll
-                for (int ks = 0; ks < RP / 16; ++ks) {
-                    const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 2 * tq));
-                    const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 8 + 2 * tq));
-                    mma_16816(acc, af[ks], b0, b1);
-                }
-                const int c = nt * 8 + 2 * tq;
+            for (int j = 0; j < NT_DT; ++j) {
+                float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+                for (int ks = 0; ks < RP / 16; ++ks) mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
+                const int c = (warp + j * NW) * 8 + 2 * tq;
                 const float b0v = __ldg(a.b_dt + c), b1v = __ldg(a.b_dt + c + 1);
-                dl_s[g][c] = softplus(acc[0] + b0v);
-                dl_s[g][c + 1] = softplus(acc[1] + b1v);
-                dl_s[g + 8][c] = softplus(acc[2] + b0v);
-                dl_s[g + 8][c + 1] = softplus(acc[3] + b1v);
+                *reinterpret_cast<float2*>(dl_s + g * DI + c) =
+                    make_float2(softplus_fast(acc[0] + b0v), softplus_fast(acc[1] + b1v));
+                *reinterpret_cast<float2*>(dl_s + (g + 8) * DI + c) =
+                    make_float2(softplus_fast(acc[2] + b0v), softplus_fast(acc[3] + b1v));
             }
         }
         __syncthreads();
-        // ---- 4. selective scan + D skip + gate
+        // ---- 4. selective scan + D skip + gate (packed fp32x2 arithmetic, MUFU.EX2 for exp)
+        __nv_bfloat16* gout = a.G + base * a.ldg + d;
         for (int tt = 0; tt < tc; ++tt) {
-            const float u = u_s[tt][d];
-            const float dl = dl_s[tt][d];
-            const float z = __bfloat162float(z_s[tt][d]);
-            const float* Bt = &dbc_s[tt][a.R];
-            const float* Ct = Bt + N;
-            float y = 0.0f;
-            if (a.disc == 1) {
-                const float du = dl * u;
+            const float u = u_s[tt * L::kUld + d];
+            const float dl = dl_s[tt * DI + d];
+            const float z = __bfloat162float(xz[tt * 2 * DI + DI + d]);
+            const float4* B4 = reinterpret_cast<const float4*>(dbc_s + tt * L::kDbcld + a.R);
+            const float4* C4 = reinterpret_cast<const float4*>(dbc_s + tt * L::kDbcld + a.R + N);
+            const float2 dl2 = make_float2(dl, dl);
+            const float2 u2 = make_float2(u, u);
+            float2 y2 = make_float2(0.f, 0.f), y2b = make_float2(0.f, 0.f);
+            if (DISC == 1) {
+                const float2 du2 = __fmul2_rn(dl2, u2);
 #pragma unroll
-                for (int n = 0; n < N; ++n) {
-                    const float Ab = ex2(dl * A2[n]);
-                    s[n] = fmaf(Ab, s[n], du * Bt[n]);
-                    y = fmaf(Ct[n], s[n], y);
+                for (int q = 0; q < N / 4; ++q) {
+                    const float4 b4 = B4[q], c4 = C4[q];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = 2 * q + h;
+                        const float2 x2 = __fmul2_rn(dl2, A2[n]);
+                        const float2 ab = make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
+                        const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+                        s[n] = __ffma2_rn(ab, s[n], __fmul2_rn(bb, du2));
+                        if (h) y2b = __ffma2_rn(cc, s[n], y2b); else y2 = __ffma2_rn(cc, s[n], y2);
+                    }
                 }
             } else {
 #pragma unroll
-                for (int n = 0; n < N; ++n) {
-                    const float Ab = ex2(dl * A2[n]);
-                    const float v = (Bt[n] * u) * iA[n];
-                    s[n] = fmaf(Ab, s[n] + v, -v);
-                    y = fmaf(Ct[n], s[n], y);
+                for (int q = 0; q < N / 4; ++q) {
+                    const float4 b4 = B4[q], c4 = C4[q];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = 2 * q + h;
+                        const float2 x2 = __fmul2_rn(dl2, A2[n]);
+                        const float2 ab = make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
+                        const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+                        // Bbar u = (Ab - 1) v with v = B u / A;  s <- Ab (s + v) - v
+                        const float2 v = __fmul2_rn(__fmul2_rn(bb, u2), iA[n]);
+                        const float2 t = __fadd2_rn(s[n], v);
+                        s[n] = __ffma2_rn(ab, t, make_float2(-v.x, -v.y));
+                        if (h) y2b = __ffma2_rn(cc, s[n], y2b); else y2 = __ffma2_rn(cc, s[n], y2);
+                    }
                 }
             }
-            y = fmaf(Dv, u, y);
-            a.G[(base + t0 + tt) * a.ldg + d] = __float2bfloat16_rn(y * silu(z));
+            const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
+            gout[(int64_t)(cur_t0 + tt) * a.ldg] = __float2bfloat16_rn(y * silu_fast(z));
         }
         __syncthreads();
+        buf ^= 1;
+        cur_i = nxt_i;
+        cur_t0 = nxt_t0;
     }
 }
 
-template <int DI, int N, int RP, int NXP, int DC>
-static cudaError_t mixer_launch_dc(const MixerArgs& a, cudaStream_t s) {
+template <int DI, int N, int RP, int NXP, int DC, int DISC>
+static cudaError_t mixer_launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
     constexpr int smem = MixerSmem<DI, NXP>::kBytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_mixer_fused<DI, N, RP, NXP, DC>,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC>;
+    static int blocks_per_sm = 0;
+    if (!blocks_per_sm) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, DI, smem);
+        if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
     }
-    k_mixer_fused<DI, N, RP, NXP, DC><<<(unsigned)a.n, DI, smem, s>>>(a);
+    int64_t grid = (int64_t)num_sms * blocks_per_sm;
+    if (grid > a.n) grid = a.n;
+    kern<<<(unsigned)grid, DI, smem, s>>>(a);
     return cudaGetLastError();
 }
 
 template <int DI, int N, int RP, int NXP>
-static cudaError_t mixer_launch(const MixerArgs& a, cudaStream_t s) {
-    switch (a.d_conv) {
-        case 4: return mixer_launch_dc<DI, N, RP, NXP, 4>(a, s);
-        case 3: return mixer_launch_dc<DI, N, RP, NXP, 3>(a, s);
-        case 2: return mixer_launch_dc<DI, N, RP, NXP, 2>(a, s);
-        default: return cudaErrorInvalidValue;
-    }
+static cudaError_t mixer_launch(const MixerArgs& a, int num_sms, cudaStream_t s) {
+    if (a.d_conv != 4) return cudaErrorInvalidValue;  // validated on the host
+    return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1>(a, num_sms, s)
+                       : mixer_launch_k<DI, N, RP, NXP, 4, 0>(a, num_sms, s);
 }
 
 template <int DI, int N>
-static cudaError_t mixer_rp(const MixerArgs& a, cudaStream_t s) {
+static cudaError_t mixer_rp(const MixerArgs& a, int num_sms, cudaStream_t s) {
     const int nxp = ((a.R + 2 * N) + 7) / 8 * 8;
     if (a.RP == 16) {
-        if (nxp <= 24) return mixer_launch<DI, N, 16, 24>(a, s);
-        if (nxp <= 48) return mixer_launch<DI, N, 16, 48>(a, s);
+        if (nxp <= 24) return mixer_launch<DI, N, 16, 24>(a, num_sms, s);
+        if (nxp <= 48) return mixer_launch<DI, N, 16, 48>(a, num_sms, s);
     } else if (a.RP == 32) {
-        if (nxp <= 48) return mixer_launch<DI, N, 32, 48>(a, s);
-        if (nxp <= 64) return mixer_launch<DI, N, 32, 64>(a, s);
+        if (nxp <= 64) return mixer_launch<DI, N, 32, 64>(a, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_mixer_fused(const MixerArgs& a, cudaStream_t s) {
+cudaError_t launch_mixer_fused(const MixerArgs& a, int num_sms, cudaStream_t s) {
     if (a.n == 0) return cudaSuccess;
-    if (a.DI == 256) return a.N == 16 ? mixer_rp<256, 16>(a, s) : mixer_rp<256, 8>(a, s);
-    if (a.DI == 128) return a.N == 16 ? mixer_rp<128, 16>(a, s) : mixer_rp<128, 8>(a, s);
-    if (a.DI == 64) return a.N == 16 ? mixer_rp<64, 16>(a, s) : mixer_rp<64, 8>(a, s);
+    if (a.DI == 256) return a.N == 16 ? mixer_rp<256, 16>(a, num_sms, s) : mixer_rp<256, 8>(a, num_sms, s);
+    if (a.DI == 128) return a.N == 16 ? mixer_rp<128, 16>(a, num_sms, s) : mixer_rp<128, 8>(a, num_sms, s);
+    if (a.DI == 64) return a.N == 16 ? mixer_rp<64, 16>(a, num_sms, s) : mixer_rp<64, 8>(a, num_sms, s);
     return cudaErrorInvalidValue;
 }
 

@@ -9,50 +9,56 @@
 
 namespace tcl {
 
-// One block of 1024 threads; each thread scans a contiguous strip of lengths.
+// One block of 1024 threads walks the lengths in coalesced tiles of 4096 (int4 per thread):
+// block-wide exclusive scan per tile + running carry.  Invalid lengths count as 0 rows.
 __global__ void __launch_bounds__(1024) k_lens_prefix(const int32_t* __restrict__ lens, int64_t n,
                                                       int32_t max_len, int32_t* __restrict__ cu,
                                                       int* __restrict__ err) {
     __shared__ int32_t warp_tot[32];
-    const int tid = threadIdx.x;
-    const int64_t per = (n + 1023) / 1024;
-    const int64_t lo = tid * per, hi = min(n, lo + per);
-    int32_t local = 0;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int32_t carry = 0;
     bool bad = false;
-    for (int64_t i = lo; i < hi; ++i) {
-        int32_t T = lens[i];
-        bool ok = (T >= 1 && T <= max_len);
-        bad |= !ok;
-        local += ok ? T : 0;
-    }
-    if (bad) atomicOr(err, ERR_LEN);
-    // block exclusive scan of `local`
-    const int lane = tid & 31, wid = tid >> 5;
-    int32_t v = local;
+    for (int64_t base = 0; base < n; base += 4096) {
+        int32_t v[4];
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        int32_t t = __shfl_up_sync(0xffffffffu, v, o);
-        if (lane >= o) v += t;
-    }
-    if (lane == 31) warp_tot[wid] = v;
-    __syncthreads();
-    if (wid == 0) {
-        int32_t w = warp_tot[lane];
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = base + tid * 4 + j;
+            int32_t T = i < n ? lens[i] : 1;
+            const bool ok = T >= 1 && T <= max_len;
+            bad |= (i < n) && !ok;
+            v[j] = (i < n && ok) ? T : 0;
+        }
+        const int32_t local = v[0] + v[1] + v[2] + v[3];
+        int32_t x = local;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            int32_t t = __shfl_up_sync(0xffffffffu, w, o);
-            if (lane >= o) w += t;
+            const int32_t t = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += t;
         }
-        warp_tot[lane] = w;  // inclusive
+        if (lane == 31) warp_tot[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+            int32_t w = warp_tot[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t t = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += t;
+            }
+            warp_tot[lane] = w;  // inclusive
+        }
+        __syncthreads();
+        int32_t run = carry + (x - local) + (wid > 0 ? warp_tot[wid - 1] : 0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int64_t i = base + tid * 4 + j;
+            if (i < n) cu[i] = run;
+            run += v[j];
+        }
+        carry += warp_tot[31];
+        __syncthreads();
     }
-    __syncthreads();
-    int32_t run = v - local + (wid > 0 ? warp_tot[wid - 1] : 0);
-    for (int64_t i = lo; i < hi; ++i) {
-        cu[i] = run;
-        int32_t T = lens[i];
-        run += (T >= 1 && T <= max_len) ? T : 0;
-    }
-    if (tid == 1023) cu[n] = warp_tot[31];
+    if (bad) atomicOr(err, ERR_LEN);
+    if (tid == 0) cu[n] = carry;
 }
 
 void launch_lens_prefix(const int32_t* lens, int64_t n, int32_t max_len, int32_t* cu, int* err,
@@ -60,36 +66,37 @@ void launch_lens_prefix(const int32_t* lens, int64_t n, int32_t max_len, int32_t
     k_lens_prefix<<<1, 1024, 0, s>>>(lens, n, max_len, cu, err);
 }
 
-// One warp per padded slot (i, t): lanes copy the d_in columns when t < T_i.
+// One warp per candidate: lane c copies column c of each real row (padded slots never read).
 __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
                                               const int32_t* __restrict__ lens,
                                               const int32_t* __restrict__ cu, int64_t n, int L,
                                               int d_in, int ldx, float* __restrict__ X,
                                               __nv_bfloat16* __restrict__ Xb,
                                               int32_t* __restrict__ row_cand) {
-    const int64_t slot = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (slot >= n * L) return;
-    const int64_t i = slot / L;
-    const int t = (int)(slot - i * L);
+    if (i >= n) return;
     const int32_t T = lens[i];
-    if (T < 1 || T > L || t >= T) return;
-    const int64_t row = cu[i] + t;
-    const float* src = feats + slot * d_in;
-    for (int c = lane; c < ldx; c += 32) {
-        float v = c < d_in ? __ldg(src + c) : 0.0f;
-        if (X) X[row * ldx + c] = v;
-        if (Xb) Xb[row * ldx + c] = __float2bfloat16_rn(v);
+    if (T < 1 || T > L) return;
+    const int64_t row0 = cu[i];
+    const float* src = feats + i * (int64_t)L * d_in;
+#pragma unroll 4
+    for (int t = 0; t < T; ++t) {
+        const int64_t row = row0 + t;
+        for (int c = lane; c < ldx; c += 32) {
+            const float v = c < d_in ? __ldg(src + t * d_in + c) : 0.0f;
+            if (X) X[row * ldx + c] = v;
+            if (Xb) Xb[row * ldx + c] = __float2bfloat16_rn(v);
+        }
+        if (lane == 0) row_cand[row] = (int32_t)i;
     }
-    if (lane == 0) row_cand[row] = (int32_t)i;
 }
 
 void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int64_t n, int L,
                  int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s) {
-    int64_t slots = n * L;
-    if (slots == 0) return;
-    k_pack<<<(unsigned)((slots + 7) / 8), 256, 0, s>>>(feats, lens, cu, n, L, d_in, ldx, X,
-                                                       (__nv_bfloat16*)x_bf16, row_cand);
+    if (n == 0) return;
+    k_pack<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(feats, lens, cu, n, L, d_in, ldx, X,
+                                                   (__nv_bfloat16*)x_bf16, row_cand);
 }
 
 }  // namespace tcl

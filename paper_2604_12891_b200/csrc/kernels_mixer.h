@@ -22,6 +22,6 @@ struct MixerArgs {
     int DI, N, R, RP, d_conv, disc, max_len;
 };
 
-cudaError_t launch_mixer_fused(const MixerArgs& a, cudaStream_t s);
+cudaError_t launch_mixer_fused(const MixerArgs& a, int num_sms, cudaStream_t s);
 
 }  // namespace tcl

@@ -123,6 +123,14 @@ def _stream(stream) -> Optional[int]:
     return stream.cuda_stream
 
 
+def shard_range(n_global: int, world: int, rank: int) -> Tuple[int, int]:
+    """Contiguous candidate shard of `rank`: [start, start + count), with
+    start = rank * ceil(n / world); the global index of local candidate i is start + i."""
+    per = -(-n_global // world) if world > 0 else 0
+    start = min(n_global, rank * per)
+    return start, max(0, min(n_global, start + per) - start)
+
+
 def tcl_weights_count(dims) -> int:
     return int(load().tcl_weights_count(ctypes.byref(tcl_dims.of(dims))))
 
