@@ -171,7 +171,7 @@ def run_reference(args, cfg, d, n, k, world, rank):
     from oracle import oracle as O
     O.build()
     w = inputs.make_weights(d, cfg["seed"])
-    sample = args.cpu_sample or {"tiny": 256, "tuning": 512, "rdu": 64, "paper": 256}.get(args.config, 64)
+    sample = args.cpu_sample or {"tiny": 256, "tuning": 512, "rdu": 64, "paper": 256}.get(args.config, 256)
     sample = min(sample, n)
     f, l = inputs.make_features(d, sample, cfg["seed"] + 1, workload=FEATURE_WORKLOAD[args.config])
     cores = O.default_threads()
@@ -363,8 +363,9 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     if world == 1 and rank == 0 and not args.no_cpu_baseline:
         from oracle import oracle as O
         O.build()
-        sample = args.cpu_sample or {"tiny": 256, "tuning": 1024, "rdu": 128, "large": 1024,
-                                     "long": 256, "paper": 512}[args.config]
+        # bounded sample: ~10-20 s of CPU work on the GPU box's host cores
+        sample = args.cpu_sample or {"tiny": 256, "tuning": 4096, "rdu": 512, "large": 6144,
+                                     "long": 1536, "paper": 4096}[args.config]
         sample = min(sample, n)
         cores = O.default_threads()
         t0 = time.perf_counter()

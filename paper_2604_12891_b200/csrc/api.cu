@@ -164,7 +164,7 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
     cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
     m->nxp = round_up(R + 2 * N, 8);
     m->rp = R <= 16 ? 16 : 32;
-    m->bn_in = std::min(256, 2 * di);
+    m->bn_in = std::min(128, 2 * di);  // 4 N tiles at di = 256: B slice 64 KB, 8-stage A ring
     HostW h = host_offsets(d, wh);
     if ((st = upload_bf16(m, h.W1, e1, d.d_in, e1, kXld, &m->W1b)) != TCL_OK) return st;
     if ((st = upload_bf16(m, h.W2, e2, e1, e2, e1, &m->W2b)) != TCL_OK) return st;
@@ -443,7 +443,12 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
             a.cu = w.cu; a.lens = lens; a.n = n;
             a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
-            if ((e = launch_mixer_fused(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "mixer");
+            static const int mixer_kind = [] {
+                const char* v = getenv("TCL_MIXER");   // "ws": warp-specialised variant
+                return (v && std::string(v) == "ws") ? 1 : 0;
+            }();
+            e = (mixer_kind == 1 && di >= 128) ? launch_mixer_ws(a, m->num_sms, s) : launch_mixer_fused(a, m->num_sms, s);
+            if (e != cudaSuccess) return cuda_error(e, "mixer");
             ++nl;
             if (debug_sync("mixer", s) != TCL_OK) return TCL_ECUDA;
         }

@@ -164,10 +164,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int m = m_first; m < num_m; m += m_step) {
-            tc::mbar_wait(&tfull[acc], acc_phase);
-            tc::tc_fence_after();
             const int row = m * kBM + rloc;
             const bool valid = row < rows;
+            // residual stream: prefetch this row's first H chunk before waiting for the MMAs
+            float4 hn[8];
+            if constexpr (EPI == 3) {
+                if (p.residual && valid) {
+                    const float4* h4 = reinterpret_cast<const float4*>(p.H + (int64_t)row * p.ldh + half * 32);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) hn[q] = h4[q];
+                } else {
+#pragma unroll
+                    for (int q = 0; q < 8; ++q) hn[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+            }
+            tc::mbar_wait(&tfull[acc], acc_phase);
+            tc::tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if constexpr (EPI != 3) {
                 int cand = 0, token = 0;
@@ -208,16 +220,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
                     float hv[32];
-                    if (p.residual && valid) {
-                        const float4* h4 = reinterpret_cast<const float4*>(hrow + c * 32);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 h = h4[q];
-                            hv[4 * q] = h.x; hv[4 * q + 1] = h.y; hv[4 * q + 2] = h.z; hv[4 * q + 3] = h.w;
-                        }
-                    } else {
+                    for (int q = 0; q < 8; ++q) {
+                        hv[4 * q] = hn[q].x; hv[4 * q + 1] = hn[q].y; hv[4 * q + 2] = hn[q].z; hv[4 * q + 3] = hn[q].w;
+                    }
+                    if (p.residual && valid && c + 2 < NCH) {  // prefetch the next chunk
+                        const float4* h4 = reinterpret_cast<const float4*>(hrow + (c + 2) * 32);
 #pragma unroll
-                        for (int j = 0; j < 32; ++j) hv[j] = 0.0f;
+                        for (int q = 0; q < 8; ++q) hn[q] = h4[q];
                     }
                     tc::tmem_ld_wait();
 #pragma unroll

@@ -23,5 +23,7 @@ struct MixerArgs {
 };
 
 cudaError_t launch_mixer_fused(const MixerArgs& a, int num_sms, cudaStream_t s);
+// Warp-specialised variant (producer warps: TMA + conv + x/dt_proj; scan warps: the recurrence).
+cudaError_t launch_mixer_ws(const MixerArgs& a, int num_sms, cudaStream_t s);
 
 }  // namespace tcl
