@@ -398,7 +398,8 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
             "clocks": clk,
             "kernels": kernels,
             "peaks": {"hbm_gbs": peaks["hbm"], "bf16_tflops": peaks["bf16"], "ex2_per_s": mb["ex2"],
-                      "ffma_per_s": mb["ffma"], "source": peaks["source"], "issue_source": mb["source"]},
+                      "ffma_per_s": mb["ffma"], "ffma2_lanes_per_s": mb.get("ffma2"),
+                      "tanh_per_s": mb.get("tanh"), "source": peaks["source"], "issue_source": mb["source"]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -425,8 +426,11 @@ def measured_issue_peaks():
         L.tclmb_run.argtypes = [ctypes.c_int, ctypes.c_int]
         ex2 = L.tclmb_run(0, 4096)
         ffma = L.tclmb_run(1, 8192)
+        ffma2 = L.tclmb_run(2, 8192)
+        tanh = L.tclmb_run(3, 4096)
         if ex2 > 0 and ffma > 0:
-            _MB = {"ex2": ex2, "ffma": ffma, "source": "measured (microbench: 148x8 CTAs x 256 thr, 8 chains)"}
+            _MB = {"ex2": ex2, "ffma": ffma, "ffma2": ffma2, "tanh": tanh,
+                   "source": "measured (microbench: 148x8 CTAs x 256 thr, 8 chains)"}
             return _MB
     except OSError:
         pass

@@ -245,6 +245,10 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
                   make_tmap_bf16(&w.tmE2b, E2b, e2, rows, (uint64_t)e2 * 2, 64, 128) &&
                   make_tmap_bf16(&w.tmAb, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128) &&
                   make_tmap_bf16(&w.tmGb, w.Gb, di, rows, (uint64_t)di * 2, 64, 128);
+        // output maps (only used when the output tile is >= 64 columns wide)
+        if (e1 >= 64) ok = ok && make_tmap_bf16(&w.tmE1o, E1b, e1, rows, (uint64_t)e1 * 2, 64, 32);
+        if (e2 >= 64) ok = ok && make_tmap_bf16(&w.tmE2o, E2b, e2, rows, (uint64_t)e2 * 2, 64, 32);
+        ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
@@ -407,11 +411,11 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         TcGemmParams p = base();
         p.epi = TC_EPI_BF16; p.bias = m->wp.enc_b1; p.act_silu = 1; p.out = E1b; p.ldo = e1;
         p.drop.enabled = drop.enabled; p.site = 0;
-        if ((e = launch_gemm_tc(w.tmXb, m->tmW1, p, e1, 1, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc1");
+        if ((e = launch_gemm_tc(w.tmXb, m->tmW1, w.tmE1o, p, e1, 1, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc1");
         ++nl;
         if (debug_sync("enc1", s) != TCL_OK) return TCL_ECUDA;
         p.bias = m->wp.enc_b2; p.out = E2b; p.ldo = e2; p.site = 1;
-        if ((e = launch_gemm_tc(w.tmE1b, m->tmW2, p, e2, kb_of(e1), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc2");
+        if ((e = launch_gemm_tc(w.tmE1b, m->tmW2, w.tmE2o, p, e2, kb_of(e1), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc2");
         ++nl;
         if (debug_sync("enc2", s) != TCL_OK) return TCL_ECUDA;
         TcGemmParams q = base();
@@ -419,7 +423,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         q.out = d.n_layer > 0 ? w.Ab : nullptr; q.ldo = dm;
         q.ln_g = d.n_layer > 0 ? m->wp.layers[0].ln_w : m->wp.lnf_w;
         q.ln_b = d.n_layer > 0 ? m->wp.layers[0].ln_b : m->wp.lnf_b;
-        if ((e = launch_gemm_tc(w.tmE2b, m->tmW3, q, dm, kb_of(e2), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc3");
+        if ((e = launch_gemm_tc(w.tmE2b, m->tmW3, w.tmXZo, q, dm, kb_of(e2), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc3");
         ++nl;
         if (debug_sync("enc3", s) != TCL_OK) return TCL_ECUDA;
     }
@@ -429,7 +433,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            if ((e = launch_gemm_tc(w.tmAb, m->tmWin[l], p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
+            if ((e = launch_gemm_tc(w.tmAb, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "in_proj");
             ++nl;
             if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;
@@ -460,7 +464,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             p.out = last ? nullptr : w.Ab; p.ldo = dm;
             p.ln_g = last ? m->wp.lnf_w : m->wp.layers[l + 1].ln_w;
             p.ln_b = last ? m->wp.lnf_b : m->wp.layers[l + 1].ln_b;
-            if ((e = launch_gemm_tc(w.tmGb, m->tmWout[l], p, dm, kb_of(di), m->num_sms, s)) != cudaSuccess)
+            if ((e = launch_gemm_tc(w.tmGb, m->tmWout[l], w.tmXZo, p, dm, kb_of(di), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "out_proj");
             ++nl;
             if (debug_sync("out_proj", s) != TCL_OK) return TCL_ECUDA;

@@ -49,7 +49,8 @@ struct Workspace {
     __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden
     __nv_bfloat16* Ab = nullptr;   // [rows][dm]    LN_l(H)
     __nv_bfloat16* Gb = nullptr;   // [rows][di]    gated scan output
-    CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;
+    CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
+    CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
     std::vector<void*> allocs;
 };
 

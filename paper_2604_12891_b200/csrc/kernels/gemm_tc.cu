@@ -27,14 +27,17 @@ constexpr int kABytes = kBM * 128;  // one 128 x 64 bf16 K-block of A
 constexpr int kEpiWarps = 8;        // two warps per TMEM lane quarter (column halves)
 constexpr int kThreads = 64 + 32 * kEpiWarps;
 
-template <int BN, int KB>
+template <int BN, int KB, int EPI>
 struct TcSmem {
+    static constexpr bool kTmaStore = EPI < 3 && BN >= 128;          // bf16 out through TMA stores
+    static constexpr int kStgBytes = kTmaStore ? kEpiWarps * 2 * 32 * 128 : 0;  // 2 x [32 rows][128 B] per warp
     static constexpr int kBBytes = KB * BN * 128;
-    static constexpr int kStagesRaw = (200 * 1024 - kBBytes) / kABytes;
+    static constexpr int kStagesRaw = (200 * 1024 - kBBytes - kStgBytes) / kABytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
     static constexpr int kOffB = 0;
     static constexpr int kOffA = kOffB + kBBytes;
-    static constexpr int kOffPar = kOffA + kStages * kABytes;         // bias, ln_g, ln_b  [3][BN] fp32
+    static constexpr int kOffStg = kOffA + kStages * kABytes;         // 1024-aligned (swizzled staging)
+    static constexpr int kOffPar = kOffStg + kStgBytes;               // bias, ln_g, ln_b  [3][BN] fp32
     static constexpr int kOffRed = kOffPar + 3 * BN * 4;              // LN partials [2][128] float2
     static constexpr int kOffBar = kOffRed + 2 * 128 * 8;
     static constexpr int kBytes = kOffBar + 256 + 1024;               // + barriers, + alignment slack
@@ -60,8 +63,9 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 template <int BN, int KB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
+                                                         const __grid_constant__ CUtensorMap tmC,
                                                          const TcGemmParams p) {
-    using S = TcSmem<BN, KB>;
+    using S = TcSmem<BN, KB, EPI>;
     constexpr int kStages = S::kStages;
     constexpr int NCH = BN / 32;  // 32-column chunks of the accumulator
     extern __shared__ uint8_t smem_raw[];
@@ -163,6 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
         const int rloc = quarter * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
+        uint32_t groups = 0;  // TMA-store groups issued by this warp (staging double buffer)
         for (int m = m_first; m < num_m; m += m_step) {
             const int row = m * kBM + rloc;
             const bool valid = row < rows;
@@ -185,8 +190,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                 int cand = 0, token = 0;
                 if (EPI == 2 && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
                 __nv_bfloat16* orow = p.out + (int64_t)row * p.ldo + n_tile * BN;
+                // S::kTmaStore: this warp owns the contiguous columns [half*BN/2, (half+1)*BN/2),
+                // staged 64 columns at a time in a 128B-swizzled [32 rows][128 B] buffer, stored by TMA.
+                constexpr int C0 = S::kTmaStore ? 1 : 2;   // chunk stride
 #pragma unroll 1
-                for (int c = half; c < NCH; c += 2) {
+                for (int k = 0; k < (S::kTmaStore ? NCH / 2 : (NCH + 1 - half) / 2); ++k) {
+                    const int c = S::kTmaStore ? half * (NCH / 2) + k : half + k * C0;
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
                     tc::tmem_ld_wait();
@@ -205,7 +214,35 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         }
                         pk[j / 2] = pack_bf16x2(v0, v1);
                     }
-                    if (valid) {
+                    if constexpr (S::kTmaStore) {
+                        // chunk parity picks the 64-byte half of the 128-byte staged row
+                        const int buf = groups & 1;
+                        uint8_t* stg = smem + S::kOffStg + ((warp - 2) * 2 + buf) * (32 * 128);
+                        if ((k & 1) == 0 && groups >= 2) {  // buffer reuse: its store must have read smem
+                            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                            __syncwarp();
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const int piece = (k & 1) * 4 + q;              // 16-byte piece of the 128-byte row
+                            const int sw = piece ^ (lane & 7);
+                            *reinterpret_cast<uint4*>(stg + lane * 128 + sw * 16) =
+                                make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+                        }
+                        if (k & 1) {
+                            tc::fence_proxy_async();
+                            __syncwarp();
+                            if (lane == 0) {
+                                asm volatile(
+                                    "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
+                                    ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(n_tile * BN + (c - 1) * 32),
+                                    "r"(m * kBM + quarter * 32), "r"(tc::smem_u32(stg))
+                                    : "memory");
+                                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                            }
+                            ++groups;
+                        }
+                    } else if (valid) {
                         uint4* dst = reinterpret_cast<uint4*>(orow + c * 32);
 #pragma unroll
                         for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
@@ -297,6 +334,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
             if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
     }
+    if constexpr (S::kTmaStore) {
+        if (warp >= 2 && lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+    }
     tc::tc_fence_before();
     __syncthreads();
     if (warp == 1) {
@@ -333,34 +373,34 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 }
 
 template <int BN, int KB, int EPI>
-static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int grid,
-                               cudaStream_t s) {
-    const int smem = TcSmem<BN, KB>::kBytes;
+static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                               const TcGemmParams& p, int grid, cudaStream_t s) {
+    const int smem = TcSmem<BN, KB, EPI>::kBytes;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, KB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_gemm_tc<BN, KB, EPI><<<grid, kThreads, smem, s>>>(a, b, p);
+    k_gemm_tc<BN, KB, EPI><<<grid, kThreads, smem, s>>>(a, b, c, p);
     return cudaGetLastError();
 }
 
 template <int BN, int KB>
-static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int grid,
-                              cudaStream_t s) {
-    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, p, grid, s);
-    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, p, grid, s);
-    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, p, grid, s);
-    return launch_impl<BN, KB, 0>(a, b, p, grid, s);
+static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                              const TcGemmParams& p, int grid, cudaStream_t s) {
+    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
+    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
+    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
+    return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);
 }
 
-cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int bn, int kb,
-                           int num_sms, cudaStream_t s) {
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s) {
     // grid: one persistent CTA per SM, a multiple of the number of N tiles
     const int grid = (num_sms / p.n_tiles) * p.n_tiles;
     if (p.epi == TC_EPI_BF16 && p.act_silu == 0 && p.bias) return cudaErrorInvalidValue;  // unsupported combo
-#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, p, grid, s);
+#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, c, p, grid, s);
     TCL_TC_CASE(256, 1) TCL_TC_CASE(256, 2) TCL_TC_CASE(256, 3) TCL_TC_CASE(256, 4)
     TCL_TC_CASE(128, 1) TCL_TC_CASE(128, 2) TCL_TC_CASE(128, 3) TCL_TC_CASE(128, 4)
     TCL_TC_CASE(64, 1) TCL_TC_CASE(64, 2) TCL_TC_CASE(64, 3) TCL_TC_CASE(64, 4)

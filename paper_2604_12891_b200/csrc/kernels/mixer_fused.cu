@@ -25,6 +25,8 @@
 // accumulator round trip, so the warp-level MMA is the right unit here.
 #include <cuda_bf16.h>
 
+#include <cstdlib>
+
 #include "../kernels.h"
 #include "../kernels_mixer.h"
 #include "../tc_ptx.cuh"
@@ -33,7 +35,7 @@ namespace tcl {
 
 constexpr int kTC = 16;  // tokens per chunk (= MMA M)
 
-template <int DI, int NXP>
+template <int DI, int NXP, int OCC>
 struct MixerSmem {
     static constexpr int kWxld = DI + 8;   // bf16 row stride of W_x (+16 B: conflict-free B fragments)
     static constexpr int kDbcld = NXP + 4;
@@ -44,7 +46,7 @@ struct MixerSmem {
     static constexpr int kDbc = kDl + kTC * DI * 4;                // float [16][NXP + 4]
     static constexpr int kUb = kDbc + kTC * kDbcld * 4;            // bf16  [16][DI + 8] (MMA A operand)
     static constexpr int kWx = kUb + kTC * kWxld * 2;              // bf16  [NXP][DI + 8]
-    static constexpr int kBar = kWx + NXP * kWxld * 2;             // 2 mbarriers
+    static constexpr int kBar = OCC == 2 ? kWx + NXP * kWxld * 2 : kUb;  // 2 mbarriers
     static constexpr int kBytes = kBar + 16;
 };
 
@@ -80,10 +82,12 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC>
-__global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC>
+__global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
+    // OCC == 3: lean variant (W_x fragments from L1, no bf16 copy of u, W_dt per chunk) so that
+    // three CTAs fit per SM (<= 85 registers, <= 75 KB shared memory).
     constexpr int NW = DI / 32;
-    using L = MixerSmem<DI, NXP>;
+    using L = MixerSmem<DI, NXP, OCC>;
     extern __shared__ __align__(128) uint8_t msm[];
     __nv_bfloat16* xz_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kXZ);   // [2][16][2 DI]
     float* u_s = reinterpret_cast<float*>(msm + L::kU);                       // [16][DI + 4]
@@ -98,15 +102,17 @@ __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
     const int g = lane >> 2, tq = lane & 3;
 
     // ---- once per CTA: W_x into padded smem, W_dt fragments into registers, per-channel constants
-    for (int idx = d; idx < NXP * DI / 8; idx += DI) {
-        const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
-        *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
-            __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
+    if (OCC == 2) {
+        for (int idx = d; idx < NXP * DI / 8; idx += DI) {
+            const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
+            *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
+                __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
+        }
     }
     constexpr int NT_DT = DI / 8 / NW;  // dt_proj n-tiles per warp
     uint32_t wdt[NT_DT][RP / 16][2];
 #pragma unroll
-    for (int j = 0; j < NT_DT; ++j) {
+    for (int j = 0; j < NT_DT && OCC == 2; ++j) {
         const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
 #pragma unroll
         for (int ks = 0; ks < RP / 16; ++ks) {
@@ -114,6 +120,9 @@ __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
             wdt[j][ks][1] = __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 8 + 2 * tq));
         }
     }
+    float2 bdt[NT_DT];  // dt_proj bias of this thread's output columns
+#pragma unroll
+    for (int j = 0; j < NT_DT; ++j) bdt[j] = __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
     float2 A2[N / 2], iA[N / 2];
 #pragma unroll
     for (int n = 0; n < N / 2; ++n) {
@@ -179,36 +188,51 @@ __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
         const __nv_bfloat16* xz = xz_s + buf * kTC * 2 * DI;
 
         // ---- 1. causal conv + SiLU
+        // (rows tt >= tc of the chunk are left stale: MMA rows are independent and never read back)
 #pragma unroll 4
-        for (int tt = 0; tt < kTC; ++tt) {
-            float u = 0.0f;
-            if (tt < tc) {
-                const float x = __bfloat162float(xz[tt * 2 * DI + d]);
-                float acc = fmaf(wc[DC - 1], x, bconv);
+        for (int tt = 0; tt < tc; ++tt) {
+            const float x = __bfloat162float(xz[tt * 2 * DI + d]);
+            float acc = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
-                for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
+            for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
 #pragma unroll
-                for (int k = DC - 1; k > 0; --k) win[k] = win[k - 1];
-                win[0] = x;
-                u = silu_fast(acc);
-            }
+            for (int k = DC - 1; k > 0; --k) win[k] = win[k - 1];
+            win[0] = x;
+            const float u = silu_fast(acc);
             u_s[tt * L::kUld + d] = u;
-            u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
+            if (OCC == 2) u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
         }
         __syncthreads();
         // ---- 2. x_proj on the tensor cores: dbc[16][NXP] = u[16][DI] . W_x^T
         for (int nt = warp; nt < NXP / 8; nt += NW) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const __nv_bfloat16* wrow = wx_s + (nt * 8 + g) * L::kWxld;
+            const __nv_bfloat16* wrow = OCC == 2 ? wx_s + (nt * 8 + g) * L::kWxld : a.Wx_b + (int64_t)(nt * 8 + g) * DI;
 #pragma unroll 4
             for (int k0 = 0; k0 < DI; k0 += 16) {
                 uint32_t af[4];
-                af[0] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 2 * tq);
-                af[1] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 2 * tq);
-                af[2] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 8 + 2 * tq);
-                af[3] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 8 + 2 * tq);
-                const uint32_t b0 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 2 * tq);
-                const uint32_t b1 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 8 + 2 * tq);
+                if (OCC == 2) {
+                    af[0] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 2 * tq);
+                    af[1] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 2 * tq);
+                    af[2] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 8 + 2 * tq);
+                    af[3] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 8 + 2 * tq);
+                } else {
+                    const float2 p0 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 2 * tq);
+                    const float2 p1 = *reinterpret_cast<const float2*>(u_s + (g + 8) * L::kUld + k0 + 2 * tq);
+                    const float2 p2 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 8 + 2 * tq);
+                    const float2 p3 = *reinterpret_cast<const float2*>(u_s + (g + 8) * L::kUld + k0 + 8 + 2 * tq);
+                    af[0] = pk_bf16(p0.x, p0.y);
+                    af[1] = pk_bf16(p1.x, p1.y);
+                    af[2] = pk_bf16(p2.x, p2.y);
+                    af[3] = pk_bf16(p3.x, p3.y);
+                }
+                uint32_t b0, b1;
+                if (OCC == 2) {
+                    b0 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 2 * tq);
+                    b1 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 8 + 2 * tq);
+                } else {
+                    b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 2 * tq));
+                    b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 8 + 2 * tq));
+                }
                 mma_16816(acc, af, b0, b1);
             }
             const int c = nt * 8 + 2 * tq;
@@ -236,9 +260,17 @@ __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
             for (int j = 0; j < NT_DT; ++j) {
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int ks = 0; ks < RP / 16; ++ks) mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
+                for (int ks = 0; ks < RP / 16; ++ks) {
+                    if (OCC == 2) {
+                        mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
+                    } else {
+                        const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
+                        mma_16816(acc, af[ks], __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 2 * tq)),
+                                  __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 8 + 2 * tq)));
+                    }
+                }
                 const int c = (warp + j * NW) * 8 + 2 * tq;
-                const float b0v = __ldg(a.b_dt + c), b1v = __ldg(a.b_dt + c + 1);
+                const float b0v = bdt[j].x, b1v = bdt[j].y;
                 *reinterpret_cast<float2*>(dl_s + g * DI + c) =
                     make_float2(softplus_fast(acc[0] + b0v), softplus_fast(acc[1] + b1v));
                 *reinterpret_cast<float2*>(dl_s + (g + 8) * DI + c) =
@@ -302,10 +334,10 @@ __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
     }
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC>
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC>
 static cudaError_t mixer_launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
-    constexpr int smem = MixerSmem<DI, NXP>::kBytes;
-    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC>;
+    constexpr int smem = MixerSmem<DI, NXP, OCC>::kBytes;
+    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC, OCC>;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -322,8 +354,12 @@ static cudaError_t mixer_launch_k(const MixerArgs& a, int num_sms, cudaStream_t 
 template <int DI, int N, int RP, int NXP>
 static cudaError_t mixer_launch(const MixerArgs& a, int num_sms, cudaStream_t s) {
     if (a.d_conv != 4) return cudaErrorInvalidValue;  // validated on the host
-    return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1>(a, num_sms, s)
-                       : mixer_launch_k<DI, N, RP, NXP, 4, 0>(a, num_sms, s);
+    static const int occ = [] { const char* v = getenv("TCL_MIXER_OCC"); return (v && v[0] == '3') ? 3 : 2; }();
+    if (occ == 3)
+        return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1, 3>(a, num_sms, s)
+                           : mixer_launch_k<DI, N, RP, NXP, 4, 0, 3>(a, num_sms, s);
+    return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1, 2>(a, num_sms, s)
+                       : mixer_launch_k<DI, N, RP, NXP, 4, 0, 2>(a, num_sms, s);
 }
 
 template <int DI, int N>

@@ -366,7 +366,7 @@ static cudaError_t launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
 template <int DI, int N>
 static cudaError_t launch_rp(const MixerArgs& a, int num_sms, cudaStream_t s) {
     const int nxp = ((a.R + 2 * N) + 7) / 8 * 8;
-    constexpr int OFF = N == 16 ? 1 : 0;  // polynomial exp pairs per token (of N/2)
+    constexpr int OFF = 0;  // polynomial exp pairs per token (of N/2); FMA pipe is ~75% busy already
     if (a.RP == 16) {
         if (nxp <= 24) return launch_k<DI, N, 16, 24, OFF>(a, num_sms, s);
         if (nxp <= 48) return launch_k<DI, N, 16, 48, OFF>(a, num_sms, s);

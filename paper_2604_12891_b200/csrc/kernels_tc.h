@@ -30,7 +30,9 @@ struct TcGemmParams {
 bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                     uint32_t box_inner, uint32_t box_outer);
 // A: [rows][K] (box {64, 128}); B: [N][K] weights (box {64, bn}); kb = ceil(K / 64).
-cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const TcGemmParams& p, int bn, int kb,
-                           int num_sms, cudaStream_t s);
+// C: bf16 output map (box {64, 32}, 128B swizzle) used for TMA stores when BN >= 128 and the
+// epilogue writes bf16 (ignored otherwise).
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
+                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s);
 
 }  // namespace tcl
