@@ -249,6 +249,8 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         if (e1 >= 64) ok = ok && make_tmap_bf16(&w.tmE1o, E1b, e1, rows, (uint64_t)e1 * 2, 64, 32);
         if (e2 >= 64) ok = ok && make_tmap_bf16(&w.tmE2o, E2b, e2, rows, (uint64_t)e2 * 2, 64, 32);
         ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
+        ok = ok && make_tmap_f32(&w.tmHf, w.H, dm, rows, (uint64_t)dm * 4, 32, 32);
+        ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
@@ -423,7 +425,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         q.out = d.n_layer > 0 ? w.Ab : nullptr; q.ldo = dm;
         q.ln_g = d.n_layer > 0 ? m->wp.layers[0].ln_w : m->wp.lnf_w;
         q.ln_b = d.n_layer > 0 ? m->wp.layers[0].ln_b : m->wp.lnf_b;
-        if ((e = launch_gemm_tc(w.tmE2b, m->tmW3, w.tmXZo, q, dm, kb_of(e2), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc3");
+        e = dm >= 128 ? launch_gemm_tc_ln(w.tmE2b, m->tmW3, w.tmHf, w.tmAo, q, dm, kb_of(e2), m->num_sms, s)
+                      : launch_gemm_tc(w.tmE2b, m->tmW3, w.tmXZo, q, dm, kb_of(e2), m->num_sms, s);
+        if (e != cudaSuccess) return cuda_error(e, "enc3");
         ++nl;
         if (debug_sync("enc3", s) != TCL_OK) return TCL_ECUDA;
     }
@@ -464,8 +468,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             p.out = last ? nullptr : w.Ab; p.ldo = dm;
             p.ln_g = last ? m->wp.lnf_w : m->wp.layers[l + 1].ln_w;
             p.ln_b = last ? m->wp.lnf_b : m->wp.layers[l + 1].ln_b;
-            if ((e = launch_gemm_tc(w.tmGb, m->tmWout[l], w.tmXZo, p, dm, kb_of(di), m->num_sms, s)) != cudaSuccess)
-                return cuda_error(e, "out_proj");
+            e = dm >= 128 ? launch_gemm_tc_ln(w.tmGb, m->tmWout[l], w.tmHf, w.tmAo, p, dm, kb_of(di), m->num_sms, s)
+                          : launch_gemm_tc(w.tmGb, m->tmWout[l], w.tmXZo, p, dm, kb_of(di), m->num_sms, s);
+            if (e != cudaSuccess) return cuda_error(e, "out_proj");
             ++nl;
             if (debug_sync("out_proj", s) != TCL_OK) return TCL_ECUDA;
         }

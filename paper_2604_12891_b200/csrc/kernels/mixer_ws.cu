@@ -111,10 +111,14 @@ struct ChunkIter {
     }
 };
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC, int OFF>
-__global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs a) {
+// SPLIT threads per channel: each scan thread owns N/SPLIT of the channel's states; the partial
+// outputs C.s of a channel are combined with one shuffle (SPLIT = 2 doubles the scan warps per SM
+// at the same register budget -> better latency hiding for the MUFU-bound recurrence).
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int SPLIT>
+__global__ void __launch_bounds__(SPLIT * DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs a) {
     using L = Smem<DI, NXP>;
-    constexpr int NSW = DI / 32;          // scan warps
+    constexpr int OFF = 0;                // polynomial exp pairs (FMA pipe already ~45% busy)
+    constexpr int NSW = SPLIT * DI / 32;  // scan warps
     constexpr int NPT = 32 * kProdWarps;  // producer threads
     constexpr int CPT = DI / NPT;         // channels per producer thread
     extern __shared__ __align__(128) uint8_t msm[];
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs 
 
     if (warp >= NSW) {
         // =============================== producer warps ===============================
-        const int p = tid - DI;             // 0 .. NPT-1
+        const int p = tid - SPLIT * DI;     // 0 .. NPT-1
         const int pw = warp - NSW;          // producer warp 0..3
         const int g = lane >> 2, tq = lane & 3;
         constexpr int NT_DT = DI / 8 / kProdWarps;
@@ -279,15 +283,17 @@ __global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs 
         }
     } else {
         // =============================== scan warps ===============================
-        const int d = tid;
-        float2 A2[N / 2], iA[N / 2];
+        constexpr int NP = N / 2 / SPLIT;         // state pairs per thread
+        const int d = SPLIT == 1 ? tid : warp * 16 + (lane >> 1);
+        const int hh = SPLIT == 1 ? 0 : (lane & 1);
+        float2 A2[NP], iA[NP];
 #pragma unroll
-        for (int n = 0; n < N / 2; ++n) {
-            A2[n] = __ldg(reinterpret_cast<const float2*>(a.A2 + d * N) + n);
-            iA[n] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + n);
+        for (int n = 0; n < NP; ++n) {
+            A2[n] = __ldg(reinterpret_cast<const float2*>(a.A2 + d * N) + hh * NP + n);
+            iA[n] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + hh * NP + n);
         }
         const float Dv = __ldg(a.Dv + d);
-        float2 s[N / 2];
+        float2 s[NP];
         uint32_t c = 0;
         while (it.valid()) {
             const int slot = c & 1, r = c % 3;
@@ -295,34 +301,33 @@ __global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs 
             const int tc = min(kTC, T - it.t0);
             if (it.t0 == 0) {
 #pragma unroll
-                for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+                for (int n = 0; n < NP; ++n) s[n] = make_float2(0.f, 0.f);
             }
             tc::mbar_wait(&full[slot], (c >> 1) & 1);
             tc::mbar_wait(&tmab[r], (c / 3) & 1);  // z rows (async-proxy writes) visible here too
-            const __nv_bfloat16* xz = xz_s + r * kTC * L::kXZld;
-            const float* us = u_s + slot * kTC * L::kUld;
-            const float* dls = dl_s + slot * kTC * DI;
-            const float* dbcs = dbc_s + slot * kTC * L::kDbcld;
+            const __nv_bfloat16* zp = xz_s + r * kTC * L::kXZld + DI + d;
+            const float* up = u_s + slot * kTC * L::kUld + d;
+            const float* dlp = dl_s + slot * kTC * DI + d;
+            const float* bp = dbc_s + slot * kTC * L::kDbcld + a.R + hh * 2 * NP;
             __nv_bfloat16* gout = a.G + (a.cu[it.i] + it.t0) * (int64_t)a.ldg + d;
             for (int tt = 0; tt < tc; ++tt) {
-                const float u = us[tt * L::kUld + d];
-                const float dl = dls[tt * DI + d];
-                const float z = __bfloat162float(xz[tt * L::kXZld + DI + d]);
-                const float4* B4 = reinterpret_cast<const float4*>(dbcs + tt * L::kDbcld + a.R);
-                const float4* C4 = reinterpret_cast<const float4*>(dbcs + tt * L::kDbcld + a.R + N);
+                const float u = *up;
+                const float dl = *dlp;
+                const float z = __bfloat162float(*zp);
                 const float2 dl2 = make_float2(dl, dl);
                 const float2 u2 = make_float2(u, u);
                 const float2 du2 = __fmul2_rn(dl2, u2);
                 float2 y2 = make_float2(0.f, 0.f), y2b = make_float2(0.f, 0.f);
 #pragma unroll
-                for (int q = 0; q < N / 4; ++q) {
-                    const float4 b4 = B4[q], c4 = C4[q];
+                for (int q = 0; q < NP / 2; ++q) {
+                    const float4 b4 = reinterpret_cast<const float4*>(bp)[q];
+                    const float4 c4 = reinterpret_cast<const float4*>(bp + N)[q];
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const int n = 2 * q + h;
                         const float2 x2 = __fmul2_rn(dl2, A2[n]);
-                        const float2 ab = (n >= N / 2 - OFF) ? exp2_poly2(x2)
-                                                             : make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 ab = (n >= NP - OFF) ? exp2_poly2(x2)
+                                                          : make_float2(ex2(x2.x), ex2(x2.y));
                         const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
                         const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
                         if (DISC == 1) {
@@ -335,8 +340,15 @@ __global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs 
                         if (h) y2b = __ffma2_rn(cc, s[n], y2b); else y2 = __ffma2_rn(cc, s[n], y2);
                     }
                 }
-                const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
-                gout[(int64_t)tt * a.ldg] = __float2bfloat16_rn(y * silu_fast(z));
+                float yp = (y2.x + y2b.x) + (y2.y + y2b.y);
+                if (SPLIT == 2) yp += __shfl_xor_sync(0xffffffffu, yp, 1);
+                const float y = fmaf(Dv, u, yp);
+                const __nv_bfloat16 gv = __float2bfloat16_rn(y * silu_fast(z));
+                if (hh == 0) gout[(int64_t)tt * a.ldg] = gv;
+                up += L::kUld;
+                dlp += DI;
+                zp += L::kXZld;
+                bp += L::kDbcld;
             }
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&empty[slot]);
@@ -346,11 +358,11 @@ __global__ void __launch_bounds__(DI + 32 * kProdWarps, 1) k_mixer_ws(MixerArgs 
     }
 }
 
-template <int DI, int N, int RP, int NXP, int OFF>
+template <int DI, int N, int RP, int NXP, int SPLIT>
 static cudaError_t launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
     constexpr int smem = Smem<DI, NXP>::kBytes;
-    constexpr int threads = DI + 32 * kProdWarps;
-    auto kern = a.disc == 1 ? k_mixer_ws<DI, N, RP, NXP, 4, 1, OFF> : k_mixer_ws<DI, N, RP, NXP, 4, 0, OFF>;
+    constexpr int threads = SPLIT * DI + 32 * kProdWarps;
+    auto kern = a.disc == 1 ? k_mixer_ws<DI, N, RP, NXP, 4, 1, SPLIT> : k_mixer_ws<DI, N, RP, NXP, 4, 0, SPLIT>;
     static bool attr[2] = {false, false};
     if (!attr[a.disc]) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -366,12 +378,12 @@ static cudaError_t launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
 template <int DI, int N>
 static cudaError_t launch_rp(const MixerArgs& a, int num_sms, cudaStream_t s) {
     const int nxp = ((a.R + 2 * N) + 7) / 8 * 8;
-    constexpr int OFF = 0;  // polynomial exp pairs per token (of N/2); FMA pipe is ~75% busy already
+    constexpr int SPLIT = N == 16 ? 2 : 1;  // two threads per channel when the state is large
     if (a.RP == 16) {
-        if (nxp <= 24) return launch_k<DI, N, 16, 24, OFF>(a, num_sms, s);
-        if (nxp <= 48) return launch_k<DI, N, 16, 48, OFF>(a, num_sms, s);
+        if (nxp <= 24) return launch_k<DI, N, 16, 24, SPLIT>(a, num_sms, s);
+        if (nxp <= 48) return launch_k<DI, N, 16, 48, SPLIT>(a, num_sms, s);
     } else if (a.RP == 32) {
-        if (nxp <= 64) return launch_k<DI, N, 32, 64, OFF>(a, num_sms, s);
+        if (nxp <= 64) return launch_k<DI, N, 32, 64, SPLIT>(a, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -29,6 +29,14 @@ struct TcGemmParams {
 // 2-D bf16 tensor map, 128B swizzle, box {box_inner (<= 64), box_outer (<= 256)}.
 bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                     uint32_t box_inner, uint32_t box_outer);
+// 2-D fp32 tensor map, 128B swizzle, box {box_inner (<= 32), box_outer}.
+bool make_tmap_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                   uint32_t box_inner, uint32_t box_outer);
+// Residual + LayerNorm GEMM (gemm_tc_ln.cu): bn = d_model in {128, 256}; H: fp32 map of the
+// residual stream (box {32, 32}); O: bf16 map of the LayerNorm output (box {64, 32}).
+cudaError_t launch_gemm_tc_ln(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& h,
+                              const CUtensorMap& o, const TcGemmParams& p, int bn, int kb, int num_sms,
+                              cudaStream_t s);
 // A: [rows][K] (box {64, 128}); B: [N][K] weights (box {64, bn}); kb = ceil(K / 64).
 // C: bf16 output map (box {64, 32}, 128B swizzle) used for TMA stores when BN >= 128 and the
 // epilogue writes bf16 (ignored otherwise).
