@@ -279,13 +279,17 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 4. selective scan + D skip + gate (packed fp32x2 arithmetic, MUFU.EX2 for exp)
-        __nv_bfloat16* gout = a.G + base * a.ldg + d;
+        __nv_bfloat16* gout = a.G + (base + cur_t0) * a.ldg + d;
+        const float* up = u_s + d;
+        const float* dlp = dl_s + d;
+        const __nv_bfloat16* gzp = xz + DI + d;
+        const float* bcp = dbc_s + a.R;
         for (int tt = 0; tt < tc; ++tt) {
-            const float u = u_s[tt * L::kUld + d];
-            const float dl = dl_s[tt * DI + d];
-            const float z = __bfloat162float(xz[tt * 2 * DI + DI + d]);
-            const float4* B4 = reinterpret_cast<const float4*>(dbc_s + tt * L::kDbcld + a.R);
-            const float4* C4 = reinterpret_cast<const float4*>(dbc_s + tt * L::kDbcld + a.R + N);
+            const float u = *up;
+            const float dl = *dlp;
+            const float gz = silu_fast(__bfloat162float(*gzp));
+            const float4* B4 = reinterpret_cast<const float4*>(bcp);
+            const float4* C4 = reinterpret_cast<const float4*>(bcp + N);
             const float2 dl2 = make_float2(dl, dl);
             const float2 u2 = make_float2(u, u);
             float2 y2 = make_float2(0.f, 0.f), y2b = make_float2(0.f, 0.f);
@@ -325,7 +329,12 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                 }
             }
             const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
-            gout[(int64_t)(cur_t0 + tt) * a.ldg] = __float2bfloat16_rn(y * silu_fast(z));
+            *gout = __float2bfloat16_rn(y * gz);
+            up += L::kUld;
+            dlp += DI;
+            gzp += 2 * DI;
+            bcp += L::kDbcld;
+            gout += a.ldg;
         }
         __syncthreads();
         buf ^= 1;
