@@ -178,7 +178,8 @@ const char* tcl_profile_name(int kind);
  * fp32, to host memory.  name: "H" (residual stream [P][d_model]), "A" (LayerNorm output
  * [P][d_model]), "XZ" (in_proj output [P][2 d_inner]), "G" (gated scan output [P][d_inner]),
  * "U" (conv output, fp32 path only), "DELTA" (fp32 path only).  Rows are the packed tokens of the
- * last chunk scored; buffers hold the values of the LAST layer that wrote them.  Synchronises. */
+ * last chunk scored; buffers hold the values of the LAST kernel that wrote them (bf16 path with
+ * d_model >= 128: the last layer writes LN_f(H) into "A" and does not write "H").  Synchronises. */
 tcl_status tcl_debug_read(tcl_model* model, const char* name, float* host_out, int64_t rows, int64_t cols);
 
 /* Thread-local message describing the last error returned on this thread ("" if none). */

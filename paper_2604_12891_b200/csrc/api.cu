@@ -276,13 +276,16 @@ static tcl_status ensure_topk_tmp(tcl_model* m, int64_t n, int k) {
 // fp32 GEMMs over the candidates (weights stream through shared memory once per 64 candidates);
 // MC passes fold each pass' score into (mean, M2) with Welford's update.
 static void run_head(tcl_model* m, const int32_t* lens, int64_t n, float* scores, const DropoutCtx& drop,
-                     float* mc_mean, cudaStream_t s) {
+                     float* mc_mean, cudaStream_t s, bool lnf_in_ab = false) {
     const tcl_dims& d = m->dims;
     Workspace& w = m->ws;
     const int dm = d.d_model, h1 = d.dec_dims[0], h2 = d.dec_dims[1];
     int64_t& nl = m->launches;
     ProfScope ps(m, TCL_PROF_HEAD, s);
-    launch_pool(w.H, dm, dm, m->wp.lnf_w, m->wp.lnf_b, d.ln_eps, w.cu, lens, d.max_len, n, w.pooled, s);
+    if (lnf_in_ab)  // bf16 path: the last GEMM epilogue already wrote LN_f(H) (bf16) into Ab
+        launch_pool_bf16(w.Ab, dm, dm, w.cu, lens, d.max_len, n, w.pooled, s);
+    else
+        launch_pool(w.H, dm, dm, m->wp.lnf_w, m->wp.lnf_b, d.ln_eps, w.cu, lens, d.max_len, n, w.pooled, s);
     ++nl;
     auto dec = [&](const float* X, int K, const float* W, const float* b, float* Y, int Nout, int epi, int site) {
         GemmArgs g{};
@@ -422,7 +425,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         if (debug_sync("enc2", s) != TCL_OK) return TCL_ECUDA;
         TcGemmParams q = base();
         q.epi = TC_EPI_RESID_LN; q.bias = m->wp.enc_b3; q.residual = 0; q.H = w.H; q.ldh = dm;
-        q.out = d.n_layer > 0 ? w.Ab : nullptr; q.ldo = dm;
+        q.out = (d.n_layer > 0 || dm >= 128) ? w.Ab : nullptr; q.ldo = dm;
         q.ln_g = d.n_layer > 0 ? m->wp.layers[0].ln_w : m->wp.lnf_w;
         q.ln_b = d.n_layer > 0 ? m->wp.layers[0].ln_b : m->wp.lnf_b;
         e = dm >= 128 ? launch_gemm_tc_ln(w.tmE2b, m->tmW3, w.tmHf, w.tmAo, q, dm, kb_of(e2), m->num_sms, s)
@@ -465,7 +468,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             TcGemmParams p = base();
             p.epi = TC_EPI_RESID_LN; p.residual = 1; p.H = w.H; p.ldh = dm;
             const bool last = l + 1 == d.n_layer;
-            p.out = last ? nullptr : w.Ab; p.ldo = dm;
+            // last layer (LN kernel): write only LN_f(H) (bf16, the head's input), not H itself
+            p.out = (last && dm < 128) ? nullptr : w.Ab; p.ldo = dm;
+            p.skip_h_store = last && dm >= 128;
             p.ln_g = last ? m->wp.lnf_w : m->wp.layers[l + 1].ln_w;
             p.ln_b = last ? m->wp.lnf_b : m->wp.layers[l + 1].ln_b;
             e = dm >= 128 ? launch_gemm_tc_ln(w.tmGb, m->tmWout[l], w.tmHf, w.tmAo, p, dm, kb_of(di), m->num_sms, s)
@@ -475,7 +480,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             if (debug_sync("out_proj", s) != TCL_OK) return TCL_ECUDA;
         }
     }
-    run_head(m, lens, n, scores, drop, mc_mean, s);
+    run_head(m, lens, n, scores, drop, mc_mean, s, /*lnf_in_ab=*/dm >= 128);
     return TCL_OK;
 }
 

@@ -69,6 +69,10 @@ void launch_scan(const ScanArgs& a, cudaStream_t s);
 void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const float* lnf_b, float eps,
                  const int32_t* cu, const int32_t* lens, int max_len, int64_t n, float* pooled,
                  cudaStream_t s);
+// Masked mean of already-normalised bf16 rows F = LN_f(H) (bf16 path: written by the last
+// out_proj epilogue) -> pooled [n][dm] fp32.
+void launch_pool_bf16(const void* F, int ldf, int dm, const int32_t* cu, const int32_t* lens, int max_len,
+                      int64_t n, float* pooled, cudaStream_t s);
 // MC: Welford update of (mean, m2) with this pass' scores; invalid lengths -> NaN.
 void launch_welford(const float* score, const int32_t* lens, int max_len, int64_t n, int pass,
                     float* mean, float* m2, cudaStream_t s);

@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_ln(const __grid_constant__
                 tc::fence_proxy_async();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&tmH, col0 + c * 32, m * kBM + quarter * 32, buf);
+                    if (!p.skip_h_store) tma_store_2d(&tmH, col0 + c * 32, m * kBM + quarter * 32, buf);
                     if (res && c + 2 < NC) {           // refill this buffer with chunk c + 2
                         store_read_wait_all();
                         load_h(m, c + 2, b);

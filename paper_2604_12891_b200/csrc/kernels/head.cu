@@ -3,6 +3,7 @@
 // after the first two (reading R1), plus the MC-dropout sites dec h1/h2 and the
 // per-candidate Welford accumulation over passes (reading R17).
 // One CTA (8 warps) per candidate; every reduction has a fixed order -> batch-invariant scores.
+#include <cuda_bf16.h>
 #include <math.h>
 
 #include "../kernels.h"
@@ -156,6 +157,55 @@ void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const floa
 #define TCL_POOL(P) case P: k_pool<P><<<grid, 256, 0, s>>>(H, ldh, lnf_w, lnf_b, eps, cu, lens, max_len, n, pooled); break;
         TCL_POOL(1) TCL_POOL(2) TCL_POOL(3) TCL_POOL(4) TCL_POOL(5) TCL_POOL(6) TCL_POOL(7) TCL_POOL(8)
 #undef TCL_POOL
+        default: break;
+    }
+}
+
+// Masked mean of bf16 rows that are already LN_f(H): one warp per candidate, rows summed in order.
+template <int PER>
+__global__ void __launch_bounds__(256) k_pool_bf16(const __nv_bfloat16* __restrict__ F, int ldf,
+                                                   const int32_t* __restrict__ cu,
+                                                   const int32_t* __restrict__ lens, int max_len, int64_t n,
+                                                   float* __restrict__ pooled) {
+    constexpr int dm = 64 * PER;  // lane handles 2 * PER columns (bf16x2 loads)
+    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const int T = lens[i];
+    float acc[2 * PER];
+#pragma unroll
+    for (int j = 0; j < 2 * PER; ++j) acc[j] = 0.0f;
+    if (T >= 1 && T <= max_len) {
+        const __nv_bfloat16* f = F + (int64_t)cu[i] * ldf;
+#pragma unroll 4
+        for (int t = 0; t < T; ++t) {
+#pragma unroll
+            for (int j = 0; j < PER; ++j) {
+                const __nv_bfloat162 v = *reinterpret_cast<const __nv_bfloat162*>(f + (int64_t)t * ldf + 2 * (lane + 32 * j));
+                const float2 fv = __bfloat1622float2(v);
+                acc[2 * j] += fv.x;
+                acc[2 * j + 1] += fv.y;
+            }
+        }
+        const float invT = 1.0f / (float)T;
+#pragma unroll
+        for (int j = 0; j < 2 * PER; ++j) acc[j] *= invT;
+    }
+#pragma unroll
+    for (int j = 0; j < PER; ++j)
+        *reinterpret_cast<float2*>(pooled + i * dm + 2 * (lane + 32 * j)) = make_float2(acc[2 * j], acc[2 * j + 1]);
+}
+
+void launch_pool_bf16(const void* F, int ldf, int dm, const int32_t* cu, const int32_t* lens, int max_len,
+                      int64_t n, float* pooled, cudaStream_t s) {
+    if (n == 0) return;
+    dim3 grid((unsigned)((n + 7) / 8));
+    const auto* f = reinterpret_cast<const __nv_bfloat16*>(F);
+    switch (dm / 64) {
+        case 1: k_pool_bf16<1><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
+        case 2: k_pool_bf16<2><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
+        case 3: k_pool_bf16<3><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
+        case 4: k_pool_bf16<4><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
         default: break;
     }
 }

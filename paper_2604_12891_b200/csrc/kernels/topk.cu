@@ -22,12 +22,11 @@ __device__ __forceinline__ u64 make_key(float f, uint32_t gidx) {
     return ((u64)ord << 32) | (u64)(0xFFFFFFFFu - gidx);
 }
 
-template <bool FROM_SCORES>
+template <bool FROM_SCORES, int C>
 __global__ void __launch_bounds__(1024) k_topk_chunk(const float* __restrict__ scores,
                                                      const u64* __restrict__ keys_in, int64_t count,
                                                      int64_t index_base, int k, u64* __restrict__ out) {
     extern __shared__ u64 sk[];
-    constexpr int C = kTopkChunk;
     const int64_t lo = (int64_t)blockIdx.x * C;
     const int64_t m = min((int64_t)C, count - lo);
     for (int j = threadIdx.x; j < C; j += blockDim.x) {
@@ -64,40 +63,48 @@ __global__ void k_topk_decode(const u64* __restrict__ keys, int k, int64_t* __re
 }
 
 size_t topk_tmp_keys(int64_t n, int k) {
-    const int64_t blocks = (n + kTopkChunk - 1) / kTopkChunk;
+    const int64_t blocks = (n + 2047) / 2048;  // smallest chunk size -> most first-round blocks
     return (size_t)(2 * blocks * k + 2 * kTopkChunk);
 }
 
-static void set_smem_once() {
+template <int C>
+static void launch_chunk(bool from_scores, unsigned blocks, const float* scores, const u64* src, int64_t cur,
+                         int64_t index_base, int k, u64* dst, cudaStream_t s) {
     static bool done = false;
-    if (done) return;
-    cudaFuncSetAttribute(k_topk_chunk<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kTopkChunk * (int)sizeof(u64));
-    cudaFuncSetAttribute(k_topk_chunk<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kTopkChunk * (int)sizeof(u64));
-    done = true;
+    const int smem = C * (int)sizeof(u64);
+    if (!done) {
+        cudaFuncSetAttribute(k_topk_chunk<true, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(k_topk_chunk<false, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        done = true;
+    }
+    if (from_scores)
+        k_topk_chunk<true, C><<<blocks, 1024, smem, s>>>(scores, nullptr, cur, index_base, k, dst);
+    else
+        k_topk_chunk<false, C><<<blocks, 1024, smem, s>>>(nullptr, src, cur, 0, k, dst);
 }
+
+// Chunk size: >= 4k (each round shrinks the candidate set >= 4x) and small enough that the first
+// round spreads over many CTAs.
+static int chunk_for(int k) { return k <= 512 ? 2048 : (k <= 1024 ? 4096 : kTopkChunk); }
 
 // Rounds of the tournament; writes exactly k keys (descending, 0-padded) to `out`.
 static int tournament(const float* scores, const u64* keys, int64_t count, int k,
                       int64_t index_base, u64* out, u64* tmp, cudaStream_t s) {
     int launched = 0;
-    set_smem_once();
-    const size_t smem = kTopkChunk * sizeof(u64);
-    const int64_t blocks0 = (count + kTopkChunk - 1) / kTopkChunk;
+    const int C = chunk_for(k);
+    const int64_t blocks0 = (count + C - 1) / C;
     u64* buf[2] = {tmp, tmp + blocks0 * k + kTopkChunk};
     int which = 0;
     const u64* src = keys;
     bool from_scores = scores != nullptr;
     int64_t cur = count;
     for (;;) {
-        int64_t blocks = (cur + kTopkChunk - 1) / kTopkChunk;
+        int64_t blocks = (cur + C - 1) / C;
         if (blocks < 1) blocks = 1;
         u64* dst = blocks == 1 ? out : buf[which];
-        if (from_scores)
-            k_topk_chunk<true><<<(unsigned)blocks, 1024, smem, s>>>(scores, nullptr, cur, index_base, k, dst);
-        else
-            k_topk_chunk<false><<<(unsigned)blocks, 1024, smem, s>>>(nullptr, src, cur, 0, k, dst);
+        if (C == 2048) launch_chunk<2048>(from_scores, (unsigned)blocks, scores, src, cur, index_base, k, dst, s);
+        else if (C == 4096) launch_chunk<4096>(from_scores, (unsigned)blocks, scores, src, cur, index_base, k, dst, s);
+        else launch_chunk<kTopkChunk>(from_scores, (unsigned)blocks, scores, src, cur, index_base, k, dst, s);
         ++launched;
         if (blocks == 1) break;
         cur = blocks * k;

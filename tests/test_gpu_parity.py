@@ -272,3 +272,51 @@ def test_score_host_matches_device(torch_cuda):
     assert np.array_equal(s_host, s_dev)
     gi, gt = _topk_gpu(torch_cuda, m, s_dev, 64)
     assert np.array_equal(idx, gi) and np.array_equal(top, gt)
+
+
+# ------------------------------------------------------------------------------------ bf16 path extras
+def test_bf16_mc_parity(torch_cuda, oracle):
+    """MC dropout through the tcgen05 epilogues (Philox masks at enc h1/h2) and the decoder."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("large", n=48)
+    m = Model(w, d)
+    mean, var = _mc_gpu(torch_cuda, m, f, l, 3, 99, index_base=5)
+    rm, rv = oracle.score_mc(d, w, f, l, 3, 99, index_base=5)
+    _check_scores(mean, rm, d.precision)
+    assert np.all(np.abs(var - rv) <= 2 * TOL[d.precision] * np.sqrt(np.maximum(rv, 1e-8)) + 1e-5)
+    s = _gpu_score(torch_cuda, Model(w, d.replace(dropout_p=0.0)), f, l)
+    m0 = Model(w, d.replace(dropout_p=0.0))
+    mean0, var0 = _mc_gpu(torch_cuda, m0, f, l, 2, 99)
+    assert np.array_equal(mean0, s) and np.all(var0 == 0)
+
+
+def test_bf16_invalid_lengths_and_host_path(torch_cuda, oracle):
+    from paper_2604_12891_b200 import Model, TclError
+    d, w, f, l = _setup("large", n=40)
+    l = l.copy()
+    l[:4] = 1
+    l[4:8] = d.max_len
+    m = Model(w, d)
+    good = _gpu_score(torch_cuda, m, f, l)
+    _check_scores(good, oracle.score(d, w, f, l), d.precision)
+    s_host, idx, top = m.tcl_score_host(f, l, k=8)
+    assert np.array_equal(s_host, good)
+    l2 = l.copy()
+    l2[10] = 0
+    torch = torch_cuda
+    st = torch.empty(40, dtype=torch.float32, device="cuda")
+    m.tcl_score(torch.from_numpy(f).cuda(), torch.from_numpy(l2).cuda(), st)
+    with pytest.raises(TclError):
+        m.tcl_sync_error()
+    s2 = st.cpu().numpy()
+    ok = np.arange(40) != 10
+    assert np.isnan(s2[10]) and np.array_equal(s2[ok], good[ok])
+
+
+def test_bf16_long_config_small_batch(torch_cuda, oracle):
+    """`long` model (L = 128) on a small batch: parity + batch invariance across chunks."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("long", n=64)
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    _check_scores(got, oracle.score(d, w, f, l), d.precision)
