@@ -308,10 +308,16 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     calls = per_step_launches[dom]
     units = (mc or 1) * (d.n_layer if dom in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan",
                                                 "out_proj", "mixer") else 1)
+    traffic = None  # DRAM bytes per launch of this kernel from one ncu --set full capture (profiles/)
+    tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get(dom)
+        if tj and args.config == "large":
+            traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
     if "exps" in wk:
         roof = {"bound": "alu", "achieved": de["ex2_per_s"] / 1e12, "peak": mb["ex2"] / 1e12,
                 "unit": "Tex2/s", "frac": de["sfu_frac"],
-                "traffic": None, "kernel": dom,
+                "traffic": traffic, "kernel": dom,
                 "peak_source": mb["source"],
                 "algorithmic_units_per_launch": wk["exps"] * units / calls,
                 "hbm": {"achieved_gbs": de.get("gbs"), "peak_gbs": peaks["hbm"], "frac": de.get("hbm_frac"),

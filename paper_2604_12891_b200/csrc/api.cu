@@ -251,6 +251,9 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
         ok = ok && make_tmap_f32(&w.tmHf, w.H, dm, rows, (uint64_t)dm * 4, 32, 32);
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
+        const int nt_in = 2 * di / m->bn_in;
+        if (nt_in == 2 || nt_in == 4)
+            ok = ok && make_tmap_bf16(&w.tmAbS, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128 / nt_in);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
@@ -440,7 +443,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            if ((e = launch_gemm_tc(w.tmAb, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
+            static const int use_mc = [] { const char* v = getenv("TCL_NO_MCAST"); return (v && v[0] == '1') ? 0 : 1; }();
+            p.mcast = use_mc && (p.n_tiles == 2 || p.n_tiles == 4);
+            if ((e = launch_gemm_tc(p.mcast ? w.tmAbS : w.tmAb, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "in_proj");
             ++nl;
             if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;

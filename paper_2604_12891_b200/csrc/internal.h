@@ -51,7 +51,8 @@ struct Workspace {
     __nv_bfloat16* Gb = nullptr;   // [rows][di]    gated scan output
     CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
     CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
-    CUtensorMap tmHf, tmAo;                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
+    CUtensorMap tmHf, tmAo;
+    CUtensorMap tmAbS;                                 // in_proj A slices for cluster multicast (box {64, 128/n_tiles})                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
     std::vector<void*> allocs;
 };
 

@@ -60,7 +60,7 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // EPI: 0 = bf16 out; 1 = bf16 out of SiLU(acc + bias); 2 = same + MC dropout;
 //      3 = residual/bias into fp32 H, then LayerNorm(H) -> bf16 out (BN == full row)
-template <int BN, int KB, int EPI>
+template <int BN, int KB, int EPI, int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
                                                          const __grid_constant__ CUtensorMap tmC,
@@ -91,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     const int m_step = gridDim.x / p.n_tiles;
 
     if (threadIdx.x == 0) {
-        for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], 1); }
+        for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], CL); }
         tc::mbar_init(bfull, 1);
         for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], kEpiWarps); }
         tc::fence_mbar_init();
@@ -104,6 +104,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
     tc::tc_fence_before();
     __syncthreads();
+    if (CL > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast lands
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -122,7 +123,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                 for (int kb = 0; kb < KB; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], kABytes);
-                    tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
+                    if (CL == 1) {
+                        tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
+                    } else {  // this CTA fetches 128/CL rows of the A k-block for the whole cluster
+                        constexpr int SL = kBM / CL;
+                        tc::tma_load_2d_mcast(sA + stage * kABytes + n_tile * SL * 128, &tmA, kb * 64,
+                                              m * kBM + n_tile * SL, &full[stage], (uint16_t)((1u << CL) - 1));
+                    }
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -152,7 +159,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         const uint64_t bd = tc::sw128_kmajor_desc(sB_addr + kb * BN * 128 + k * 32);
                         tc::mma_bf16(d, ad, bd, idesc, (kb | k) != 0);
                     }
-                    tc::mma_commit(&empty[stage]);
+                    if (CL == 1) tc::mma_commit(&empty[stage]);
+                    else tc::mma_commit_mcast(&empty[stage], (uint16_t)((1u << CL) - 1));  // free the slot cluster-wide
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 tc::mma_commit(&tfull[acc]);
@@ -339,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     }
     tc::tc_fence_before();
     __syncthreads();
+    if (CL > 1) tc::cluster_sync();  // no CTA leaves while peers may still multicast / commit into it
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, 2 * BN);
@@ -390,17 +399,35 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int KB, int EPI>
+template <int BN, int KB, int EPI, int CL = 1>
 static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
                                const TcGemmParams& p, int grid, cudaStream_t s) {
     const int smem = TcSmem<BN, KB, EPI>::kBytes;
+    auto kern = k_gemm_tc<BN, KB, EPI, CL>;
     static bool attr = false;
     if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<BN, KB, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    k_gemm_tc<BN, KB, EPI><<<grid, kThreads, smem, s>>>(a, b, c, p);
+    if (CL == 1) {
+        kern<<<grid, kThreads, smem, s>>>(a, b, c, p);
+    } else {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = CL;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
+        if (e != cudaSuccess) return e;
+    }
     return cudaGetLastError();
 }
 
@@ -410,6 +437,8 @@ static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const 
     if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
     if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
     if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
+    if (p.mcast && p.n_tiles == 4) return launch_impl<BN, KB, 0, 4>(a, b, c, p, grid, s);
+    if (p.mcast && p.n_tiles == 2) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
     return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);
 }
 
