@@ -443,7 +443,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            static const int use_mc = [] { const char* v = getenv("TCL_NO_MCAST"); return (v && v[0] == '1') ? 0 : 1; }();
+            // cluster multicast of A across the N-tile CTAs: correct but measured slower (1.40 vs
+            // 0.81 ms at `large`: 4 KB slices + cluster-coupled stalls), so opt-in only
+            static const int use_mc = [] { const char* v = getenv("TCL_MCAST"); return (v && v[0] == '1') ? 1 : 0; }();
             p.mcast = use_mc && (p.n_tiles == 2 || p.n_tiles == 4);
             if ((e = launch_gemm_tc(p.mcast ? w.tmAbS : w.tmAb, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "in_proj");
