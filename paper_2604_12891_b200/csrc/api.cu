@@ -461,6 +461,8 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
             a.cu = w.cu; a.lens = lens; a.n = n;
             a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
+            static const int diag = [] { const char* v = getenv("TCL_MIXER_DIAG"); return v ? atoi(v) : 0; }();
+            a.diag = diag;
             static const int mixer_kind = [] {
                 const char* v = getenv("TCL_MIXER");   // "ws": warp-specialised variant
                 return (v && std::string(v) == "ws") ? 1 : 0;

@@ -26,6 +26,7 @@
 #include <cuda_bf16.h>
 
 #include <cstdlib>
+#include <cstdio>
 
 #include "../kernels.h"
 #include "../kernels_mixer.h"
@@ -204,7 +205,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         // ---- 1. causal conv + SiLU
         // (rows tt >= tc of the chunk are left stale: MMA rows are independent and never read back)
 #pragma unroll 4
-        for (int tt = 0; tt < tc; ++tt) {
+        for (int tt = 0; tt < (a.diag == 2 ? 0 : tc); ++tt) {
             const float x = __bfloat162float(xz[tt * 2 * DI + d]);
             float acc = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
@@ -218,7 +219,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 2. x_proj on the tensor cores: dbc[16][NXP] = u[16][DI] . W_x^T
-        for (int nt = warp; nt < NXP / 8; nt += NW) {
+        for (int nt = warp; nt < (a.diag == 2 ? 0 : NXP / 8); nt += NW) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             const __nv_bfloat16* wrow = OCC == 2 ? wx_s + (nt * 8 + g) * L::kWxld : a.Wx_b + (int64_t)(nt * 8 + g) * DI;
 #pragma unroll 4
@@ -255,7 +256,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 3. dt_proj + softplus: dl[16][DI] = softplus(dt_r[16][RP] . W_dt^T + b_dt)
-        {
+        if (a.diag != 2) {
             uint32_t af[RP / 16][4];
 #pragma unroll
             for (int ks = 0; ks < RP / 16; ++ks) {
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         const float* dlp = dl_s + d;
         const __nv_bfloat16* gzp = xz + DI + d;
         const float* bcp = dbc_s + a.R;
-        for (int tt = 0; tt < tc; ++tt) {
+        for (int tt = 0; tt < (a.diag == 1 ? 0 : tc); ++tt) {
             const float u = *up;
             const float dl = *dlp;
             const float gz = silu_fast(__bfloat162float(*gzp));
