@@ -155,6 +155,25 @@ tcl_status tcl_score_host(tcl_model* model, const float* feats_host, const int32
                           int64_t n, int64_t index_base, float* scores_host, int32_t k,
                           int64_t* idx_host, float* topscore_host, void* stream);
 
+/* RDU acquisition, one selection round (Algorithm 1 lines 16-31,
+ * Eqs. 1-3; reading R21 in DESIGN.md).  Given the model's predictions for the unlabeled pool
+ * (pool_scores_dev [n_pool], with operator types pool_ops_dev [n_pool] in [0, n_ops)) and for the
+ * current labeled set (labeled_scores_dev [n_labeled]), greedily picks up to budget_total pool
+ * candidates by the total score t_s = f^ d_s + u_s (f^ min-max normalised over pool and labeled,
+ * d_s = distance to the nearest labeled score, u_s = variance of the labeled set plus the
+ * candidate), ties broken by higher f^ then lower index, skipping operator types whose budget
+ * budget_total * count(op) / n_pool is exhausted; each pick joins the labeled set before the next.
+ * selected_idx_dev [budget_total] receives the picks in order, n_selected_dev [1] their number.
+ * Requires 1 <= n_ops <= 256 and n_pool <= 4096 * (SM count).  Non-finite scores take no part
+ * (never selected, not in the labeled set nor the min/max; their op still counts in the budget
+ * shares); pool entries with op outside [0, n_ops) are never selected.  Scores are evaluated in
+ * fp32 with a fixed operation order (bit-reproducible, identical picks to oracle/).  Device
+ * pointers; no allocation after the first call per model; asynchronous on `stream`. */
+tcl_status tcl_rdu_select(tcl_model* model, const float* pool_scores_dev, const int32_t* pool_ops_dev,
+                          int64_t n_pool, const float* labeled_scores_dev, int64_t n_labeled, int32_t n_ops,
+                          int32_t budget_total, int64_t* selected_idx_dev, int32_t* n_selected_dev,
+                          void* stream);
+
 /* Synchronise `stream`, then return (and clear) the sticky device error of the model. */
 tcl_status tcl_sync_error(tcl_model* model, void* stream);
 

@@ -22,7 +22,7 @@ def build(force: bool = False) -> str:
     """gcc -O2, no -march, no BLAS, no intrinsics: the 'plain, slow' baseline."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
         tmp = LIB + f".tmp{os.getpid()}"
-        subprocess.check_call(["gcc", "-O2", "-std=c11", "-Wall", "-shared", "-fPIC", "-pthread",
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-Wall", "-shared", "-fPIC", "-pthread",
                                "-o", tmp, SRC, "-lm"])
         os.replace(tmp, LIB)
     return LIB
@@ -74,6 +74,9 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_uint64, ctypes.c_int64, dp, dp, ctypes.c_int]
         L.tclo_topk_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, dp]
         L.tclo_topk_f32.argtypes = [fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, fp]
+        L.tclo_rdu_scores.argtypes = [fp, ctypes.c_int64, fp, ctypes.c_int64, fp, fp, fp]
+        L.tclo_rdu_select.restype = ctypes.c_int64
+        L.tclo_rdu_select.argtypes = [fp, ip, ctypes.c_int64, fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, lp]
         _lib = L
     return _lib
 
@@ -229,3 +232,25 @@ def topk(scores: np.ndarray, k: int, index_base: int = 0) -> Tuple[np.ndarray, n
     if rc != 0:
         raise ValueError("topk failed")
     return idx, top
+
+
+def rdu_select(pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int) -> np.ndarray:
+    """One RDU selection round (Alg. 1 lines 16-31, Eqs. 1-3): indices of the picks, in order."""
+    ps = _f32(pool_scores)
+    po = np.ascontiguousarray(pool_ops, dtype=np.int32)
+    ls = _f32(labeled_scores) if len(labeled_scores) else np.zeros(1, np.float32)
+    out = np.zeros(max(1, budget_total), dtype=np.int64)
+    k = lib().tclo_rdu_select(_p(ps, ctypes.c_float), _p(po, ctypes.c_int32), ps.shape[0],
+                              _p(ls, ctypes.c_float), len(labeled_scores), n_ops, budget_total,
+                              _p(out, ctypes.c_int64))
+    return out[:k]
+
+
+def rdu_scores(fh_pool, fh_lab):
+    """(d_s, u_s, t_s) of Eqs. 1-3 / line 24 for already-normalised predictions (fp32)."""
+    fp_ = _f32(fh_pool)
+    fl = _f32(fh_lab) if len(fh_lab) else np.zeros(1, np.float32)
+    ds, us, ts = (np.zeros(fp_.shape[0], np.float32) for _ in range(3))
+    lib().tclo_rdu_scores(_p(fp_, ctypes.c_float), fp_.shape[0], _p(fl, ctypes.c_float), len(fh_lab),
+                          _p(ds, ctypes.c_float), _p(us, ctypes.c_float), _p(ts, ctypes.c_float))
+    return ds, us, ts

@@ -490,3 +490,131 @@ int tclo_topk_f32(const float* scores, int64_t n, int32_t k, int64_t index_base,
     free(s); free(t);
     return rc;
 }
+
+/* ------------------------------------------------------------------ RDU acquisition (NEXT #1) */
+/* One selection round of PAPER.md Algorithm 1 (lines 16-31) with Eqs. 1-3 (§4), reading R21:
+ *   f^ = (f - lo) / (hi - lo), lo/hi over pool u labeled predictions ("normalized");
+ *        every f^ = 0.5 when hi == lo; non-finite predictions take no part anywhere (never picked,
+ *        not counted in the labeled set), their operator still counts toward the budget shares
+ *   d_s(i) = min_j |f^_i - f^_j| over the labeled set (Eq. 1); 1 when the labeled set is empty
+ *   mu = (f^_i + S)/(M+1) (Eq. 2); u_s = ((f^_i - mu)^2 + sum_j (f^_j - mu)^2)/(M+1) (Eq. 3) with
+ *        sum_j (f^_j - mu)^2 = Q - 2 mu S + M mu^2 (S = sum f^_j, Q = sum f^_j^2, running sums)
+ *   t_s = f^_i d_s + u_s (line 24); pick argmax t_s, ties: higher f^, then lower index
+ *   budget[op] = B_t * count(op) / n_pool (lines 16-19); an operator type whose selected count has
+ *        reached its budget is skipped (lines 25-31); the pick joins D_l before the next pick.
+ * Where floating point decides the integer pick, this follows the kernel's precision: the scores are
+ * evaluated in fp32, one IEEE operation at a time in the order written above (the file is compiled
+ * with -ffp-contract=off), and the labeled sums are accumulated sequentially in index order.
+ * Returns the number of picks written to out_idx (<= budget_total). */
+static float rdu_uncertainty(float fi, float S, float Q, float Mf) {   /* Eqs. 2-3 */
+    float m1 = Mf + 1.0f;
+    float mu = (fi + S) / m1;
+    float a = fi - mu;
+    float a2 = a * a;
+    float t1 = mu * S;
+    float t2 = t1 + t1;
+    float t3 = mu * mu;
+    float t4 = Mf * t3;
+    float b = (Q - t2) + t4;
+    return (a2 + b) / m1;
+}
+
+static float rdu_total_score(float fi, float ds, float S, float Q, float Mf) {   /* line 24 */
+    float us = rdu_uncertainty(fi, S, Q, Mf);
+    float t5 = fi * ds;
+    return t5 + us;
+}
+
+/* Eqs. 1-3 + line 24 for already-normalised predictions (fh_pool, fh_lab): the per-candidate scores
+ * of the first pick of a round.  Used by the pins (SPEC rdu examples, two-pass variance). */
+void tclo_rdu_scores(const float* fh_pool, int64_t n_pool, const float* fh_lab, int64_t n_lab,
+                     float* ds, float* us, float* ts) {
+    float S = 0.0f, Q = 0.0f, Mf = 0.0f;
+    for (int64_t j = 0; j < n_lab; ++j) {
+        S = S + fh_lab[j];
+        Q = Q + fh_lab[j] * fh_lab[j];
+        Mf = Mf + 1.0f;
+    }
+    for (int64_t i = 0; i < n_pool; ++i) {
+        float d = INFINITY;
+        for (int64_t j = 0; j < n_lab; ++j) {
+            float e = fabsf(fh_pool[i] - fh_lab[j]);
+            if (e < d) d = e;
+        }
+        ds[i] = n_lab > 0 ? d : 1.0f;
+        us[i] = rdu_uncertainty(fh_pool[i], S, Q, Mf);
+        ts[i] = rdu_total_score(fh_pool[i], ds[i], S, Q, Mf);
+    }
+}
+
+int64_t tclo_rdu_select(const float* pool, const int32_t* ops, int64_t n_pool, const float* lab,
+                        int64_t n_lab, int32_t n_ops, int32_t budget_total, int64_t* out_idx) {
+    if (n_pool <= 0 || budget_total <= 0 || n_ops < 1) return 0;
+    float lo = INFINITY, hi = -INFINITY;
+    for (int64_t i = 0; i < n_pool + n_lab; ++i) {
+        float v = i < n_pool ? pool[i] : lab[i - n_pool];
+        if (!isfinite(v)) continue;   /* only finite predictions take part (R21) */
+        if (v < lo) lo = v;
+        if (v > hi) hi = v;
+    }
+    int flat = !(hi > lo);
+    float range = hi - lo;
+#define NORM(v) (flat ? 0.5f : (((v) - lo) / range))
+    int64_t* count = (int64_t*)calloc((size_t)n_ops, sizeof(int64_t));
+    int64_t* sel = (int64_t*)calloc((size_t)n_ops, sizeof(int64_t));
+    float* budget = (float*)malloc(sizeof(float) * (size_t)n_ops);
+    for (int64_t i = 0; i < n_pool; ++i)
+        if (ops[i] >= 0 && ops[i] < n_ops) count[ops[i]]++;
+    for (int o = 0; o < n_ops; ++o) budget[o] = (float)((double)budget_total * (double)count[o] / (double)n_pool);
+    float S = 0.0f, Q = 0.0f, Mf = 0.0f;
+    for (int64_t j = 0; j < n_lab; ++j) {
+        if (!isfinite(lab[j])) continue;
+        float f = NORM(lab[j]);
+        S = S + f;
+        Q = Q + f * f;
+        Mf = Mf + 1.0f;
+    }
+    float* fh = (float*)malloc(sizeof(float) * (size_t)n_pool);
+    float* ds = (float*)malloc(sizeof(float) * (size_t)n_pool);
+    unsigned char* alive = (unsigned char*)malloc((size_t)n_pool);
+    for (int64_t i = 0; i < n_pool; ++i) {
+        fh[i] = NORM(pool[i]);
+        alive[i] = isfinite(pool[i]) && isfinite(fh[i]) && ops[i] >= 0 && ops[i] < n_ops;
+        float d = INFINITY;
+        for (int64_t j = 0; j < n_lab; ++j) {
+            if (!isfinite(lab[j])) continue;
+            float e = fabsf(fh[i] - NORM(lab[j]));
+            if (e < d) d = e;
+        }
+        ds[i] = d == INFINITY ? 1.0f : d;   /* empty labeled set: maximal novelty 1 */
+    }
+    int64_t picks = 0;
+    for (int32_t p = 0; p < budget_total; ++p) {
+        int64_t best = -1;
+        float bts = 0.0f, bf = 0.0f;
+        for (int64_t i = 0; i < n_pool; ++i) {
+            if (!alive[i] || !((float)sel[ops[i]] < budget[ops[i]])) continue;
+            float ts = rdu_total_score(fh[i], ds[i], S, Q, Mf);
+            if (best < 0 || ts > bts || (ts == bts && (fh[i] > bf || (fh[i] == bf && i < best)))) {
+                best = i;
+                bts = ts;
+                bf = fh[i];
+            }
+        }
+        if (best < 0) break;
+        out_idx[picks++] = best;
+        alive[best] = 0;
+        sel[ops[best]]++;
+        float fs = fh[best];
+        S = S + fs;
+        Q = Q + fs * fs;
+        Mf = Mf + 1.0f;
+        for (int64_t i = 0; i < n_pool; ++i) {
+            float e = fabsf(fh[i] - fs);
+            if (e < ds[i]) ds[i] = e;
+        }
+    }
+#undef NORM
+    free(count); free(sel); free(budget); free(fh); free(ds); free(alive);
+    return picks;
+}

@@ -619,6 +619,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     if (m->copy_stream) cudaStreamDestroy(m->copy_stream);
     for (auto ev : m->chunk_events) cudaEventDestroy(ev);
     for (void* q : m->bf_allocs) cudaFree(q);
+    if (m->rdu_scratch) cudaFree(m->rdu_scratch);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
     delete m;
@@ -702,6 +703,37 @@ tcl_status tcl_topk(tcl_model* m, const float* scores, int64_t n, int32_t k, int
     m->launches += launch_topk_keys(scores, n, k, index_base, keys, tmp, s);
     m->launches += launch_topk_merge(keys, k, k, idx, top, tmp, s);
     CUDA_TRY(cudaGetLastError());
+    return TCL_OK;
+}
+
+tcl_status tcl_rdu_select(tcl_model* m, const float* pool, const int32_t* ops, int64_t n_pool, const float* lab,
+                          int64_t n_lab, int32_t n_ops, int32_t budget_total, int64_t* out, int32_t* n_out,
+                          void* stream) {
+    if (!m || n_pool < 0 || n_lab < 0 || budget_total < 0 || n_ops < 1 || n_ops > 256)
+        return set_error(TCL_EINVAL, "bad argument");
+    if (!out || !n_out || (n_pool > 0 && (!pool || !ops)) || (n_lab > 0 && !lab))
+        return set_error(TCL_EINVAL, "null pointer");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_pool == 0 || budget_total == 0) {
+        CUDA_TRY(cudaMemsetAsync(n_out, 0, sizeof(int32_t), s));
+        return TCL_OK;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+    if (n_pool > (int64_t)4096 * sms) return set_error(TCL_ESHAPE, "n_pool exceeds 4096 * SM count");
+    const size_t need = rdu_scratch_bytes(sms, n_ops);
+    if (need > m->rdu_scratch_cap) {
+        if (m->rdu_scratch) cudaFree(m->rdu_scratch);
+        m->rdu_scratch = nullptr;
+        m->rdu_scratch_cap = 0;
+        CUDA_TRY(cudaMalloc(&m->rdu_scratch, need));
+        m->rdu_scratch_cap = need;
+    }
+    cudaError_t e = launch_rdu_select(pool, ops, n_pool, lab, n_lab, n_ops, budget_total, out, n_out,
+                                      m->rdu_scratch, sms, s);
+    if (e != cudaSuccess) return cuda_error(e, "rdu_select");
+    m->launches += 2;
     return TCL_OK;
 }
 

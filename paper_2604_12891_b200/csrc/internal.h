@@ -89,6 +89,8 @@ struct tcl_model {
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> chunk_events;
     int64_t launches = 0;
+    void* rdu_scratch = nullptr;
+    size_t rdu_scratch_cap = 0;
     // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)
     int use_tc = 0, num_sms = 148, nxp = 0, rp = 0, bn_in = 0;
     std::vector<void*> bf_allocs;

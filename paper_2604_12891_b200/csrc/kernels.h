@@ -108,4 +108,10 @@ int launch_topk_keys(const float* scores, int64_t n, int k, int64_t index_base,
 int launch_topk_merge(const unsigned long long* keys, int64_t count, int k, int64_t* idx,
                       float* score, unsigned long long* tmp, cudaStream_t s);
 
+// ---- RDU acquisition (Alg. 1, Eqs. 1-3) -------------------------------
+size_t rdu_scratch_bytes(int grid_max, int n_ops);
+cudaError_t launch_rdu_select(const float* pool, const int32_t* ops, int64_t n_pool, const float* lab,
+                              int64_t n_lab, int n_ops, int budget_total, int64_t* out, int32_t* n_out,
+                              void* scratch, int num_sms, cudaStream_t s);
+
 }  // namespace tcl

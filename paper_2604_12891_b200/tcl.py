@@ -46,7 +46,7 @@ class tcl_dims(ctypes.Structure):
 EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score",
            "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
-           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read"]
+           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select"]
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc"]
 
@@ -90,11 +90,12 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_profile_enable.argtypes = [vp, ctypes.c_int]
     L.tcl_profile_read.argtypes = [vp, P(ctypes.c_double), P(i64), ctypes.c_int]
     L.tcl_debug_read.argtypes = [vp, ctypes.c_char_p, vp, i64, i64]
+    L.tcl_rdu_select.argtypes = [vp, vp, vp, i64, vp, i64, i32, i32, vp, vp, vp]
     L.tcl_profile_name.restype = ctypes.c_char_p
     L.tcl_profile_name.argtypes = [ctypes.c_int]
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
-               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read"):
+               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -192,6 +193,14 @@ class Model:
     def tcl_topk_global(self, scores, index_base: int, k: int, idx, top, stream=None):
         _check(load().tcl_topk_global(self._h, _ptr(scores), scores.shape[0], index_base, k, _ptr(idx),
                                       _ptr(top), _stream(stream)))
+
+    def tcl_rdu_select(self, pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int,
+                       selected, n_selected, stream=None):
+        """RDU acquisition round (Alg. 1 lines 16-31): device tensors in, picks in `selected`."""
+        _check(load().tcl_rdu_select(self._h, _ptr(pool_scores), _ptr(pool_ops), pool_scores.shape[0],
+                                     _ptr(labeled_scores) if labeled_scores.shape[0] else None,
+                                     labeled_scores.shape[0], n_ops, budget_total, _ptr(selected),
+                                     _ptr(n_selected), _stream(stream)))
 
     def tcl_sync_error(self, stream=None):
         _check(load().tcl_sync_error(self._h, _stream(stream)))

@@ -1,0 +1,4 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -m pytest tests/test_gpu_rdu.py -x -q 2>&1 | tail -20
+python scripts/rdu_time.py

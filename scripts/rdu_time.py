@@ -1,0 +1,26 @@
+"""Time tcl_rdu_select on the rdu configuration's pool size (and the max pool) with CUDA events."""
+import sys, os, json
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+import inputs
+from paper_2604_12891_b200 import Model
+c = inputs.config("tiny"); d = c["dims"]
+m = Model(inputs.make_weights(d, c["seed"]), d)
+sms = torch.cuda.get_device_properties(0).multi_processor_count
+out = {}
+for n, lab_n, B, n_ops in ((16384, 1024, 1638, 13), (131072, 4096, 4096, 40), (4096 * sms, 4096, 4096, 40)):
+    rng = np.random.default_rng(0)
+    pool = torch.from_numpy(rng.normal(size=n).astype(np.float32)).cuda()
+    ops = torch.from_numpy(rng.integers(0, n_ops, n).astype(np.int32)).cuda()
+    lab = torch.from_numpy(rng.normal(size=lab_n).astype(np.float32)).cuda()
+    sel = torch.empty(B, dtype=torch.int64, device="cuda"); ns = torch.empty(1, dtype=torch.int32, device="cuda")
+    for _ in range(3): m.tcl_rdu_select(pool, ops, lab, n_ops, B, sel, ns)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10): m.tcl_rdu_select(pool, ops, lab, n_ops, B, sel, ns)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    out[f"n{n}_lab{lab_n}_B{B}"] = {"ms": ms, "us_per_pick": 1000 * ms / B, "picks": int(ns.item())}
+    print(n, lab_n, B, f"{ms:.3f} ms", f"{1000*ms/B:.2f} us/pick", flush=True)
+json.dump(out, open("gpurun_out/rdu_time.json", "w"), indent=1)
