@@ -155,6 +155,22 @@ tcl_status tcl_score_host(tcl_model* model, const float* feats_host, const int32
                           int64_t n, int64_t index_base, float* scores_host, int32_t k,
                           int64_t* idx_host, float* topscore_host, void* stream);
 
+/* Top-k score, Eq. 12 (§7.1.2; reading R22):
+ *   Top-k = sum_t minlat_t w_t / sum_t min{latency of task t's k best-predicted candidates} w_t
+ * Tasks (one per subgraph of a model) are CSR segments: candidates task_offsets_dev[t] ..
+ * task_offsets_dev[t+1]-1 (int64, [n_tasks+1], offsets into scores_dev / latency_dev) with
+ * predicted scores (larger = better; ties: lower index first; NaN = -inf, R15), true latencies
+ * (positive, finite) and a task weight task_weights_dev [n_tasks] (occurrence frequency).  k values
+ * come from ks_host [n_k] (1 <= n_k <= 16, each k >= 1; k > task size clamps to the task size).
+ * result_dev [3 * n_k] fp64 receives Top-k score[j], numerator[j], denominator[j].  Every task
+ * must hold 1 .. max_task_len candidates (max_task_len <= 16384); a task outside that range makes
+ * its terms NaN and tcl_sync_error return TCL_ESHAPE.  Integer ranking (exact); fp64 sums in a
+ * fixed order (deterministic).  Device pointers; asynchronous on `stream`. */
+tcl_status tcl_topk_score(tcl_model* model, const float* scores_dev, const float* latency_dev,
+                          const int64_t* task_offsets_dev, const float* task_weights_dev, int64_t n_tasks,
+                          int32_t max_task_len, const int32_t* ks_host, int32_t n_k, double* result_dev,
+                          void* stream);
+
 /* RDU acquisition, one selection round (Algorithm 1 lines 16-31,
  * Eqs. 1-3; reading R21 in DESIGN.md).  Given the model's predictions for the unlabeled pool
  * (pool_scores_dev [n_pool], with operator types pool_ops_dev [n_pool] in [0, n_ops)) and for the

@@ -266,3 +266,27 @@ def config(name: str) -> dict:
     c = dict(CONFIGS[name])
     c["name"] = name
     return c
+
+
+def make_eval_tasks(n_tasks: int, seed: int, min_len: int = 16, max_len: int = 4096, noise: float = 0.5,
+                    tie_quant: float = 0.0):
+    """Synthetic evaluation tasks for the Top-k score (Eq. 12): one task per (model, subgraph).
+
+    Shapes follow §7.1.1: a task is a subgraph with the programs measured for it (log-uniform
+    count in [min_len, max_len]); latencies are log-normal around a per-task scale; the predicted
+    score is a noisy monotone predictor (-log latency + noise·N(0,1)); weights are occurrence
+    frequencies (integers 1..8).  tie_quant > 0 quantises the scores (forces equal scores).
+    Returns (scores f32 [n], latency f32 [n], offsets i64 [n_tasks+1], weights f32 [n_tasks])."""
+    rng = np.random.default_rng(seed)
+    lens = np.exp(rng.uniform(np.log(min_len), np.log(max_len + 1), n_tasks)).astype(np.int64)
+    lens = np.clip(lens, min_len, max_len)
+    off = np.zeros(n_tasks + 1, np.int64)
+    off[1:] = np.cumsum(lens)
+    n = int(off[-1])
+    scale = np.repeat(rng.uniform(-9.0, -3.0, n_tasks), lens)          # log-seconds per task
+    lat = np.exp(scale + rng.normal(0.0, 0.6, n)).astype(np.float32)
+    sc = (-np.log(lat.astype(np.float64)) + noise * rng.normal(size=n)).astype(np.float32)
+    if tie_quant > 0:
+        sc = (np.round(sc / tie_quant) * tie_quant).astype(np.float32)
+    w = rng.integers(1, 9, n_tasks).astype(np.float32)
+    return sc, lat, off, w

@@ -74,6 +74,7 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_uint64, ctypes.c_int64, dp, dp, ctypes.c_int]
         L.tclo_topk_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, dp]
         L.tclo_topk_f32.argtypes = [fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, fp]
+        L.tclo_topk_score.argtypes = [fp, fp, lp, fp, ctypes.c_int64, ip, ctypes.c_int32, dp, dp, dp]
         L.tclo_rdu_scores.argtypes = [fp, ctypes.c_int64, fp, ctypes.c_int64, fp, fp, fp]
         L.tclo_rdu_select.restype = ctypes.c_int64
         L.tclo_rdu_select.argtypes = [fp, ip, ctypes.c_int64, fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, lp]
@@ -254,3 +255,18 @@ def rdu_scores(fh_pool, fh_lab):
     lib().tclo_rdu_scores(_p(fp_, ctypes.c_float), fp_.shape[0], _p(fl, ctypes.c_float), len(fh_lab),
                           _p(ds, ctypes.c_float), _p(us, ctypes.c_float), _p(ts, ctypes.c_float))
     return ds, us, ts
+
+
+def topk_score(scores, latency, task_offsets, task_weights, ks):
+    """Eq. 12 Top-k score for each k in ks: (score[], num[], den[]) in fp64."""
+    sc, la = _f32(scores), _f32(latency)
+    off = np.ascontiguousarray(task_offsets, dtype=np.int64)
+    w = _f32(task_weights)
+    kk = np.ascontiguousarray(ks, dtype=np.int32)
+    out, num, den = (np.zeros(kk.size) for _ in range(3))
+    rc = lib().tclo_topk_score(_p(sc, ctypes.c_float), _p(la, ctypes.c_float), _p(off, ctypes.c_int64),
+                               _p(w, ctypes.c_float), off.size - 1, _p(kk, ctypes.c_int32), kk.size,
+                               _p(out, ctypes.c_double), _p(num, ctypes.c_double), _p(den, ctypes.c_double))
+    if rc != 0:
+        raise ValueError("tclo_topk_score: bad arguments")
+    return out, num, den

@@ -618,3 +618,47 @@ int64_t tclo_rdu_select(const float* pool, const int32_t* ops, int64_t n_pool, c
     free(count); free(sel); free(budget); free(fh); free(ds); free(alive);
     return picks;
 }
+
+/* ------------------------------------------------------------------ Top-k score (NEXT #4) */
+/* PAPER.md Eq. 12 (§7.1.2), reading R22:
+ *   Top-k = sum_{m,s} min_latency_{m,s} w_{m,s} / sum_{m,s} min_{i in [1,k]} p_latency_{m,s,i} w_{m,s}
+ * Task t (one subgraph s of model m) holds candidates off[t] .. off[t+1]-1 with true latencies lat[]
+ * and predicted scores scores[] (larger = better, R14); p_latency_{m,s,i} is the latency of the
+ * i-th candidate ranked by predicted score (ties: lower index first, NaN = -inf: R15, the order
+ * tclo_topk_f64 defines); k larger than the task clamps to the task size.
+ * For each of the n_k values ks[j]: num[j], den[j] (fp64 sums in task order) and out[j] = num/den.
+ * Returns 0, or -1 on bad arguments (a task with no candidates, k < 1). */
+int tclo_topk_score(const float* scores, const float* lat, const int64_t* off, const float* w,
+                    int64_t n_tasks, const int32_t* ks, int32_t n_k, double* out, double* num, double* den) {
+    for (int32_t j = 0; j < n_k; ++j) {
+        if (ks[j] < 1) return -1;
+        num[j] = 0.0;
+        den[j] = 0.0;
+    }
+    for (int64_t t = 0; t < n_tasks; ++t) {
+        int64_t T = off[t + 1] - off[t];
+        if (T < 1) return -1;
+        double minlat = INFINITY;
+        double* s = (double*)malloc(sizeof(double) * (size_t)T);
+        for (int64_t i = 0; i < T; ++i) {
+            s[i] = (double)scores[off[t] + i];
+            if ((double)lat[off[t] + i] < minlat) minlat = (double)lat[off[t] + i];
+        }
+        for (int32_t j = 0; j < n_k; ++j) {
+            int32_t k = ks[j] < T ? ks[j] : (int32_t)T;
+            int64_t* idx = (int64_t*)malloc(sizeof(int64_t) * (size_t)k);
+            double* top = (double*)malloc(sizeof(double) * (size_t)k);
+            tclo_topk_f64(s, T, k, 0, idx, top);
+            double pmin = INFINITY;
+            for (int32_t r = 0; r < k; ++r)
+                if ((double)lat[off[t] + idx[r]] < pmin) pmin = (double)lat[off[t] + idx[r]];
+            num[j] += minlat * (double)w[t];
+            den[j] += pmin * (double)w[t];
+            free(idx);
+            free(top);
+        }
+        free(s);
+    }
+    for (int32_t j = 0; j < n_k; ++j) out[j] = num[j] / den[j];
+    return 0;
+}

@@ -620,6 +620,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     for (auto ev : m->chunk_events) cudaEventDestroy(ev);
     for (void* q : m->bf_allocs) cudaFree(q);
     if (m->rdu_scratch) cudaFree(m->rdu_scratch);
+    if (m->eval_cols) cudaFree(m->eval_cols);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
     delete m;
@@ -706,6 +707,36 @@ tcl_status tcl_topk(tcl_model* m, const float* scores, int64_t n, int32_t k, int
     return TCL_OK;
 }
 
+tcl_status tcl_topk_score(tcl_model* m, const float* scores, const float* lat, const int64_t* off, const float* w,
+                          int64_t n_tasks, int32_t max_task_len, const int32_t* ks_host, int32_t n_k,
+                          double* result, void* stream) {
+    if (!m || n_tasks < 1 || n_k < 1 || n_k > 16 || max_task_len < 1) return set_error(TCL_EINVAL, "bad argument");
+    if (max_task_len > 16384) return set_error(TCL_ESHAPE, "max_task_len > 16384");
+    if (!scores || !lat || !off || !w || !ks_host || !result) return set_error(TCL_EINVAL, "null pointer");
+    tcl::TopkEvalKs ks{};
+    ks.n = n_k;
+    for (int j = 0; j < n_k; ++j) {
+        if (ks_host[j] < 1) return set_error(TCL_EINVAL, "k < 1");
+        ks.k[j] = ks_host[j];
+    }
+    CUDA_TRY(cudaSetDevice(m->device));
+    const size_t need = (size_t)(n_k + 1) * (size_t)n_tasks;
+    if (need > m->eval_cols_cap) {
+        if (m->eval_cols) cudaFree(m->eval_cols);
+        m->eval_cols = nullptr;
+        m->eval_cols_cap = 0;
+        CUDA_TRY(cudaMalloc(&m->eval_cols, need * sizeof(double)));
+        m->eval_cols_cap = need;
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m->device);
+    cudaError_t e = tcl::launch_topk_eval(scores, lat, off, w, n_tasks, max_task_len, ks, m->eval_cols, result,
+                                          m->d_err, sms, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_error(e, "topk_score");
+    m->launches += 2;
+    return TCL_OK;
+}
+
 tcl_status tcl_rdu_select(tcl_model* m, const float* pool, const int32_t* ops, int64_t n_pool, const float* lab,
                           int64_t n_lab, int32_t n_ops, int32_t budget_total, int64_t* out, int32_t* n_out,
                           void* stream) {
@@ -745,6 +776,7 @@ tcl_status tcl_sync_error(tcl_model* m, void* stream) {
     CUDA_TRY(cudaMemcpy(&flag, m->d_err, sizeof(int), cudaMemcpyDeviceToHost));
     CUDA_TRY(cudaMemset(m->d_err, 0, sizeof(int)));
     if (flag & ERR_LEN) return set_error(TCL_ELEN, "a candidate length outside [1, max_len] was seen");
+    if (flag & ERR_TASK) return set_error(TCL_ESHAPE, "a task with 0 or more than max_task_len candidates was seen");
     return TCL_OK;
 }
 

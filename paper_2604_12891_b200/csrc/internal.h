@@ -91,6 +91,8 @@ struct tcl_model {
     int64_t launches = 0;
     void* rdu_scratch = nullptr;
     size_t rdu_scratch_cap = 0;
+    double* eval_cols = nullptr;   // tcl_topk_score per-task columns
+    size_t eval_cols_cap = 0;
     // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)
     int use_tc = 0, num_sms = 148, nxp = 0, rp = 0, bn_in = 0;
     std::vector<void*> bf_allocs;

@@ -8,7 +8,7 @@
 namespace tcl {
 
 // Device error bits (sticky, tcl_sync_error).
-enum : int { ERR_LEN = 1 };
+enum : int { ERR_LEN = 1, ERR_TASK = 2 };
 
 // ---- pack ------------------------------------------------------------------
 // cu[n+1] exclusive prefix of the valid lengths (invalid lengths count as 0 rows and raise
@@ -109,6 +109,11 @@ int launch_topk_merge(const unsigned long long* keys, int64_t count, int k, int6
                       float* score, unsigned long long* tmp, cudaStream_t s);
 
 // ---- RDU acquisition (Alg. 1, Eqs. 1-3) -------------------------------
+// Top-k score (Eq. 12): up to 16 k values per call.
+struct TopkEvalKs { int n; int k[16]; };
+cudaError_t launch_topk_eval(const float* scores, const float* lat, const int64_t* off, const float* w,
+                             int64_t n_tasks, int max_task_len, const TopkEvalKs& ks, double* cols,
+                             double* out, int* err, int num_sms, cudaStream_t s);
 size_t rdu_scratch_bytes(int grid_max, int n_ops);
 cudaError_t launch_rdu_select(const float* pool, const int32_t* ops, int64_t n_pool, const float* lab,
                               int64_t n_lab, int n_ops, int budget_total, int64_t* out, int32_t* n_out,

@@ -46,7 +46,8 @@ class tcl_dims(ctypes.Structure):
 EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score",
            "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
-           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select"]
+           "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
+           "tcl_topk_score"]
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc"]
 
@@ -91,11 +92,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_profile_read.argtypes = [vp, P(ctypes.c_double), P(i64), ctypes.c_int]
     L.tcl_debug_read.argtypes = [vp, ctypes.c_char_p, vp, i64, i64]
     L.tcl_rdu_select.argtypes = [vp, vp, vp, i64, vp, i64, i32, i32, vp, vp, vp]
+    L.tcl_topk_score.argtypes = [vp, vp, vp, vp, vp, i64, i32, vp, i32, vp, vp]
     L.tcl_profile_name.restype = ctypes.c_char_p
     L.tcl_profile_name.argtypes = [ctypes.c_int]
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
-               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select"):
+               "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select",
+               "tcl_topk_score"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -193,6 +196,14 @@ class Model:
     def tcl_topk_global(self, scores, index_base: int, k: int, idx, top, stream=None):
         _check(load().tcl_topk_global(self._h, _ptr(scores), scores.shape[0], index_base, k, _ptr(idx),
                                       _ptr(top), _stream(stream)))
+
+    def tcl_topk_score(self, scores, latency, task_offsets, task_weights, max_task_len: int, ks, result,
+                       stream=None):
+        """Eq. 12 Top-k score over CSR tasks (device tensors); result [3*len(ks)] fp64 = score|num|den."""
+        kk = np.ascontiguousarray(ks, dtype=np.int32)
+        _check(load().tcl_topk_score(self._h, _ptr(scores), _ptr(latency), _ptr(task_offsets),
+                                     _ptr(task_weights), task_offsets.shape[0] - 1, max_task_len,
+                                     kk.ctypes.data, kk.size, _ptr(result), _stream(stream)))
 
     def tcl_rdu_select(self, pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int,
                        selected, n_selected, stream=None):

@@ -24,3 +24,19 @@ for n, lab_n, B, n_ops in ((16384, 1024, 1638, 13), (131072, 4096, 4096, 40), (4
     out[f"n{n}_lab{lab_n}_B{B}"] = {"ms": ms, "us_per_pick": 1000 * ms / B, "picks": int(ns.item())}
     print(n, lab_n, B, f"{ms:.3f} ms", f"{1000*ms/B:.2f} us/pick", flush=True)
 json.dump(out, open("gpurun_out/rdu_time.json", "w"), indent=1)
+
+# Top-k score (Eq. 12): 5 models x ~ 400 subgraphs of 16..4096 programs
+sc, lat, off, w = inputs.make_eval_tasks(2000, 1)
+ks = [1, 5, 10]
+args = [torch.from_numpy(a).cuda() for a in (sc, lat, off, w)]
+res = torch.empty(9, dtype=torch.float64, device="cuda")
+ml = int(np.diff(off).max())
+for _ in range(3): m.tcl_topk_score(*args, ml, ks, res)
+torch.cuda.synchronize()
+e0.record()
+for _ in range(10): m.tcl_topk_score(*args, ml, ks, res)
+e1.record(); torch.cuda.synchronize()
+ms = e0.elapsed_time(e1) / 10
+out["topk_score_2000_tasks"] = {"ms": ms, "candidates": int(off[-1]), "Gcand_per_s": off[-1] / ms / 1e6}
+print("topk_score", int(off[-1]), f"{ms:.3f} ms", flush=True)
+json.dump(out, open("gpurun_out/rdu_time.json", "w"), indent=1)
