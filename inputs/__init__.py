@@ -290,3 +290,53 @@ def make_eval_tasks(n_tasks: int, seed: int, min_len: int = 16, max_len: int = 4
         sc = (np.round(sc / tie_quant) * tie_quant).astype(np.float32)
     w = rng.integers(1, 9, n_tasks).astype(np.float32)
     return sc, lat, off, w
+
+
+def adapter_layout(d: Dims, a: int) -> List[Tuple[str, Tuple[int, ...]]]:
+    """KB+AC lateral adapters (Eq. 7, reading R23), per site in the order enc1, enc2, enc3,
+    layer 0..n_layer-1, dec1, dec2: V [a][in], c [a], U [out][a], alpha [out]."""
+    sites = [("enc1", d.d_in, d.enc_dims[0]), ("enc2", d.enc_dims[0], d.enc_dims[1]),
+             ("enc3", d.enc_dims[1], d.d_model)]
+    sites += [(f"layer{l}", d.d_model, d.d_model) for l in range(d.n_layer)]
+    sites += [("dec1", d.d_model, d.dec_dims[0]), ("dec2", d.dec_dims[0], d.dec_dims[1])]
+    out = []
+    for name, i, o in sites:
+        out += [(f"{name}.V", (a, i)), (f"{name}.c", (a,)), (f"{name}.U", (o, a)), (f"{name}.alpha", (o,))]
+    return out
+
+
+def adapters_count(d: Dims, a: int) -> int:
+    return sum(int(np.prod(s)) for _, s in adapter_layout(d, a))
+
+
+def make_adapters(d: Dims, a: int, seed: int, alpha_range=(0.2, 1.0)) -> np.ndarray:
+    """Seeded adapter blob: V, U LeCun-uniform, c ~ U(+-1/sqrt(in)), alpha ~ U(alpha_range)."""
+    rng = np.random.default_rng(seed)
+    parts = []
+    for name, shp in adapter_layout(d, a):
+        kind = name.split(".")[1]
+        if kind == "V" or kind == "U":
+            fan_in = shp[1]
+            v = rng.uniform(-np.sqrt(3.0 / fan_in), np.sqrt(3.0 / fan_in), shp)
+        elif kind == "c":
+            fan_in = [s for nm, s in adapter_layout(d, a) if nm == name.replace(".c", ".V")][0][1]
+            v = rng.uniform(-1 / np.sqrt(fan_in), 1 / np.sqrt(fan_in), shp)
+        else:
+            v = rng.uniform(alpha_range[0], alpha_range[1], shp)
+        parts.append(v.astype(np.float32).ravel())
+    return np.concatenate(parts)
+
+
+def split_adapters(d: Dims, a: int, blob: np.ndarray) -> Dict[str, np.ndarray]:
+    out, off = {}, 0
+    for name, shp in adapter_layout(d, a):
+        cnt = int(np.prod(shp))
+        out[name] = blob[off:off + cnt].reshape(shp)
+        off += cnt
+    return out
+
+
+def default_adapter_rank(d: Dims) -> int:
+    """Reading R23: adapter width a = dt_rank = ceil(d_model / 16) (the paper gives only the 0.7 MB
+    total of KB + AC at d_model 128; a = 8 gives 0.74 MiB)."""
+    return d.dt_rank

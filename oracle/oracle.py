@@ -74,6 +74,11 @@ def lib() -> ctypes.CDLL:
                                     ctypes.c_uint64, ctypes.c_int64, dp, dp, ctypes.c_int]
         L.tclo_topk_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, dp]
         L.tclo_topk_f32.argtypes = [fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, fp]
+        L.tclo_adapters_count.restype = ctypes.c_int64
+        L.tclo_adapters_count.argtypes = [P(_Dims), ctypes.c_int]
+        L.tclo_score_kbac.argtypes = [P(_Dims), fp, fp, fp, ctypes.c_int, fp, ip, ctypes.c_int64, dp, ctypes.c_int]
+        L.tclo_score_mc_kbac.argtypes = [P(_Dims), fp, fp, fp, ctypes.c_int, fp, ip, ctypes.c_int64, ctypes.c_int32,
+                                         ctypes.c_uint64, ctypes.c_int64, dp, dp, ctypes.c_int]
         L.tclo_topk_score.argtypes = [fp, fp, lp, fp, ctypes.c_int64, ip, ctypes.c_int32, dp, dp, dp]
         L.tclo_rdu_scores.argtypes = [fp, ctypes.c_int64, fp, ctypes.c_int64, fp, fp, fp]
         L.tclo_rdu_select.restype = ctypes.c_int64
@@ -270,3 +275,39 @@ def topk_score(scores, latency, task_offsets, task_weights, ks):
     if rc != 0:
         raise ValueError("tclo_topk_score: bad arguments")
     return out, num, den
+
+
+def adapters_count(d, a: int) -> int:
+    """Floats in the KB+AC adapter blob of rank a (Eq. 7 sites, reading R23)."""
+    return int(lib().tclo_adapters_count(ctypes.byref(_cdims(d)), a))
+
+
+def score_kbac(d, kb_w, ac_w, ad_w, a: int, feats, lens, nthreads: Optional[int] = None) -> np.ndarray:
+    """KB + AC two-column scores (Eq. 7 lateral adapters; the AC column's output)."""
+    feats = _f32(feats)
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    n = lens.shape[0]
+    out = np.zeros(n, dtype=np.float64)
+    rc = lib().tclo_score_kbac(ctypes.byref(_cdims(d)), _p(_f32(kb_w), ctypes.c_float), _p(_f32(ac_w), ctypes.c_float),
+                               _p(_f32(ad_w), ctypes.c_float), a, _p(feats, ctypes.c_float),
+                               _p(lens, ctypes.c_int32), n, _p(out, ctypes.c_double), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError("tclo_score_kbac failed")
+    return out
+
+
+def score_mc_kbac(d, kb_w, ac_w, ad_w, a: int, feats, lens, n_passes: int, seed: int, index_base: int = 0,
+                  nthreads: Optional[int] = None) -> Tuple[np.ndarray, np.ndarray]:
+    feats = _f32(feats)
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    n = lens.shape[0]
+    mean = np.zeros(n, dtype=np.float64)
+    var = np.zeros(n, dtype=np.float64)
+    rc = lib().tclo_score_mc_kbac(ctypes.byref(_cdims(d)), _p(_f32(kb_w), ctypes.c_float),
+                                  _p(_f32(ac_w), ctypes.c_float), _p(_f32(ad_w), ctypes.c_float), a,
+                                  _p(feats, ctypes.c_float), _p(lens, ctypes.c_int32), n, n_passes, seed,
+                                  index_base, _p(mean, ctypes.c_double), _p(var, ctypes.c_double),
+                                  nthreads or default_threads())
+    if rc != 0:
+        raise ValueError("tclo_score_mc_kbac failed")
+    return mean, var

@@ -237,8 +237,74 @@ typedef struct {
     int64_t gidx;
 } mc_ctx;
 
+/* ---- KB + AC two-column model (§6 Eq. 7; reading R23).
+ * The AC's layer i output is h_i = act(W_i h_{i-1} + alpha_i (.) U_i SiLU(V_i h^KB_{i-1} + c_i) + b_i)
+ * at every encoder linear, after every Mamba block (act = identity: the lateral joins the
+ * residual stream) and at the two hidden decoder layers; h^KB_{i-1} is the KB's input to its own
+ * layer i (the features for encoder layer 1).  The KB runs first, deterministic (frozen); its
+ * site inputs are recorded and read by the AC column.  Adapter blob, per site in the order
+ * enc1, enc2, enc3, layer 0..n_layer-1, dec1, dec2: V [a][in], c [a], U [out][a], alpha [out]. */
+typedef struct {
+    double *e1, *e2, *hin, *pooled, *dh1;   /* KB site inputs: [T][e1], [T][e2], [n_layer][T][dm], [dm], [h1] */
+} kb_rec;
+typedef struct {
+    const float *V, *c, *U, *alpha;
+    int in, out;
+} adapter_w;
+typedef struct {
+    const kb_rec* kb;
+    const adapter_w* ad;   /* sites: 0..2 encoder, 3..3+n_layer-1 Mamba blocks, then dec1, dec2 */
+    int a;
+} lateral_ctx;
+
+/* y[o] += alpha[o] * sum_j U[o][j] SiLU(sum_i V[j][i] hkb[i] + c[j])   (the Eq. 7 lateral term) */
+static void lateral_add(const adapter_w* A, int a, const double* hkb, double* y) {
+    double* sj = (double*)calloc((size_t)a, sizeof(double));
+    for (int j = 0; j < a; ++j) {
+        double v = (double)A->c[j];
+        for (int i = 0; i < A->in; ++i) v += (double)A->V[(size_t)j * A->in + i] * hkb[i];
+        sj[j] = tclo_silu(v);
+    }
+    for (int o = 0; o < A->out; ++o) {
+        double u = 0.0;
+        for (int j = 0; j < a; ++j) u += (double)A->U[(size_t)o * a + j] * sj[j];
+        y[o] += (double)A->alpha[o] * u;
+    }
+    free(sj);
+}
+
+static int adapter_sites(const tclo_dims* d, int a, const float* blob, adapter_w* out, int64_t* count) {
+    const int ins[3] = {d->d_in, d->enc_dims[0], d->enc_dims[1]};
+    const int outs[3] = {d->enc_dims[0], d->enc_dims[1], d->d_model};
+    const int nsite = 3 + d->n_layer + 2;
+    int64_t off = 0;
+    for (int s = 0; s < nsite; ++s) {
+        int in, o;
+        if (s < 3) { in = ins[s]; o = outs[s]; }
+        else if (s < 3 + d->n_layer) { in = d->d_model; o = d->d_model; }
+        else if (s == 3 + d->n_layer) { in = d->d_model; o = d->dec_dims[0]; }
+        else { in = d->dec_dims[0]; o = d->dec_dims[1]; }
+        if (out) {
+            out[s].in = in; out[s].out = o;
+            out[s].V = blob + off;
+            out[s].c = blob + off + (int64_t)a * in;
+            out[s].U = blob + off + (int64_t)a * in + a;
+            out[s].alpha = blob + off + (int64_t)a * in + a + (int64_t)o * a;
+        }
+        off += (int64_t)a * in + a + (int64_t)o * a + o;
+    }
+    if (count) *count = off;
+    return nsite;
+}
+
+int64_t tclo_adapters_count(const tclo_dims* d, int a) {
+    int64_t c = 0;
+    adapter_sites(d, a, NULL, NULL, &c);
+    return c;
+}
+
 static double forward_one(const tclo_dims* d, const float* wblob, const float* x_in, int T,
-                          const mc_ctx* mc, double* dump) {
+                          const mc_ctx* mc, double* dump, kb_rec* rec, const lateral_ctx* lat) {
     const int dm = d->d_model, di = d->expand * d->d_model, N = d->d_state, R = d->dt_rank;
     const int e1 = d->enc_dims[0], e2 = d->enc_dims[1];
     const int h1 = d->dec_dims[0], h2 = d->dec_dims[1];
@@ -260,16 +326,21 @@ static double forward_one(const tclo_dims* d, const float* wblob, const float* x
     for (int t = 0; t < T; ++t) {
         for (int i = 0; i < d->d_in; ++i) xin[i] = (double)x_in[(size_t)t * d->d_in + i];
         linear(enc.W1, enc.b1, e1, d->d_in, xin, t1);
+        if (lat) lateral_add(&lat->ad[0], lat->a, xin, t1);                 /* h^KB_0 = the features */
         for (int i = 0; i < e1; ++i) {
             t1[i] = tclo_silu(t1[i]);
             if (mc && mc->mc_pass >= 0) t1[i] *= dropout_mult(mc->seed, p, thr, i, t, 0, mc->mc_pass, mc->gidx);
         }
+        if (rec) memcpy(&rec->e1[(size_t)t * e1], t1, sizeof(double) * e1);
         linear(enc.W2, enc.b2, e2, e1, t1, t2);
+        if (lat) lateral_add(&lat->ad[1], lat->a, &lat->kb->e1[(size_t)t * e1], t2);
         for (int i = 0; i < e2; ++i) {
             t2[i] = tclo_silu(t2[i]);
             if (mc && mc->mc_pass >= 0) t2[i] *= dropout_mult(mc->seed, p, thr, i, t, 1, mc->mc_pass, mc->gidx);
         }
+        if (rec) memcpy(&rec->e2[(size_t)t * e2], t2, sizeof(double) * e2);
         linear(enc.W3, enc.b3, dm, e2, t2, &h[(size_t)t * dm]);
+        if (lat) lateral_add(&lat->ad[2], lat->a, &lat->kb->e2[(size_t)t * e2], &h[(size_t)t * dm]);
     }
     if (dp) { memcpy(dp, h, sizeof(double) * T * dm); dp += (size_t)T * dm; }
 
@@ -291,6 +362,7 @@ static double forward_one(const tclo_dims* d, const float* wblob, const float* x
 
     for (int l = 0; l < d->n_layer; ++l) {
         const layer_w* q = &L[l];
+        if (rec) memcpy(&rec->hin[(size_t)l * T * dm], h, sizeof(double) * (size_t)T * dm);
         /* pre-norm (R2, R3) and in_proj */
         for (int t = 0; t < T; ++t) {
             tclo_layernorm_row(&h[(size_t)t * dm], dm, q->ln_w, q->ln_b, eps, &a[(size_t)t * dm]);
@@ -316,6 +388,8 @@ static double forward_one(const tclo_dims* d, const float* wblob, const float* x
             for (int i = 0; i < di; ++i) g[(size_t)t * di + i] = y[(size_t)t * di + i] * tclo_silu(z[(size_t)t * di + i]);
             linear(q->W_out, NULL, dm, di, &g[(size_t)t * di], o);
             for (int i = 0; i < dm; ++i) h[(size_t)t * dm + i] += o[i];
+            /* Eq. 7 at the Mamba-block output (identity activation: joins the residual stream) */
+            if (lat) lateral_add(&lat->ad[3 + l], lat->a, &lat->kb->hin[((size_t)l * T + t) * dm], &h[(size_t)t * dm]);
         }
         if (dp) {
 #define DUMP(src, cnt) do { memcpy(dp, src, sizeof(double) * (size_t)(cnt)); dp += (cnt); } while (0)
@@ -333,12 +407,16 @@ static double forward_one(const tclo_dims* d, const float* wblob, const float* x
         for (int i = 0; i < dm; ++i) pooled[i] += f[i];
     }
     for (int i = 0; i < dm; ++i) pooled[i] /= (double)T;
+    if (rec) memcpy(rec->pooled, pooled, sizeof(double) * dm);
     linear(dec.W1, dec.b1, h1, dm, pooled, t1);
+    if (lat) lateral_add(&lat->ad[3 + d->n_layer], lat->a, lat->kb->pooled, t1);
     for (int i = 0; i < h1; ++i) {
         t1[i] = tclo_silu(t1[i]);
         if (mc && mc->mc_pass >= 0) t1[i] *= dropout_mult(mc->seed, p, thr, i, 0, 2, mc->mc_pass, mc->gidx);
     }
+    if (rec) memcpy(rec->dh1, t1, sizeof(double) * h1);
     linear(dec.W2, dec.b2, h2, h1, t1, t2);
+    if (lat) lateral_add(&lat->ad[4 + d->n_layer], lat->a, lat->kb->dh1, t2);
     for (int i = 0; i < h2; ++i) {
         t2[i] = tclo_silu(t2[i]);
         if (mc && mc->mc_pass >= 0) t2[i] *= dropout_mult(mc->seed, p, thr, i, 0, 3, mc->mc_pass, mc->gidx);
@@ -354,6 +432,27 @@ static double forward_one(const tclo_dims* d, const float* wblob, const float* x
     return score;
 }
 
+/* Two-column forward (R23): the frozen KB column (deterministic, site inputs recorded), then the
+ * AC column reading them through the lateral adapters; the AC's output is the score.  MC dropout
+ * (when mc) applies to the AC column only. */
+static double forward_kbac(const tclo_dims* d, const float* kb_w, const float* ac_w, const float* ad_w, int a,
+                           const float* x_in, int T, const mc_ctx* mc) {
+    const int dm = d->d_model;
+    kb_rec rec;
+    rec.e1 = (double*)calloc((size_t)T * d->enc_dims[0], sizeof(double));
+    rec.e2 = (double*)calloc((size_t)T * d->enc_dims[1], sizeof(double));
+    rec.hin = (double*)calloc((size_t)(d->n_layer > 0 ? d->n_layer : 1) * T * dm, sizeof(double));
+    rec.pooled = (double*)calloc((size_t)dm, sizeof(double));
+    rec.dh1 = (double*)calloc((size_t)d->dec_dims[0], sizeof(double));
+    adapter_w* ad = (adapter_w*)calloc((size_t)(5 + d->n_layer), sizeof(adapter_w));
+    adapter_sites(d, a, ad_w, ad, NULL);
+    (void)forward_one(d, kb_w, x_in, T, NULL, NULL, &rec, NULL);
+    lateral_ctx lat = {&rec, ad, a};
+    double score = forward_one(d, ac_w, x_in, T, mc, NULL, NULL, &lat);
+    free(ad); free(rec.dh1); free(rec.pooled); free(rec.hin); free(rec.e2); free(rec.e1);
+    return score;
+}
+
 /* Size of the dump of forward_one, in doubles. */
 int64_t tclo_dump_size(const tclo_dims* d, int T) {
     const int64_t dm = d->d_model, di = (int64_t)d->expand * d->d_model, N = d->d_state, R = d->dt_rank;
@@ -366,7 +465,7 @@ int64_t tclo_dump_size(const tclo_dims* d, int T) {
 int tclo_forward_one(const tclo_dims* d, const float* w, const float* feats_one, int T, double* dump,
                      double* score) {
     if (!dims_ok(d) || T < 1 || T > d->max_len) return -1;
-    *score = forward_one(d, w, feats_one, T, NULL, dump);
+    *score = forward_one(d, w, feats_one, T, NULL, dump, NULL, NULL);
     return 0;
 }
 
@@ -383,6 +482,9 @@ typedef struct {
     double* scores;   /* deterministic mode */
     double* mean;     /* MC mode */
     double* var;
+    const float* kb_w;   /* non-NULL: KB + AC two-column model; w is the AC column */
+    const float* ad_w;
+    int ad_rank;
 } job_t;
 
 static void* worker(void* arg) {
@@ -397,13 +499,15 @@ static void* worker(void* arg) {
             continue;
         }
         if (j->mc_passes <= 0) {
-            j->scores[i] = forward_one(j->d, j->w, xf, T, NULL, NULL);
+            j->scores[i] = j->kb_w ? forward_kbac(j->d, j->kb_w, j->w, j->ad_w, j->ad_rank, xf, T, NULL)
+                                   : forward_one(j->d, j->w, xf, T, NULL, NULL, NULL, NULL);
         } else {
             /* Welford over passes; population variance (divide by the number of passes) (R17) */
             double m = 0.0, M2 = 0.0;
             for (int ps = 0; ps < j->mc_passes; ++ps) {
                 mc_ctx mc = {ps, j->seed, j->index_base + i};
-                double v = forward_one(j->d, j->w, xf, T, &mc, NULL);
+                double v = j->kb_w ? forward_kbac(j->d, j->kb_w, j->w, j->ad_w, j->ad_rank, xf, T, &mc)
+                                   : forward_one(j->d, j->w, xf, T, &mc, NULL, NULL, NULL);
                 double delta = v - m;
                 m += delta / (double)(ps + 1);
                 M2 += delta * (v - m);
@@ -435,7 +539,23 @@ static int run_threads(job_t* proto, int nthreads) {
 int tclo_score(const tclo_dims* d, const float* w, const float* feats, const int32_t* lens,
                int64_t n, double* scores, int nthreads) {
     if (!dims_ok(d) || n < 0) return -1;
-    job_t j = {d, w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL};
+    job_t j = {d, w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, NULL, NULL, 0};
+    return run_threads(&j, nthreads);
+}
+
+/* KB + AC two-column scores (R23): kb_w, ac_w canonical blobs, ad_w the adapter blob of rank a. */
+int tclo_score_kbac(const tclo_dims* d, const float* kb_w, const float* ac_w, const float* ad_w, int a,
+                    const float* feats, const int32_t* lens, int64_t n, double* scores, int nthreads) {
+    if (!dims_ok(d) || n < 0 || a < 1) return -1;
+    job_t j = {d, ac_w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, kb_w, ad_w, a};
+    return run_threads(&j, nthreads);
+}
+
+int tclo_score_mc_kbac(const tclo_dims* d, const float* kb_w, const float* ac_w, const float* ad_w, int a,
+                       const float* feats, const int32_t* lens, int64_t n, int32_t n_passes, uint64_t seed,
+                       int64_t index_base, double* mean, double* var, int nthreads) {
+    if (!dims_ok(d) || n < 0 || n_passes < 1 || a < 1) return -1;
+    job_t j = {d, ac_w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, kb_w, ad_w, a};
     return run_threads(&j, nthreads);
 }
 
@@ -445,7 +565,7 @@ int tclo_score_mc(const tclo_dims* d, const float* w, const float* feats, const 
                   int64_t n, int32_t n_passes, uint64_t seed, int64_t index_base, double* mean,
                   double* var, int nthreads) {
     if (!dims_ok(d) || n < 0 || n_passes < 1) return -1;
-    job_t j = {d, w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var};
+    job_t j = {d, w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, NULL, NULL, 0};
     return run_threads(&j, nthreads);
 }
 
