@@ -155,6 +155,23 @@ tcl_status tcl_score_host(tcl_model* model, const float* feats_host, const int32
                           int64_t n, int64_t index_base, float* scores_host, int32_t k,
                           int64_t* idx_host, float* topscore_host, void* stream);
 
+/* KB + AC two-column model (§6, Eq. 7; reading R23):
+ * the model TCL deploys on a target after continual knowledge distillation.  Both columns share
+ * `dims` (canonical blobs of tcl_weights_count(dims) floats each).  The AC's layer i output is
+ *   h_i = act(W_i h_{i-1} + alpha_i (.) U_i SiLU(V_i h^KB_{i-1} + c_i) + b_i)
+ * at the three encoder linears, after every Mamba block (act = identity: added to the residual
+ * stream) and at the two hidden decoder layers; h^KB_{i-1} is the KB's input to its own layer i
+ * (the features for encoder layer 1).  Adapter blob (adapters_host, tcl_adapters_count floats),
+ * per site in the order enc1, enc2, enc3, layer 0..n_layer-1, dec1, dec2:
+ *   V [a][in], c [a], U [out][a], alpha [out]   (a = adapter_rank, 1..64).
+ * The returned handle is used with tcl_score / tcl_score_mc / tcl_score_host / tcl_topk like a
+ * one-column model; the score is the AC column's output; MC dropout applies to the AC column only
+ * (the KB is frozen).  TCL_PREC_FP32 only (TCL_ESHAPE otherwise).  Host buffers are copied. */
+size_t tcl_adapters_count(const tcl_dims* dims, int32_t adapter_rank);
+tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_weights_host, size_t n_floats,
+                                 const float* adapters_host, size_t n_adapter_floats, int32_t adapter_rank,
+                                 const tcl_dims* dims, int cuda_device, tcl_model** out);
+
 /* Top-k score, Eq. 12 (§7.1.2; reading R22):
  *   Top-k = sum_t minlat_t w_t / sum_t min{latency of task t's k best-predicted candidates} w_t
  * Tasks (one per subgraph of a model) are CSR segments: candidates task_offsets_dev[t] ..
@@ -203,7 +220,7 @@ int64_t tcl_launch_count(const tcl_model* model);
 typedef enum {
     TCL_PROF_PACK = 0, TCL_PROF_ENCODER, TCL_PROF_LAYERNORM, TCL_PROF_IN_PROJ, TCL_PROF_CONV,
     TCL_PROF_X_PROJ, TCL_PROF_DT_PROJ, TCL_PROF_SCAN, TCL_PROF_OUT_PROJ, TCL_PROF_HEAD,
-    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_NKINDS
+    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_LATERAL, TCL_PROF_NKINDS
 } tcl_prof_kind;
 tcl_status tcl_profile_enable(tcl_model* model, int enable);
 tcl_status tcl_profile_read(tcl_model* model, double* ms_out, int64_t* launches_out, int reset);

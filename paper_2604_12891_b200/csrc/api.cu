@@ -231,6 +231,19 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     TAKE(dh1, chunk_n * d.dec_dims[0]);
     TAKE(dh2, chunk_n * d.dec_dims[1]);
     TAKE(dsc, chunk_n);
+    if (m->kb) {
+        TAKE(Hk, rows * dm);
+        TAKE(E1k, rows * d.enc_dims[0]);
+        TAKE(E2k, rows * d.enc_dims[1]);
+        TAKE(Lat, rows * m->ad_ld);
+        TAKE(pooled_k, chunk_n * dm);
+        TAKE(dh1k, chunk_n * d.dec_dims[0]);
+        // columns a .. ad_ld of Lat are never written: zero them once (they meet zero weights)
+        if (cudaMemset(w.Lat, 0, sizeof(float) * (size_t)(rows * m->ad_ld)) != cudaSuccess) {
+            free_workspace(m);
+            return set_error(TCL_ECUDA, "cudaMemset(Lat)");
+        }
+    }
     if (m->use_tc) {
         const int64_t xzw = std::max<int64_t>(2 * di, (int64_t)d.enc_dims[0] + d.enc_dims[1]);
         TAKE(Xb, rows * kXld);
@@ -309,70 +322,163 @@ static void run_head(tcl_model* m, const int32_t* lens, int64_t n, float* scores
 }
 
 // ------------------------------------------------------------------------------ forward
-// One chunk of candidates [0, n) (pointers already offset).  If mc_mean != nullptr the head
-// accumulates Welford statistics for pass drop.pass instead of writing scores.
-static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
-                          float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
-    const tcl_dims& d = m->dims;
-    Workspace& w = m->ws;
-    const int L = d.max_len, dm = d.d_model, di = d.expand * d.d_model, N = d.d_state,
-              R = d.dt_rank;
-    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
-    const int max_rows = (int)(n * L);
-    const int32_t* P = w.cu + n;  // device: number of packed rows
-    int64_t& nl = m->launches;
+// fp32 launch helpers shared by the one-column and the KB + AC two-column forward.
+struct F32Run {
+    tcl_model* m;      // owner of the workspace (the AC column for KB + AC)
+    int max_rows;
+    const int32_t* P;  // device: packed row count
+    DropoutCtx drop;
+    cudaStream_t s;
+    const int32_t* lens;
+    int64_t n;
 
-    {
-        ProfScope ps(m, TCL_PROF_PACK, s);
-        launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++nl;
-        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++nl;
-    }
-
-    auto gemm = [&](const float* X, int ldx, const float* W, int ldw, const float* b, float* Y,
-                    int ldy, int K, int Nout, int epi, int site, int kind) {
+    // Y = epi(X W^T [+ X2 W2^T] + b) over the packed rows (or over the n candidates: cands = true)
+    void gemm(const float* X, int ldx, const float* W, int ldw, const float* b, float* Y, int ldy, int K,
+              int Nout, int epi, int site, int kind, const float* X2 = nullptr, int ldx2 = 0,
+              const float* W2 = nullptr, int K2 = 0, bool cands = false, bool dropout = true) const {
         ProfScope ps(m, kind, s);
         GemmArgs g{};
         g.X = X; g.ldx = ldx; g.W = W; g.ldw = ldw; g.bias = b; g.Y = Y; g.ldy = ldy;
-        g.K = K; g.N = Nout; g.max_rows = max_rows; g.p_rows = P; g.epi = epi;
-        g.drop = drop; g.site = site; g.row_cand = w.row_cand; g.cu = w.cu;
-        if (epi != EPI_SILU) g.drop.enabled = 0;
+        g.K = K; g.N = Nout; g.epi = epi; g.drop = drop; g.site = site;
+        if (cands) { g.max_rows = (int)n; g.rows_const = (int)n; g.rows_are_cands = 1; }
+        else { g.max_rows = max_rows; g.p_rows = P; g.row_cand = m->ws.row_cand; g.cu = m->ws.cu; }
+        g.X2 = X2; g.ldx2 = ldx2; g.W2 = W2; g.ldw2 = K2; g.K2 = K2;
+        if (epi != EPI_SILU || !dropout) g.drop.enabled = 0;
         launch_gemm_simt(g, s);
-        ++nl;
-    };
-    // encoder (P:449, P:451): SiLU after linears 1 and 2 (R1), dropout sites 0, 1 (R17)
-    float* E1 = w.U;      // aliases: encoder hidden states live in the mixer buffers
-    float* E2 = w.Delta;
-    gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
-    gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
-    gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER);
-
-    for (int l = 0; l < d.n_layer; ++l) {
-        const LayerPtrs& q = m->wp.layers[l];
+        ++m->launches;
+    }
+    // Lat = SiLU(V hkb + c) for one Eq. 7 site (no dropout: the adapters' inner activation)
+    void lateral(const AdapterSite& a, const float* hkb, int ldh, bool cands) const {
+        gemm(hkb, ldh, a.V, a.ldv, a.c, m->ws.Lat, m->ad_ld, a.ldv, m->ad_rank, EPI_SILU, -1,
+             TCL_PROF_LATERAL, nullptr, 0, nullptr, 0, cands, false);
+    }
+    // One Mamba block of column `col` on the residual stream H (pre-norm, in_proj, conv, x_proj,
+    // dt_proj, scan, out_proj + residual); `site` adds the Eq. 7 lateral to out_proj's sums.
+    void layer(const tcl_model* col, int l, float* H, const AdapterSite* site) const {
+        const tcl_dims& d = m->dims;
+        Workspace& w = m->ws;
+        const int dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
+        const LayerPtrs& q = col->wp.layers[l];
         {
             ProfScope ps(m, TCL_PROF_LAYERNORM, s);
-            launch_layernorm(w.H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s); ++nl;
+            launch_layernorm(H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s); ++m->launches;
         }
         gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
         {
             ProfScope ps(m, TCL_PROF_CONV, s);
             launch_conv_silu(w.XZ, 2 * di, q.w_conv, q.b_conv, di, d.d_conv, w.U, w.row_cand, w.cu,
-                             max_rows, P, s); ++nl;
+                             max_rows, P, s); ++m->launches;
         }
         gemm(w.U, di, q.W_x, di, nullptr, w.DBC, m->ldbc, di, R + 2 * N, EPI_NONE, -1, TCL_PROF_X_PROJ);
         gemm(w.DBC, m->ldbc, q.W_dt, R, q.b_dt, w.Delta, di, R, di, EPI_SOFTPLUS, -1, TCL_PROF_DT_PROJ);
         ScanArgs sa{};
         sa.U = w.U; sa.Delta = w.Delta; sa.Z = w.XZ + di; sa.ldz = 2 * di;
         sa.BC = w.DBC; sa.ldbc = m->ldbc; sa.b_off = R; sa.c_off = R + N;
-        sa.A2 = m->A2 + (size_t)l * di * N; sa.invA = m->invA + (size_t)l * di * N; sa.Dv = q.Dv;
+        sa.A2 = col->A2 + (size_t)l * di * N; sa.invA = col->invA + (size_t)l * di * N; sa.Dv = q.Dv;
         sa.G = w.G; sa.cu = w.cu; sa.lens = lens; sa.n = n; sa.di = di; sa.N = N; sa.disc = d.disc;
-        sa.accurate = d.precision == TCL_PREC_FP32; sa.max_len = L;
+        sa.accurate = d.precision == TCL_PREC_FP32; sa.max_len = d.max_len;
         {
             ProfScope ps(m, TCL_PROF_SCAN, s);
-            launch_scan(sa, s); ++nl;
+            launch_scan(sa, s); ++m->launches;
         }
-        gemm(w.G, di, q.W_out, di, nullptr, w.H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ);
+        if (site)
+            gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ, w.Lat, m->ad_ld,
+                 site->Ua, m->ad_ld);
+        else
+            gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ);
     }
+};
 
+// KB + AC two-column forward (§6 Eq. 7, reading R23), fp32 path.  Site by site the KB
+// (frozen, deterministic) runs first; Lat = SiLU(V h^KB_{i-1} + c) is formed from the KB's input
+// to that site and enters the AC's GEMM as a second K segment against diag(alpha) U (the lateral
+// sum joins the same accumulators, before bias and activation).  MC dropout: AC column only.
+static void forward_chunk_kbac(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
+                               float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+    const tcl_dims& d = m->dims;
+    Workspace& w = m->ws;
+    const tcl_model* kb = m->kb;
+    const int L = d.max_len, dm = d.d_model;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1], h1 = d.dec_dims[0], h2 = d.dec_dims[1];
+    const int ld = m->ad_ld;
+    F32Run r{m, (int)(n * L), w.cu + n, drop, s, lens, n};
+    const std::vector<AdapterSite>& ad = m->ad;
+    {
+        ProfScope ps(m, TCL_PROF_PACK, s);
+        launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++m->launches;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++m->launches;
+    }
+    float* E1 = w.U;
+    float* E2 = w.Delta;
+    // encoder layer 1: h^KB_0 = the features
+    r.gemm(w.X, kXld, kb->W1p, kXld, kb->wp.enc_b1, w.E1k, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER, nullptr, 0,
+           nullptr, 0, false, false);
+    r.lateral(ad[0], w.X, kXld, false);
+    r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER, w.Lat, ld, ad[0].Ua, ld);
+    // encoder layer 2
+    r.lateral(ad[1], w.E1k, e1, false);
+    r.gemm(w.E1k, e1, kb->wp.enc_W2, e1, kb->wp.enc_b2, w.E2k, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER, nullptr, 0,
+           nullptr, 0, false, false);
+    r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER, w.Lat, ld, ad[1].Ua, ld);
+    // encoder layer 3 (no activation, R1)
+    r.lateral(ad[2], w.E2k, e2, false);
+    r.gemm(w.E2k, e2, kb->wp.enc_W3, e2, kb->wp.enc_b3, w.Hk, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER);
+    r.gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER, w.Lat, ld,
+           ad[2].Ua, ld);
+    // Mamba blocks: the lateral reads the KB's block input, so it is formed before the KB block runs
+    DropoutCtx nodrop = drop;
+    nodrop.enabled = 0;
+    F32Run rk = r;
+    rk.drop = nodrop;
+    for (int l = 0; l < d.n_layer; ++l) {
+        r.lateral(ad[3 + l], w.Hk, dm, false);
+        rk.layer(kb, l, w.Hk, nullptr);
+        r.layer(m, l, w.H, &ad[3 + l]);
+    }
+    // head: KB pooled + dec1 (its inputs to the AC's dec1 / dec2 laterals), then the AC decoder
+    {
+        ProfScope ps(m, TCL_PROF_HEAD, s);
+        launch_pool(w.Hk, dm, dm, kb->wp.lnf_w, kb->wp.lnf_b, d.ln_eps, w.cu, lens, L, n, w.pooled_k, s);
+        launch_pool(w.H, dm, dm, m->wp.lnf_w, m->wp.lnf_b, d.ln_eps, w.cu, lens, L, n, w.pooled, s);
+        m->launches += 2;
+    }
+    r.gemm(w.pooled_k, dm, kb->wp.dec_W1, dm, kb->wp.dec_b1, w.dh1k, h1, dm, h1, EPI_SILU, 2, TCL_PROF_HEAD, nullptr,
+           0, nullptr, 0, true, false);
+    r.lateral(ad[3 + d.n_layer], w.pooled_k, dm, true);
+    r.gemm(w.pooled, dm, m->wp.dec_W1, dm, m->wp.dec_b1, w.dh1, h1, dm, h1, EPI_SILU, 2, TCL_PROF_HEAD, w.Lat, ld,
+           ad[3 + d.n_layer].Ua, ld, true);
+    r.lateral(ad[4 + d.n_layer], w.dh1k, h1, true);
+    r.gemm(w.dh1, h1, m->wp.dec_W2, h1, m->wp.dec_b2, w.dh2, h2, h1, h2, EPI_SILU, 3, TCL_PROF_HEAD, w.Lat, ld,
+           ad[4 + d.n_layer].Ua, ld, true);
+    float* out = mc_mean ? w.dsc : scores;
+    r.gemm(w.dh2, h2, m->wp.dec_W3, h2, m->wp.dec_b3, out, 1, h2, 1, EPI_NONE, -1, TCL_PROF_HEAD, nullptr, 0, nullptr,
+           0, true);
+    if (mc_mean) launch_welford(w.dsc, lens, L, n, drop.pass, mc_mean, w.m2, s);
+    else launch_mask_invalid(lens, L, n, scores, s);
+    ++m->launches;
+}
+
+// One chunk of candidates [0, n) (pointers already offset).  If mc_mean != nullptr the head
+// accumulates Welford statistics for pass drop.pass instead of writing scores.
+static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
+                          float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+    const tcl_dims& d = m->dims;
+    Workspace& w = m->ws;
+    const int L = d.max_len, dm = d.d_model;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+    F32Run r{m, (int)(n * L), w.cu + n, drop, s, lens, n};
+    {
+        ProfScope ps(m, TCL_PROF_PACK, s);
+        launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++m->launches;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++m->launches;
+    }
+    // encoder (P:449, P:451): SiLU after linears 1 and 2 (R1), dropout sites 0, 1 (R17)
+    float* E1 = w.U;      // aliases: encoder hidden states live in the mixer buffers
+    float* E2 = w.Delta;
+    r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
+    r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
+    r.gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER);
+    for (int l = 0; l < d.n_layer; ++l) r.layer(m, l, w.H, nullptr);
     run_head(m, lens, n, scores, drop, mc_mean, s);
 }
 
@@ -500,6 +606,10 @@ static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* l
         if (st != TCL_OK) return st;
         return debug_sync("forward_chunk_tc", s);
     }
+    if (m->kb) {
+        forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s);
+        return debug_sync("forward_chunk_kbac", s);
+    }
     forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s);
     return debug_sync("forward_chunk", s);
 }
@@ -605,6 +715,77 @@ tcl_status tcl_model_create(const float* weights_host, size_t n_floats, const tc
     return TCL_OK;
 }
 
+static int64_t adapters_count_of(const tcl_dims& d, int a, std::vector<AdapterSite>* sites) {
+    const int ins[3] = {d.d_in, d.enc_dims[0], d.enc_dims[1]};
+    const int outs[3] = {d.enc_dims[0], d.enc_dims[1], d.d_model};
+    int64_t c = 0;
+    for (int s = 0; s < 5 + d.n_layer; ++s) {
+        int in, out;
+        if (s < 3) { in = ins[s]; out = outs[s]; }
+        else if (s < 3 + d.n_layer) { in = out = d.d_model; }
+        else if (s == 3 + d.n_layer) { in = d.d_model; out = d.dec_dims[0]; }
+        else { in = d.dec_dims[0]; out = d.dec_dims[1]; }
+        if (sites) sites->push_back(AdapterSite{nullptr, nullptr, nullptr, in, out, s == 0 ? kXld : in});
+        c += (int64_t)a * in + a + (int64_t)out * a + out;
+    }
+    return c;
+}
+
+size_t tcl_adapters_count(const tcl_dims* dims, int32_t adapter_rank) {
+    if (!dims || adapter_rank < 1) return 0;
+    return (size_t)adapters_count_of(*dims, adapter_rank, nullptr);
+}
+
+tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_weights_host, size_t n_floats,
+                                 const float* adapters_host, size_t n_adapter_floats, int32_t adapter_rank,
+                                 const tcl_dims* dims, int cuda_device, tcl_model** out) {
+    if (!kb_weights_host || !ac_weights_host || !adapters_host || !out) return set_error(TCL_EINVAL, "null pointer");
+    *out = nullptr;
+    tcl_status st = validate_dims(dims);
+    if (st != TCL_OK) return st;
+    if (dims->precision != TCL_PREC_FP32) return set_error(TCL_ESHAPE, "KB+AC: only TCL_PREC_FP32 is supported");
+    if (adapter_rank < 1 || adapter_rank > 64) return set_error(TCL_ESHAPE, "adapter_rank must be in [1, 64]");
+    std::vector<AdapterSite> sites;
+    if ((int64_t)n_adapter_floats != adapters_count_of(*dims, adapter_rank, &sites))
+        return set_error(TCL_ESHAPE, "n_adapter_floats does not match tcl_adapters_count(dims, adapter_rank)");
+    tcl_model *kb = nullptr, *m = nullptr;
+    if ((st = tcl_model_create(kb_weights_host, n_floats, dims, cuda_device, &kb)) != TCL_OK) return st;
+    if ((st = tcl_model_create(ac_weights_host, n_floats, dims, cuda_device, &m)) != TCL_OK) {
+        tcl_model_destroy(kb);
+        return st;
+    }
+    m->kb = kb;
+    const int a = adapter_rank, ld = round_up(a, 16);
+    m->ad_rank = a;
+    m->ad_ld = ld;
+    // device layout per site: V [a][ldv] (zero-padded), c [a], Ua = diag(alpha) U [out][ld] (zero-padded)
+    std::vector<float> host;
+    std::vector<size_t> offs;
+    const float* p = adapters_host;
+    for (AdapterSite& st_ : sites) {
+        const float *V = p, *c = p + (size_t)a * st_.in, *U = c + a, *alpha = U + (size_t)st_.out * a;
+        p = alpha + st_.out;
+        offs.push_back(host.size());
+        for (int j = 0; j < a; ++j)
+            for (int i = 0; i < st_.ldv; ++i) host.push_back(i < st_.in ? V[(size_t)j * st_.in + i] : 0.0f);
+        for (int j = 0; j < a; ++j) host.push_back(c[j]);
+        for (int o = 0; o < st_.out; ++o)
+            for (int j = 0; j < ld; ++j) host.push_back(j < a ? alpha[o] * U[(size_t)o * a + j] : 0.0f);
+    }
+    if ((st = dev_alloc(&m->ad_dev, host.size())) != TCL_OK) { tcl_model_destroy(m); return st; }
+    cudaError_t e = cudaMemcpy(m->ad_dev, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { tcl_model_destroy(m); return cuda_error(e, "cudaMemcpy(adapters)"); }
+    for (size_t k = 0; k < sites.size(); ++k) {
+        AdapterSite& q = sites[k];
+        q.V = m->ad_dev + offs[k];
+        q.c = q.V + (size_t)a * q.ldv;
+        q.Ua = q.c + a;
+    }
+    m->ad = sites;
+    *out = m;
+    return TCL_OK;
+}
+
 tcl_status tcl_model_destroy(tcl_model* m) {
     if (!m) return TCL_OK;
     cudaSetDevice(m->device);
@@ -621,6 +802,8 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     for (void* q : m->bf_allocs) cudaFree(q);
     if (m->rdu_scratch) cudaFree(m->rdu_scratch);
     if (m->eval_cols) cudaFree(m->eval_cols);
+    if (m->ad_dev) cudaFree(m->ad_dev);
+    if (m->kb) tcl_model_destroy(m->kb);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
     delete m;
@@ -840,7 +1023,7 @@ tcl_status tcl_profile_read(tcl_model* m, double* ms_out, int64_t* launches_out,
 const char* tcl_profile_name(int kind) {
     static const char* names[TCL_PROF_NKINDS] = {"pack", "encoder", "layernorm", "in_proj", "conv",
                                                  "x_proj", "dt_proj", "scan", "out_proj", "head",
-                                                 "topk", "mixer", "allgather", "mc"};
+                                                 "topk", "mixer", "allgather", "mc", "lateral"};
     return (kind >= 0 && kind < TCL_PROF_NKINDS) ? names[kind] : "";
 }
 

@@ -27,6 +27,13 @@ struct WeightPtrs {  // device pointers into the fp32 blob (canonical order, inc
     const float *dec_W1, *dec_b1, *dec_W2, *dec_b2, *dec_W3, *dec_b3;
 };
 
+// One Eq. 7 lateral site: V [a][ldv] (zero-padded input columns), c [a], Ua = diag(alpha) U
+// [out][ad_ld] (zero-padded to a multiple of 16 columns).
+struct AdapterSite {
+    const float *V, *c, *Ua;
+    int in, out, ldv;
+};
+
 struct Workspace {
     int64_t cap_n = 0, rows = 0;
     int32_t* cu = nullptr;        // [cap_n + 1]
@@ -52,6 +59,13 @@ struct Workspace {
     CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
     CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
     CUtensorMap tmHf, tmAo;
+    // KB + AC two-column model (fp32 path): the KB column's buffers and the lateral activations
+    float* Hk = nullptr;          // [rows][dm]  KB residual stream
+    float* E1k = nullptr;         // [rows][e1]  KB encoder hidden 1
+    float* E2k = nullptr;         // [rows][e2]  KB encoder hidden 2
+    float* Lat = nullptr;         // [rows][ad_ld] SiLU(V h^KB + c), columns >= a stay zero
+    float* pooled_k = nullptr;    // [cap_n][dm]
+    float* dh1k = nullptr;        // [cap_n][h1]
     CUtensorMap tmAbS;                                 // in_proj A slices for cluster multicast (box {64, 128/n_tiles})                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
     std::vector<void*> allocs;
 };
@@ -91,6 +105,11 @@ struct tcl_model {
     int64_t launches = 0;
     void* rdu_scratch = nullptr;
     size_t rdu_scratch_cap = 0;
+    // KB + AC two-column model (tcl_model_create_kbac): this object holds the AC column
+    tcl_model* kb = nullptr;      // the KB column (weights only; its workspace is unused)
+    int ad_rank = 0, ad_ld = 0;
+    float* ad_dev = nullptr;
+    std::vector<tcl::AdapterSite> ad;   // enc1, enc2, enc3, layer 0..n_layer-1, dec1, dec2
     double* eval_cols = nullptr;   // tcl_topk_score per-task columns
     size_t eval_cols_cap = 0;
     // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)

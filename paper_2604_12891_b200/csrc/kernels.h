@@ -36,6 +36,9 @@ struct GemmArgs {
     // dropout (EPI_SILU only): per-row candidate and token
     DropoutCtx drop; int site;
     const int32_t* row_cand; const int32_t* cu;
+    // optional second operand pair accumulated into the same sums (KB+AC lateral term of Eq. 7):
+    // Y = epi(X W^T + X2 W2^T + b), X2 [M][ldx2], W2 [N][ldw2], K2 columns; K % 16 == 0 when K2 > 0
+    const float* X2; int ldx2; const float* W2; int ldw2; int K2;
 };
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 

@@ -28,15 +28,22 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
 
-    for (int k0 = 0; k0 < a.K; k0 += BK) {
+    const int k_end = a.K + a.K2;
+    for (int k0 = 0; k0 < k_end; k0 += BK) {
         {
-            const int gm = m0 + lr, gk = k0 + lk;
+            // k in [0, K): X / W; k in [K, K + K2): the lateral pair X2 / W2 (K2 > 0 only)
+            const bool second = k0 >= a.K;
+            const float* X = second ? a.X2 : a.X;
+            const float* W = second ? a.W2 : a.W;
+            const int ldx = second ? a.ldx2 : a.ldx, ldw = second ? a.ldw2 : a.ldw;
+            const int kk_end = second ? a.K2 : a.K;
+            const int gm = m0 + lr, gk = (second ? k0 - a.K : k0) + lk;
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gm < rows && gk < a.K) v = *reinterpret_cast<const float4*>(a.X + (int64_t)gm * a.ldx + gk);
+            if (gm < rows && gk < kk_end) v = *reinterpret_cast<const float4*>(X + (int64_t)gm * ldx + gk);
             As[lk + 0][lr] = v.x; As[lk + 1][lr] = v.y; As[lk + 2][lr] = v.z; As[lk + 3][lr] = v.w;
             const int gn = n0 + lr;
             float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gn < a.N && gk < a.K) w = __ldg(reinterpret_cast<const float4*>(a.W + (int64_t)gn * a.ldw + gk));
+            if (gn < a.N && gk < kk_end) w = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
             Ws[lk + 0][lr] = w.x; Ws[lk + 1][lr] = w.y; Ws[lk + 2][lr] = w.z; Ws[lk + 3][lr] = w.w;
         }
         __syncthreads();

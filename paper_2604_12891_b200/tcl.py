@@ -47,9 +47,9 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
            "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
-           "tcl_topk_score"]
+           "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac"]
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
-              "head", "topk", "mixer", "allgather", "mc"]
+              "head", "topk", "mixer", "allgather", "mc", "lateral"]
 
 _lib: Optional[ctypes.CDLL] = None
 
@@ -72,6 +72,9 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_weights_count.restype = sz
     L.tcl_weights_count.argtypes = [P(tcl_dims)]
     L.tcl_model_create.argtypes = [vp, sz, P(tcl_dims), ctypes.c_int, P(vp)]
+    L.tcl_model_create_kbac.argtypes = [vp, vp, sz, vp, sz, i32, P(tcl_dims), ctypes.c_int, P(vp)]
+    L.tcl_adapters_count.restype = sz
+    L.tcl_adapters_count.argtypes = [P(tcl_dims), i32]
     L.tcl_model_destroy.argtypes = [vp]
     L.tcl_reserve.argtypes = [vp, i64, i32]
     L.tcl_score.argtypes = [vp, vp, vp, i64, vp, vp]
@@ -98,7 +101,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
                "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select",
-               "tcl_topk_score"):
+               "tcl_topk_score", "tcl_model_create_kbac"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -156,6 +159,24 @@ class Model:
         _check(load().tcl_model_create(w.ctypes.data, w.size, ctypes.byref(tcl_dims.of(dims)), device,
                                        ctypes.byref(h)))
         self._h = h
+
+    @classmethod
+    def kbac(cls, kb_weights: np.ndarray, ac_weights: np.ndarray, adapters: np.ndarray, adapter_rank: int, dims,
+             device: int = 0) -> "Model":
+        """KB + AC two-column model (Eq. 7 lateral adapters); scores are the AC column's output."""
+        kb = np.ascontiguousarray(kb_weights, dtype=np.float32)
+        ac = np.ascontiguousarray(ac_weights, dtype=np.float32)
+        ad = np.ascontiguousarray(adapters, dtype=np.float32)
+        if kb.size != ac.size:
+            raise ValueError("KB and AC weight blobs differ in size")
+        self = cls.__new__(cls)
+        self.dims = dims
+        self.device = device
+        h = ctypes.c_void_p()
+        _check(load().tcl_model_create_kbac(kb.ctypes.data, ac.ctypes.data, ac.size, ad.ctypes.data, ad.size,
+                                            adapter_rank, ctypes.byref(tcl_dims.of(dims)), device, ctypes.byref(h)))
+        self._h = h
+        return self
 
     def close(self):
         if getattr(self, "_h", None) and self._h.value:

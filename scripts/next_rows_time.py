@@ -23,7 +23,7 @@ for n, lab_n, B, n_ops in ((16384, 1024, 1638, 13), (131072, 4096, 4096, 40), (4
     ms = e0.elapsed_time(e1) / 10
     out[f"n{n}_lab{lab_n}_B{B}"] = {"ms": ms, "us_per_pick": 1000 * ms / B, "picks": int(ns.item())}
     print(n, lab_n, B, f"{ms:.3f} ms", f"{1000*ms/B:.2f} us/pick", flush=True)
-json.dump(out, open("gpurun_out/rdu_time.json", "w"), indent=1)
+json.dump(out, open("gpurun_out/next_rows_time.json", "w"), indent=1)
 
 # Top-k score (Eq. 12): 5 models x ~ 400 subgraphs of 16..4096 programs
 sc, lat, off, w = inputs.make_eval_tasks(2000, 1)
@@ -39,4 +39,23 @@ e1.record(); torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 10
 out["topk_score_2000_tasks"] = {"ms": ms, "candidates": int(off[-1]), "Gcand_per_s": off[-1] / ms / 1e6}
 print("topk_score", int(off[-1]), f"{ms:.3f} ms", flush=True)
-json.dump(out, open("gpurun_out/rdu_time.json", "w"), indent=1)
+json.dump(out, open("gpurun_out/next_rows_time.json", "w"), indent=1)
+
+# KB + AC two-column inference vs the one-column model (fp32 path): paper and tuning configs
+from paper_2604_12891_b200 import Model as _M
+for name, n in (("paper", 16384), ("tuning", 16384)):
+    c = inputs.config(name); d = c["dims"]; a = inputs.default_adapter_rank(d)
+    kbw = inputs.make_weights(d, 1); acw = inputs.make_weights(d, 2); adw = inputs.make_adapters(d, a, 3)
+    f, l = inputs.make_features(d, n, 5, workload="tuning")
+    ft, lt = torch.from_numpy(f).cuda(), torch.from_numpy(l).cuda()
+    s = torch.empty(n, device="cuda")
+    for label, mm in (("one_column", _M(acw, d)), ("kb_ac", _M.kbac(kbw, acw, adw, a, d))):
+        for _ in range(3): mm.tcl_score(ft, lt, s)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(10): mm.tcl_score(ft, lt, s)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 10
+        out[f"{name}_{label}"] = {"n": n, "ms": ms, "cand_per_s": n / ms * 1e3}
+        print(name, label, f"{ms:.3f} ms", f"{n / ms * 1e3:.0f} cand/s", flush=True)
+json.dump(out, open("gpurun_out/next_rows_time.json", "w"), indent=1)

@@ -1,0 +1,105 @@
+"""GPU parity of the KB + AC two-column model (tcl_model_create_kbac; Eq. 7, reading R23) against
+oracle.score_kbac / score_mc_kbac, tolerance as the fp32 path: 1e-4 * max(1, |ref|)."""
+import numpy as np
+import pytest
+
+import inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2604_12891_b200 import build
+    build.build()
+    return torch
+
+
+def _setup(name, n=None, seed=0):
+    c = inputs.config(name)
+    d = c["dims"]
+    a = inputs.default_adapter_rank(d)
+    kb = inputs.make_weights(d, c["seed"] + 10 + seed)
+    ac = inputs.make_weights(d, c["seed"] + 20 + seed)
+    ad = inputs.make_adapters(d, a, c["seed"] + 30 + seed)
+    n = c["n"] if n is None else n
+    f, l = inputs.make_features(d, n, c["seed"] + 1, workload="tuning")
+    return d, a, kb, ac, ad, f, l
+
+
+def _score(torch, m, f, l):
+    s = torch.empty(l.shape[0], device="cuda")
+    m.tcl_score(torch.from_numpy(f).cuda(), torch.from_numpy(l).cuda(), s)
+    m.tcl_sync_error()
+    return s.cpu().numpy()
+
+
+@pytest.mark.parametrize("name,n", [("tiny", None), ("paper", 1000), ("tuning", 1500)])
+def test_kbac_parity(torch_cuda, oracle, name, n):
+    from paper_2604_12891_b200 import Model
+    d, a, kb, ac, ad, f, l = _setup(name, n)
+    m = Model.kbac(kb, ac, ad, a, d)
+    got = _score(torch_cuda, m, f, l)
+    ref = oracle.score_kbac(d, kb, ac, ad, a, f, l)
+    err = np.abs(got - ref)
+    assert np.all(err <= 1e-4 * np.maximum(1.0, np.abs(ref))), err.max()
+    # the laterals matter at this tolerance
+    assert np.abs(ref - oracle.score(d, ac, f, l)).max() > 1e-2
+
+
+def test_kbac_closed_gate_equals_plain_ac(torch_cuda):
+    """alpha = 0: the lateral K segment multiplies zero weights -> bit-identical to the AC alone."""
+    from paper_2604_12891_b200 import Model
+    d, a, kb, ac, ad, f, l = _setup("tuning", 300)
+    ad = ad.copy()
+    off = 0
+    for name, shp in inputs.adapter_layout(d, a):
+        cnt = int(np.prod(shp))
+        if name.endswith(".alpha"):
+            ad[off:off + cnt] = 0.0
+        off += cnt
+    got = _score(torch_cuda, Model.kbac(kb, ac, ad, a, d), f, l)
+    plain = _score(torch_cuda, Model(ac, d), f, l)
+    assert np.array_equal(got, plain)
+
+
+def test_kbac_batch_invariance_and_host_path(torch_cuda, oracle):
+    from paper_2604_12891_b200 import Model
+    d, a, kb, ac, ad, f, l = _setup("paper", 600)
+    m = Model.kbac(kb, ac, ad, a, d)
+    full = _score(torch_cuda, m, f, l)
+    part = _score(torch_cuda, m, f[100:350], l[100:350])
+    assert np.array_equal(full[100:350], part)
+    scores, idx, top = m.tcl_score_host(f, l, k=16)
+    assert np.array_equal(scores, full)
+    assert idx.tolist() == np.argsort(-full, kind="stable")[:16].tolist()
+
+
+def test_kbac_mc_parity(torch_cuda, oracle):
+    from paper_2604_12891_b200 import Model
+    d, a, kb, ac, ad, f, l = _setup("tiny", 200)
+    m = Model.kbac(kb, ac, ad, a, d)
+    mean = torch_cuda.empty(200, device="cuda")
+    var = torch_cuda.empty(200, device="cuda")
+    m.tcl_score_mc(torch_cuda.from_numpy(f).cuda(), torch_cuda.from_numpy(l).cuda(), 6, 4321, 0, mean, var)
+    m.tcl_sync_error()
+    rm, rv = oracle.score_mc_kbac(d, kb, ac, ad, a, f, l, 6, 4321, 0)
+    assert np.all(np.abs(mean.cpu().numpy() - rm) <= 1e-4 * np.maximum(1.0, np.abs(rm)))
+    assert np.all(np.abs(var.cpu().numpy() - rv) <= 1e-4 * np.maximum(1.0, np.abs(rv)))
+
+
+def test_kbac_rejects_bf16_and_bad_sizes(torch_cuda):
+    from paper_2604_12891_b200 import Model
+    from paper_2604_12891_b200.tcl import TclError
+    c = inputs.config("large")
+    d = c["dims"]
+    w = inputs.make_weights(d, 1)
+    ad = inputs.make_adapters(d, 16, 2)
+    with pytest.raises(TclError):
+        Model.kbac(w, w, ad, 16, d)
+    d2, a, kb, ac, ad2, f, l = _setup("tiny", 8)
+    with pytest.raises(TclError):
+        Model.kbac(kb, ac, ad2[:-1], a, d2)
