@@ -172,6 +172,27 @@ tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_w
                                  const float* adapters_host, size_t n_adapter_floats, int32_t adapter_rank,
                                  const tcl_dims* dims, int cuda_device, tcl_model** out);
 
+/* Training (§5.3 Eq. 6, §7.1.3; reading R24), fp32 one-column
+ * models only (TCL_ESHAPE otherwise).  tcl_train_init allocates the training state for batches of
+ * up to n_max candidates (gradients, Adam moments (zero), saved activations) and sets Adam's lr,
+ * beta1, beta2, eps (paper: Adam, lr 7e-4) and the LambdaRank scale sigma_rank (1).
+ * tcl_train_step runs one step on a batch already on the device: feats/lens as tcl_score,
+ * latency_dev [n] the measured latencies (> 0), group_offsets_dev [n_groups+1] int64 CSR groups
+ * (one tuning task each; 2 <= members <= max_group <= 4096), the loss
+ *   L = mean_g sum_{y_i > y_j} |G_i - G_j| |1/D_i - 1/D_j| log2(1 + e^{-sigma (s_i - s_j)}),
+ *   y = min latency of the group / latency, G = (2^y - 1) / maxDCG, D = log2(1 + predicted rank)
+ * (fp32) goes to loss_dev [1] (may be NULL), the gradient of every weight (canonical blob layout)
+ * is computed by the backward pass, and apply_update != 0 applies one Adam step to the model's
+ * weights (scoring calls then use the updated model).  No dropout during training.
+ * tcl_train_read copies (synchronising) what = 0: weights [tcl_weights_count], 1: last gradients
+ * [tcl_weights_count], 2: last dL/dscore [n], 3: last training scores [n] to host memory. */
+tcl_status tcl_train_init(tcl_model* model, int64_t n_max, float lr, float beta1, float beta2, float eps,
+                          float sigma_rank);
+tcl_status tcl_train_step(tcl_model* model, const float* feats_dev, const int32_t* lens_dev, int64_t n,
+                          const float* latency_dev, const int64_t* group_offsets_dev, int64_t n_groups,
+                          int32_t max_group, int32_t apply_update, float* loss_dev, void* stream);
+tcl_status tcl_train_read(tcl_model* model, int32_t what, float* host, int64_t count);
+
 /* Top-k score, Eq. 12 (§7.1.2; reading R22):
  *   Top-k = sum_t minlat_t w_t / sum_t min{latency of task t's k best-predicted candidates} w_t
  * Tasks (one per subgraph of a model) are CSR segments: candidates task_offsets_dev[t] ..

@@ -803,6 +803,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     if (m->rdu_scratch) cudaFree(m->rdu_scratch);
     if (m->eval_cols) cudaFree(m->eval_cols);
     if (m->ad_dev) cudaFree(m->ad_dev);
+    if (m->tr) { for (void* q : m->tr->allocs) cudaFree(q); delete m->tr; m->tr = nullptr; }
     if (m->kb) tcl_model_destroy(m->kb);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
@@ -1095,3 +1096,262 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
 }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------------------ training
+// SURVEY §8(f) NEXT #3 (reading R24): one LambdaRank (Eq. 6) training step of the fp32 model --
+// forward with saved activations, loss + score gradient, backward of every layer, Adam (§7.1.3).
+
+static void free_train(tcl_model* m) {
+    if (!m->tr) return;
+    for (void* p : m->tr->allocs) cudaFree(p);
+    delete m->tr;
+    m->tr = nullptr;
+}
+
+tcl_status tcl_train_init(tcl_model* m, int64_t n_max, float lr, float beta1, float beta2, float eps,
+                          float sigma_rank) {
+    if (!m || n_max < 1 || !(lr > 0.f) || !(beta1 >= 0.f && beta1 < 1.f) || !(beta2 >= 0.f && beta2 < 1.f) ||
+        !(eps > 0.f) || !(sigma_rank > 0.f))
+        return set_error(TCL_EINVAL, "bad argument");
+    if (m->use_tc || m->kb) return set_error(TCL_ESHAPE, "training: TCL_PREC_FP32 one-column models only");
+    if (n_max > chunk_cap(m)) return set_error(TCL_ESHAPE, "training: n_max exceeds one chunk");
+    CUDA_TRY(cudaSetDevice(m->device));
+    free_train(m);
+    tcl_status st = ensure_workspace(m, n_max);
+    if (st != TCL_OK) return st;
+    const tcl_dims& d = m->dims;
+    const int64_t rows = n_max * d.max_len;
+    const int dm = d.d_model, di = d.expand * d.d_model, N = d.d_state;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1], h1 = d.dec_dims[0], h2 = d.dec_dims[1];
+    TrainState* t = new TrainState();
+    m->tr = t;
+    t->cap_n = n_max;
+    t->rows = rows;
+    t->nW = weights_count_of(d);
+    t->lr = lr; t->b1 = beta1; t->b2 = beta2; t->eps = eps; t->sigma = sigma_rank;
+    auto take = [&](float** p, int64_t cnt) -> tcl_status {
+        tcl_status s2 = dev_alloc(p, (size_t)std::max<int64_t>(cnt, 1));
+        if (s2 == TCL_OK) t->allocs.push_back(*p);
+        return s2;
+    };
+#define TT(p, cnt) if ((st = take(&t->p, (cnt))) != TCL_OK) { free_train(m); return st; }
+    TT(g, t->nW); TT(mA, t->nW); TT(vA, t->nW);
+    TT(E1pre, rows * e1); TT(E1, rows * e1); TT(E2pre, rows * e2); TT(E2, rows * e2);
+    for (int l = 0; l <= d.n_layer; ++l) {
+        float* p = nullptr;
+        if ((st = take(&p, rows * dm)) != TCL_OK) { free_train(m); return st; }
+        t->Hin.push_back(p);
+        if (l == d.n_layer) break;
+        const int64_t sizes[7] = {rows * dm, rows * 2 * di, rows * di, rows * m->ldbc, rows * di, rows * di * N, rows * di};
+        std::vector<float*>* lists[7] = {&t->Aln, &t->XZ, &t->U, &t->DBC, &t->Delta, &t->S, &t->G};
+        for (int k = 0; k < 7; ++k) {
+            if ((st = take(&p, sizes[k])) != TCL_OK) { free_train(m); return st; }
+            lists[k]->push_back(p);
+        }
+    }
+    TT(pooled, n_max * dm); TT(d1pre, n_max * h1); TT(d1, n_max * h1); TT(d2pre, n_max * h2); TT(d2, n_max * h2);
+    TT(scores, n_max);
+    TT(dH, rows * dm); TT(dA, rows * dm); TT(dXZ, rows * 2 * di); TT(dU, rows * di); TT(dpre, rows * di);
+    TT(dDpre, rows * di); TT(dDBC, rows * m->ldbc); TT(dG, rows * di); TT(xhdy, rows * dm);
+    TT(dE1, rows * e1); TT(dE2, rows * e2);
+    TT(ds, n_max); TT(dd1, n_max * h1); TT(dd2, n_max * h2); TT(dpooled, n_max * dm);
+    TT(dAlog_part, n_max * di * N); TT(dD_part, n_max * di); TT(gloss, n_max); TT(loss, 1);
+    t->part_cap = (size_t)8 << 20;
+    TT(part, (int64_t)t->part_cap);
+#undef TT
+    CUDA_TRY(cudaMemset(t->mA, 0, sizeof(float) * t->nW));
+    CUDA_TRY(cudaMemset(t->vA, 0, sizeof(float) * t->nW));
+    CUDA_TRY(cudaMemset(t->dDBC, 0, sizeof(float) * rows * m->ldbc));
+    return TCL_OK;
+}
+
+tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, const float* latency,
+                          const int64_t* group_offsets, int64_t n_groups, int32_t max_group, int32_t apply_update,
+                          float* loss_dev, void* stream) {
+    if (!m || !m->tr) return set_error(TCL_ESTATE, "tcl_train_init was not called");
+    TrainState& t = *m->tr;
+    if (n < 2 || n > t.cap_n || n_groups < 1 || n_groups > n || max_group < 2 || max_group > 4096)
+        return set_error(TCL_EINVAL, "bad argument (2 <= n <= n_max, 1 <= n_groups <= n, 2 <= max_group <= 4096)");
+    if (!feats || !lens || !latency || !group_offsets) return set_error(TCL_EINVAL, "null pointer");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    const tcl_dims& d = m->dims;
+    Workspace& w = m->ws;
+    const int L = d.max_len, dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
+    const int e1 = d.enc_dims[0], e2 = d.enc_dims[1], h1 = d.dec_dims[0], h2 = d.dec_dims[1];
+    const int max_rows = (int)(n * L);
+    const int32_t* P = w.cu + n;
+    DropoutCtx nodrop{};
+    F32Run r{m, max_rows, P, nodrop, s, lens, n};
+    int64_t& nl = m->launches;
+    auto G_ = [&](const float* p) { return t.g + (p - m->w_dev); };   // gradient slot of a weight
+    auto wg = [&](const float* dY, int lddy, const float* X, int ldx, int Nout, int K, float* out, bool cands) {
+        launch_wgrad(dY, lddy, X, ldx, Nout, K, cands ? nullptr : P, cands ? (int)n : max_rows, t.part, t.part_cap,
+                     out, K, s);
+        nl += 2;
+    };
+    auto cs = [&](const float* dY, int lddy, int Ncol, float* out, bool cands) {
+        launch_colsum(dY, lddy, Ncol, cands ? nullptr : P, cands ? (int)n : max_rows, t.part, t.part_cap, out, s);
+        nl += 2;
+    };
+    // ---- forward, saving activations
+    {
+        ProfScope ps(m, TCL_PROF_PACK, s);
+        launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++nl;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++nl;
+    }
+    auto fgemm = [&](const float* X, int ldx, const float* W, const float* b, float* Y, int K, int Nout, int epi,
+                     float* Ypre, bool cands) {
+        GemmArgs g{};
+        g.X = X; g.ldx = ldx; g.W = W; g.ldw = ldx == kXld && W == m->W1p ? kXld : K; g.bias = b; g.Y = Y; g.ldy = Nout;
+        g.K = K; g.N = Nout; g.epi = epi; g.Ypre = Ypre;
+        if (cands) { g.max_rows = (int)n; g.rows_const = (int)n; g.rows_are_cands = 1; }
+        else { g.max_rows = max_rows; g.p_rows = P; g.row_cand = w.row_cand; g.cu = w.cu; }
+        launch_gemm_simt(g, s);
+        ++nl;
+    };
+    fgemm(w.X, kXld, m->W1p, m->wp.enc_b1, t.E1, kXld, e1, EPI_SILU, t.E1pre, false);
+    fgemm(t.E1, e1, m->wp.enc_W2, m->wp.enc_b2, t.E2, e1, e2, EPI_SILU, t.E2pre, false);
+    fgemm(t.E2, e2, m->wp.enc_W3, m->wp.enc_b3, t.Hin[0], e2, dm, EPI_NONE, nullptr, false);
+    for (int l = 0; l < d.n_layer; ++l) {
+        const LayerPtrs& q = m->wp.layers[l];
+        launch_layernorm(t.Hin[l], dm, dm, q.ln_w, q.ln_b, d.ln_eps, t.Aln[l], nullptr, dm, max_rows, P, s); ++nl;
+        fgemm(t.Aln[l], dm, q.W_in, nullptr, t.XZ[l], dm, 2 * di, EPI_NONE, nullptr, false);
+        launch_conv_silu(t.XZ[l], 2 * di, q.w_conv, q.b_conv, di, d.d_conv, t.U[l], w.row_cand, w.cu, max_rows, P, s); ++nl;
+        {
+            GemmArgs g{};
+            g.X = t.U[l]; g.ldx = di; g.W = q.W_x; g.ldw = di; g.Y = t.DBC[l]; g.ldy = m->ldbc; g.K = di; g.N = R + 2 * N;
+            g.epi = EPI_NONE; g.max_rows = max_rows; g.p_rows = P;
+            launch_gemm_simt(g, s); ++nl;
+            GemmArgs h{};
+            h.X = t.DBC[l]; h.ldx = m->ldbc; h.W = q.W_dt; h.ldw = R; h.bias = q.b_dt; h.Y = t.Delta[l]; h.ldy = di;
+            h.K = R; h.N = di; h.epi = EPI_SOFTPLUS; h.max_rows = max_rows; h.p_rows = P;
+            launch_gemm_simt(h, s); ++nl;
+        }
+        ScanArgs sa{};
+        sa.U = t.U[l]; sa.Delta = t.Delta[l]; sa.Z = t.XZ[l] + di; sa.ldz = 2 * di;
+        sa.BC = t.DBC[l]; sa.ldbc = m->ldbc; sa.b_off = R; sa.c_off = R + N;
+        sa.A2 = m->A2 + (size_t)l * di * N; sa.invA = m->invA + (size_t)l * di * N; sa.Dv = q.Dv;
+        sa.G = t.G[l]; sa.cu = w.cu; sa.lens = lens; sa.n = n; sa.di = di; sa.N = N; sa.disc = d.disc;
+        sa.accurate = 1; sa.max_len = L; sa.S_out = t.S[l];
+        launch_scan(sa, s); ++nl;
+        CUDA_TRY(cudaMemcpyAsync(t.Hin[l + 1], t.Hin[l], sizeof(float) * (size_t)max_rows * dm, cudaMemcpyDeviceToDevice, s));
+        GemmArgs g{};
+        g.X = t.G[l]; g.ldx = di; g.W = q.W_out; g.ldw = di; g.Y = t.Hin[l + 1]; g.ldy = dm; g.K = di; g.N = dm;
+        g.epi = EPI_RESID; g.max_rows = max_rows; g.p_rows = P;
+        launch_gemm_simt(g, s); ++nl;
+    }
+    float* Hf = t.Hin[d.n_layer];
+    launch_pool(Hf, dm, dm, m->wp.lnf_w, m->wp.lnf_b, d.ln_eps, w.cu, lens, L, n, t.pooled, s); ++nl;
+    fgemm(t.pooled, dm, m->wp.dec_W1, m->wp.dec_b1, t.d1, dm, h1, EPI_SILU, t.d1pre, true);
+    fgemm(t.d1, h1, m->wp.dec_W2, m->wp.dec_b2, t.d2, h1, h2, EPI_SILU, t.d2pre, true);
+    fgemm(t.d2, h2, m->wp.dec_W3, m->wp.dec_b3, t.scores, h2, 1, EPI_NONE, nullptr, true);
+    // ---- LambdaRank loss and dL/ds (Eq. 6)
+    cudaError_t e = launch_lambdarank(t.scores, latency, group_offsets, n_groups, max_group, t.sigma, t.ds, t.gloss,
+                                      t.loss, s);
+    if (e != cudaSuccess) return cuda_error(e, "lambdarank");
+    nl += 2;
+    if (loss_dev) CUDA_TRY(cudaMemcpyAsync(loss_dev, t.loss, sizeof(float), cudaMemcpyDeviceToDevice, s));
+    // ---- backward: decoder
+    auto bgemm = [&](const float* X, int ldx, const float* W, int ldw, float* Y, int ldy, int K, int Nout, int epi,
+                     bool cands) {   // Y (=|+=) X W   (W stored [K][Nout])
+        GemmArgs g{};
+        g.X = X; g.ldx = ldx; g.W = W; g.ldw = ldw; g.wT = 1; g.Y = Y; g.ldy = ldy; g.K = K; g.N = Nout; g.epi = epi;
+        if (cands) { g.max_rows = (int)n; g.rows_const = (int)n; g.rows_are_cands = 1; }
+        else { g.max_rows = max_rows; g.p_rows = P; }
+        launch_gemm_simt(g, s);
+        ++nl;
+    };
+    wg(t.ds, 1, t.d2, h2, 1, h2, G_(m->wp.dec_W3), true);
+    cs(t.ds, 1, 1, G_(m->wp.dec_b3), true);
+    launch_dec_out_bwd(t.ds, m->wp.dec_W3, t.d2pre, h2, n, t.dd2, s); ++nl;
+    wg(t.dd2, h2, t.d1, h1, h2, h1, G_(m->wp.dec_W2), true);
+    cs(t.dd2, h2, h2, G_(m->wp.dec_b2), true);
+    bgemm(t.dd2, h2, m->wp.dec_W2, h1, t.dd1, h1, h2, h1, EPI_NONE, true);
+    launch_silu_bwd(t.dd1, h1, t.d1pre, h1, t.dd1, h1, h1, nullptr, (int)n, s); ++nl;
+    wg(t.dd1, h1, t.pooled, dm, h1, dm, G_(m->wp.dec_W1), true);
+    cs(t.dd1, h1, h1, G_(m->wp.dec_b1), true);
+    bgemm(t.dd1, h1, m->wp.dec_W1, dm, t.dpooled, dm, h1, dm, EPI_NONE, true);
+    // final norm + masked mean
+    launch_ln_bwd(Hf, dm, m->wp.lnf_w, d.ln_eps, nullptr, t.dpooled, w.row_cand, lens, t.dA, t.dH, 0, t.xhdy, max_rows,
+                  P, s); ++nl;
+    cs(t.xhdy, dm, dm, G_(m->wp.lnf_w), false);
+    cs(t.dA, dm, dm, G_(m->wp.lnf_b), false);
+    // Mamba blocks, last to first
+    for (int l = d.n_layer - 1; l >= 0; --l) {
+        const LayerPtrs& q = m->wp.layers[l];
+        bgemm(t.dH, dm, q.W_out, di, t.dG, di, dm, di, EPI_NONE, false);
+        wg(t.dH, dm, t.G[l], di, dm, di, G_(q.W_out), false);
+        ScanBwdArgs b{};
+        b.U = t.U[l]; b.Delta = t.Delta[l]; b.Z = t.XZ[l] + di; b.ldz = 2 * di;
+        b.BC = t.DBC[l]; b.ldbc = m->ldbc; b.b_off = R; b.c_off = R + N;
+        b.A_log = q.A_log; b.Dv = q.Dv; b.S = t.S[l]; b.dG = t.dG;
+        b.dZ = t.dXZ + di; b.lddz = 2 * di; b.dU = t.dU; b.dDpre = t.dDpre; b.dBC = t.dDBC;
+        b.dAlog_part = t.dAlog_part; b.dD_part = t.dD_part; b.cu = w.cu; b.lens = lens;
+        b.n = n; b.di = di; b.N = N; b.disc = d.disc; b.max_len = L;
+        launch_scan_bwd(b, s); ++nl;
+        cs(t.dAlog_part, di * N, di * N, G_(q.A_log), true);
+        cs(t.dD_part, di, di, G_(q.Dv), true);
+        // dt_proj (softplus folded into dDpre)
+        bgemm(t.dDpre, di, q.W_dt, R, t.dDBC, m->ldbc, di, R, EPI_NONE, false);
+        wg(t.dDpre, di, t.DBC[l], m->ldbc, di, R, G_(q.W_dt), false);
+        cs(t.dDpre, di, di, G_(q.b_dt), false);
+        // x_proj: du += d[dt_r|B|C] W_x
+        bgemm(t.dDBC, m->ldbc, q.W_x, di, t.dU, di, R + 2 * N, di, EPI_RESID, false);
+        wg(t.dDBC, m->ldbc, t.U[l], di, R + 2 * N, di, G_(q.W_x), false);
+        // causal conv + SiLU -> dx (x part of d[x|z])
+        launch_conv_bwd(t.XZ[l], 2 * di, q.w_conv, q.b_conv, di, d.d_conv, t.dU, t.dpre, t.dXZ, 2 * di, w.row_cand,
+                        w.cu, lens, P, max_rows, t.part, t.part_cap, G_(q.w_conv), G_(q.b_conv), s);
+        nl += 4;
+        // in_proj
+        bgemm(t.dXZ, 2 * di, q.W_in, dm, t.dA, dm, 2 * di, dm, EPI_NONE, false);
+        wg(t.dXZ, 2 * di, t.Aln[l], dm, 2 * di, dm, G_(q.W_in), false);
+        // pre-norm, residual: dH += LN'(dA)
+        launch_ln_bwd(t.Hin[l], dm, q.ln_w, d.ln_eps, t.dA, nullptr, w.row_cand, lens, nullptr, t.dH, 1, t.xhdy,
+                      max_rows, P, s); ++nl;
+        cs(t.xhdy, dm, dm, G_(q.ln_w), false);
+        cs(t.dA, dm, dm, G_(q.ln_b), false);
+    }
+    // encoder
+    wg(t.dH, dm, t.E2, e2, dm, e2, G_(m->wp.enc_W3), false);
+    cs(t.dH, dm, dm, G_(m->wp.enc_b3), false);
+    bgemm(t.dH, dm, m->wp.enc_W3, e2, t.dE2, e2, dm, e2, EPI_NONE, false);
+    launch_silu_bwd(t.dE2, e2, t.E2pre, e2, t.dE2, e2, e2, P, max_rows, s); ++nl;
+    wg(t.dE2, e2, t.E1, e1, e2, e1, G_(m->wp.enc_W2), false);
+    cs(t.dE2, e2, e2, G_(m->wp.enc_b2), false);
+    bgemm(t.dE2, e2, m->wp.enc_W2, e1, t.dE1, e1, e2, e1, EPI_NONE, false);
+    launch_silu_bwd(t.dE1, e1, t.E1pre, e1, t.dE1, e1, e1, P, max_rows, s); ++nl;
+    wg(t.dE1, e1, w.X, kXld, e1, d.d_in, G_(m->wp.enc_W1), false);
+    cs(t.dE1, e1, e1, G_(m->wp.enc_b1), false);
+    // ---- Adam, then the derived copies the forward reads (padded W1, A * log2 e, 1 / A)
+    if (apply_update) {
+        t.step += 1;
+        launch_adam(m->w_dev, t.g, t.mA, t.vA, t.nW, t.lr, t.b1, t.b2, t.eps, t.step, s); ++nl;
+        launch_refresh_w1(m->wp.enc_W1, e1, d.d_in, kXld, m->W1p, s); ++nl;
+        for (int l = 0; l < d.n_layer; ++l) {
+            launch_refresh_a(m->wp.layers[l].A_log, di * N, m->A2 + (size_t)l * di * N, m->invA + (size_t)l * di * N, s);
+            ++nl;
+        }
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "train_step");
+    return TCL_OK;
+}
+
+tcl_status tcl_train_read(tcl_model* m, int32_t what, float* host, int64_t count) {
+    if (!m || !host || count < 0) return set_error(TCL_EINVAL, "bad argument");
+    CUDA_TRY(cudaSetDevice(m->device));
+    CUDA_TRY(cudaDeviceSynchronize());
+    const float* src = nullptr;
+    int64_t avail = 0;
+    const int64_t nW = weights_count_of(m->dims);
+    if (what == 0) { src = m->w_dev; avail = nW; }
+    else if (!m->tr) return set_error(TCL_ESTATE, "tcl_train_init was not called");
+    else if (what == 1) { src = m->tr->g; avail = nW; }
+    else if (what == 2) { src = m->tr->ds; avail = m->tr->cap_n; }
+    else if (what == 3) { src = m->tr->scores; avail = m->tr->cap_n; }
+    else return set_error(TCL_EINVAL, "what must be 0 (weights), 1 (gradients), 2 (dL/dscore), 3 (scores)");
+    if (count > avail) return set_error(TCL_ESHAPE, "count exceeds the buffer");
+    CUDA_TRY(cudaMemcpy(host, src, sizeof(float) * count, cudaMemcpyDeviceToHost));
+    return TCL_OK;
+}

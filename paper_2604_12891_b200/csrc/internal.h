@@ -34,6 +34,24 @@ struct AdapterSite {
     int in, out, ldv;
 };
 
+// Training state (tcl_train_init): gradients, Adam moments, saved activations, backward scratch.
+struct TrainState {
+    int64_t cap_n = 0, rows = 0, nW = 0;
+    int step = 0;
+    float lr = 7e-4f, b1 = 0.9f, b2 = 0.999f, eps = 1e-8f, sigma = 1.0f;
+    float *g = nullptr, *mA = nullptr, *vA = nullptr;                 // [nW]
+    float *E1pre = nullptr, *E1 = nullptr, *E2pre = nullptr, *E2 = nullptr;
+    std::vector<float*> Hin, Aln, XZ, U, DBC, Delta, S, G;             // per layer (Hin: n_layer + 1)
+    float *pooled = nullptr, *d1pre = nullptr, *d1 = nullptr, *d2pre = nullptr, *d2 = nullptr, *scores = nullptr;
+    float *dH = nullptr, *dA = nullptr, *dXZ = nullptr, *dU = nullptr, *dpre = nullptr, *dDpre = nullptr,
+          *dDBC = nullptr, *dG = nullptr, *xhdy = nullptr, *dE1 = nullptr, *dE2 = nullptr;
+    float *ds = nullptr, *dd1 = nullptr, *dd2 = nullptr, *dpooled = nullptr, *dAlog_part = nullptr,
+          *dD_part = nullptr, *gloss = nullptr, *loss = nullptr;
+    float* part = nullptr;
+    size_t part_cap = 0;
+    std::vector<void*> allocs;
+};
+
 struct Workspace {
     int64_t cap_n = 0, rows = 0;
     int32_t* cu = nullptr;        // [cap_n + 1]
@@ -110,7 +128,8 @@ struct tcl_model {
     int ad_rank = 0, ad_ld = 0;
     float* ad_dev = nullptr;
     std::vector<tcl::AdapterSite> ad;   // enc1, enc2, enc3, layer 0..n_layer-1, dec1, dec2
-    double* eval_cols = nullptr;   // tcl_topk_score per-task columns
+    double* eval_cols = nullptr;
+    tcl::TrainState* tr = nullptr;  // tcl_train_init   // tcl_topk_score per-task columns
     size_t eval_cols_cap = 0;
     // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)
     int use_tc = 0, num_sms = 148, nxp = 0, rp = 0, bn_in = 0;

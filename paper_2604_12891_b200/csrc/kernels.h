@@ -39,6 +39,9 @@ struct GemmArgs {
     // optional second operand pair accumulated into the same sums (KB+AC lateral term of Eq. 7):
     // Y = epi(X W^T + X2 W2^T + b), X2 [M][ldx2], W2 [N][ldw2], K2 columns; K % 16 == 0 when K2 > 0
     const float* X2; int ldx2; const float* W2; int ldw2; int K2;
+    // training: wT != 0 reads W transposed (element (j, k) at W[k * ldw + j], i.e. Y = X W);
+    // Ypre != nullptr also stores the pre-activation (before the epilogue) at Ypre[m * ldy + j]
+    int wT; float* Ypre;
 };
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 
@@ -65,6 +68,7 @@ struct ScanArgs {
     float* G;            // [P][di]  y * SiLU(z)
     const int32_t* cu; const int32_t* lens;
     int64_t n; int di, N, disc, accurate, max_len;
+    float* S_out;        // training: states after step t at S_out[(row * di + d) * N + n] (or nullptr)
 };
 void launch_scan(const ScanArgs& a, cudaStream_t s);
 
@@ -112,6 +116,45 @@ int launch_topk_merge(const unsigned long long* keys, int64_t count, int k, int6
                       float* score, unsigned long long* tmp, cudaStream_t s);
 
 // ---- RDU acquisition (Alg. 1, Eqs. 1-3) -------------------------------
+// ---- training (train.cu) -------------------------------------------------
+struct ScanBwdArgs {
+    const float* U; const float* Delta; const float* Z; int ldz;
+    const float* BC; int ldbc; int b_off, c_off;
+    const float* A_log; const float* Dv;
+    const float* S;      // saved states [P][di][N]
+    const float* dG;     // [P][di]
+    float* dZ; int lddz; // gate gradient (z part of d[x|z])
+    float* dU;           // [P][di] scan-input gradient
+    float* dDpre;        // [P][di] gradient of the softplus input
+    float* dBC;          // B / C gradients at dBC[row * ldbc + b_off / c_off + n]
+    float* dAlog_part;   // [n][di][N]
+    float* dD_part;      // [n][di]
+    const int32_t* cu; const int32_t* lens;
+    int64_t n; int di, N, disc, max_len;
+};
+void launch_wgrad(const float* dY, int lddy, const float* X, int ldx, int Nout, int K, const int32_t* p_rows,
+                  int max_rows, float* part, size_t part_cap, float* out, int ldo, cudaStream_t s);
+void launch_colsum(const float* dY, int lddy, int Ncol, const int32_t* p_rows, int max_rows, float* part,
+                   size_t part_cap, float* out, cudaStream_t s);
+void launch_silu_bwd(const float* dPost, int ldp, const float* pre, int ldpre, float* dPre, int ldo, int Ncol,
+                     const int32_t* p_rows, int max_rows, cudaStream_t s);
+void launch_dec_out_bwd(const float* ds, const float* W3, const float* pre2, int h2, int64_t n, float* dpre2,
+                        cudaStream_t s);
+void launch_ln_bwd(const float* H, int dm, const float* g, float eps, const float* dY, const float* dpooled,
+                   const int32_t* row_cand, const int32_t* lens, float* dYout, float* dH, int accumulate,
+                   float* xhdy, int max_rows, const int32_t* p_rows, cudaStream_t s);
+void launch_conv_bwd(const float* X, int ldx, const float* w, const float* b, int di, int dc, const float* dU,
+                     float* dpre, float* dX, int lddx, const int32_t* row_cand, const int32_t* cu,
+                     const int32_t* lens, const int32_t* p_rows, int max_rows, float* part, size_t part_cap,
+                     float* dw, float* db, cudaStream_t s);
+void launch_scan_bwd(const ScanBwdArgs& a, cudaStream_t s);
+cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64_t* off, int64_t n_groups,
+                              int max_group, float sigma, float* dscores, float* gloss, float* loss, cudaStream_t s);
+void launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
+                 int step, cudaStream_t s);
+void launch_refresh_w1(const float* W1, int e1, int d_in, int ldp, float* W1p, cudaStream_t s);
+void launch_refresh_a(const float* alog, int diN, float* A2, float* invA, cudaStream_t s);
+
 // Top-k score (Eq. 12): up to 16 k values per call.
 struct TopkEvalKs { int n; int k[16]; };
 cudaError_t launch_topk_eval(const float* scores, const float* lat, const int64_t* off, const float* w,

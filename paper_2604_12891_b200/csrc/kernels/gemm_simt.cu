@@ -43,7 +43,16 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
             As[lk + 0][lr] = v.x; As[lk + 1][lr] = v.y; As[lk + 2][lr] = v.z; As[lk + 3][lr] = v.w;
             const int gn = n0 + lr;
             float4 w = make_float4(0.f, 0.f, 0.f, 0.f);
-            if (gn < a.N && gk < kk_end) w = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
+            if (a.wT && !second) {   // W stored [K][N]: four strided scalars
+                if (gn < a.N) {
+                    if (gk + 0 < kk_end) w.x = __ldg(W + (int64_t)(gk + 0) * ldw + gn);
+                    if (gk + 1 < kk_end) w.y = __ldg(W + (int64_t)(gk + 1) * ldw + gn);
+                    if (gk + 2 < kk_end) w.z = __ldg(W + (int64_t)(gk + 2) * ldw + gn);
+                    if (gk + 3 < kk_end) w.w = __ldg(W + (int64_t)(gk + 3) * ldw + gn);
+                }
+            } else if (gn < a.N && gk < kk_end) {
+                w = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
+            }
             Ws[lk + 0][lr] = w.x; Ws[lk + 1][lr] = w.y; Ws[lk + 2][lr] = w.z; Ws[lk + 3][lr] = w.w;
         }
         __syncthreads();
@@ -75,6 +84,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
             if (gn >= a.N) continue;
             float v = acc[i][j] + (a.bias ? __ldg(a.bias + gn) : 0.0f);
             float* dst = a.Y + (int64_t)gm * a.ldy + gn;
+            if (a.Ypre) a.Ypre[(int64_t)gm * a.ldy + gn] = v;
             switch (a.epi) {
                 case EPI_SILU:
                     v = silu(v);

@@ -99,6 +99,10 @@ __global__ void __launch_bounds__(128) k_scan(ScanArgs a) {
                 y = fmaf(Ct[n], s[n], y);
             }
         }
+        if (a.S_out) {
+#pragma unroll
+            for (int n = 0; n < N; ++n) a.S_out[(row * a.di + d) * N + n] = s[n];
+        }
         y = fmaf(Dv, u, y);
         a.G[row * a.di + d] = y * silu(z);
     }

@@ -47,7 +47,8 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_score_mc", "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
            "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
-           "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac"]
+           "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step",
+           "tcl_train_read"]
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc", "lateral"]
 
@@ -73,6 +74,10 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_weights_count.argtypes = [P(tcl_dims)]
     L.tcl_model_create.argtypes = [vp, sz, P(tcl_dims), ctypes.c_int, P(vp)]
     L.tcl_model_create_kbac.argtypes = [vp, vp, sz, vp, sz, i32, P(tcl_dims), ctypes.c_int, P(vp)]
+    L.tcl_train_init.argtypes = [vp, i64, ctypes.c_float, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                 ctypes.c_float]
+    L.tcl_train_step.argtypes = [vp, vp, vp, i64, vp, vp, i64, i32, i32, vp, vp]
+    L.tcl_train_read.argtypes = [vp, i32, vp, i64]
     L.tcl_adapters_count.restype = sz
     L.tcl_adapters_count.argtypes = [P(tcl_dims), i32]
     L.tcl_model_destroy.argtypes = [vp]
@@ -101,7 +106,7 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
                "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select",
-               "tcl_topk_score", "tcl_model_create_kbac"):
+               "tcl_topk_score", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step", "tcl_train_read"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -225,6 +230,25 @@ class Model:
         _check(load().tcl_topk_score(self._h, _ptr(scores), _ptr(latency), _ptr(task_offsets),
                                      _ptr(task_weights), task_offsets.shape[0] - 1, max_task_len,
                                      kk.ctypes.data, kk.size, _ptr(result), _stream(stream)))
+
+    # -- training (fp32 models) ------------------------------------------------------------------
+    def tcl_train_init(self, n_max: int, lr: float = 7e-4, beta1: float = 0.9, beta2: float = 0.999,
+                       eps: float = 1e-8, sigma_rank: float = 1.0):
+        _check(load().tcl_train_init(self._h, n_max, lr, beta1, beta2, eps, sigma_rank))
+
+    def tcl_train_step(self, feats, lens, latency, group_offsets, max_group: int, apply_update: bool = True,
+                       loss=None, stream=None):
+        """One LambdaRank + Adam step on device tensors; loss (fp32 [1] device tensor) optional."""
+        _check(load().tcl_train_step(self._h, _ptr(feats), _ptr(lens), lens.shape[0], _ptr(latency),
+                                     _ptr(group_offsets), group_offsets.shape[0] - 1, max_group,
+                                     1 if apply_update else 0, _ptr(loss) if loss is not None else None,
+                                     _stream(stream)))
+
+    def tcl_train_read(self, what: str, count: int) -> np.ndarray:
+        code = {"weights": 0, "grads": 1, "dscores": 2, "scores": 3}[what]
+        out = np.empty(count, np.float32)
+        _check(load().tcl_train_read(self._h, code, out.ctypes.data, count))
+        return out
 
     def tcl_rdu_select(self, pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int,
                        selected, n_selected, stream=None):
