@@ -59,3 +59,28 @@ for name, n in (("paper", 16384), ("tuning", 16384)):
         out[f"{name}_{label}"] = {"n": n, "ms": ms, "cand_per_s": n / ms * 1e3}
         print(name, label, f"{ms:.3f} ms", f"{n / ms * 1e3:.0f} cand/s", flush=True)
 json.dump(out, open("gpurun_out/next_rows_time.json", "w"), indent=1)
+
+# Training step (LambdaRank + backward + Adam), paper batch size 1024 in groups of 64
+for name in ("paper", "tuning"):
+    c = inputs.config(name); d = c["dims"]
+    mm = _M(inputs.make_weights(d, 1), d)
+    n = 1024
+    f, l = inputs.make_features(d, n, 5, workload="tuning")
+    rng = np.random.default_rng(0)
+    lat = np.exp(rng.normal(-6, 0.7, n)).astype(np.float32)
+    off = np.arange(0, n + 1, 64, dtype=np.int64)
+    ft, lt, latt, offt = (torch.from_numpy(a).cuda() for a in (f, l, lat, off))
+    mm.tcl_train_init(n)
+    loss = torch.zeros(1, device="cuda")
+    for _ in range(3): mm.tcl_train_step(ft, lt, latt, offt, 64, True, loss)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(10): mm.tcl_train_step(ft, lt, latt, offt, 64, True, loss)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    launches0 = mm.launch_count()
+    mm.tcl_train_step(ft, lt, latt, offt, 64, True, loss); torch.cuda.synchronize()
+    out[f"train_{name}_b1024"] = {"ms_per_step": ms, "cand_per_s": n / ms * 1e3,
+                                  "launches_per_step": mm.launch_count() - launches0, "loss": float(loss.item())}
+    print("train", name, f"{ms:.3f} ms/step", f"{n / ms * 1e3:.0f} cand/s", flush=True)
+json.dump(out, open("gpurun_out/next_rows_time.json", "w"), indent=1)
