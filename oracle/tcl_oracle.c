@@ -617,7 +617,7 @@ int tclo_topk_f32(const float* scores, int64_t n, int32_t k, int64_t index_base,
  *        every f^ = 0.5 when hi == lo; non-finite predictions take no part anywhere (never picked,
  *        not counted in the labeled set), their operator still counts toward the budget shares
  *   d_s(i) = min_j |f^_i - f^_j| over the labeled set (Eq. 1); 1 when the labeled set is empty
- *   mu = (f^_i + S)/(M+1) (Eq. 2); u_s = ((f^_i - mu)^2 + sum_j (f^_j - mu)^2)/(M+1) (Eq. 3) with
+ *   mu = (f^_i + S) r (Eq. 2); u_s = ((f^_i - mu)^2 + sum_j (f^_j - mu)^2) r (Eq. 3), r = 1/(M+1), with
  *        sum_j (f^_j - mu)^2 = Q - 2 mu S + M mu^2 (S = sum f^_j, Q = sum f^_j^2, running sums)
  *   t_s = f^_i d_s + u_s (line 24); pick argmax t_s, ties: higher f^, then lower index
  *   budget[op] = B_t * count(op) / n_pool (lines 16-19); an operator type whose selected count has
@@ -628,7 +628,8 @@ int tclo_topk_f32(const float* scores, int64_t n, int32_t k, int64_t index_base,
  * Returns the number of picks written to out_idx (<= budget_total). */
 static float rdu_uncertainty(float fi, float S, float Q, float Mf) {   /* Eqs. 2-3 */
     float m1 = Mf + 1.0f;
-    float mu = (fi + S) / m1;
+    float r = 1.0f / m1;              /* 1/(M+1), once per pick (R21) */
+    float mu = (fi + S) * r;
     float a = fi - mu;
     float a2 = a * a;
     float t1 = mu * S;
@@ -636,7 +637,7 @@ static float rdu_uncertainty(float fi, float S, float Q, float Mf) {   /* Eqs. 2
     float t3 = mu * mu;
     float t4 = Mf * t3;
     float b = (Q - t2) + t4;
-    return (a2 + b) / m1;
+    return (a2 + b) * r;
 }
 
 static float rdu_total_score(float fi, float ds, float S, float Q, float Mf) {   /* line 24 */
