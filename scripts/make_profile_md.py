@@ -1,0 +1,70 @@
+#!/usr/bin/env python
+"""Assemble profiles/<name>.md from a gpu_official.sh run (gpurun_out/): bench lines, launch list,
+per-kernel ncu summaries, and refresh profiles/<traffic>.json (DRAM bytes per launch).
+
+    python scripts/make_profile_md.py round1_ncu round1_traffic
+"""
+import json
+import os
+import subprocess
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.path.join(ROOT, "gpurun_out")
+
+
+def run(*args):
+    return subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "ncu_summary.py")] + list(args),
+                          capture_output=True, text=True).stdout
+
+
+def main():
+    name = sys.argv[1] if len(sys.argv) > 1 else "round1_ncu"
+    tname = sys.argv[2] if len(sys.argv) > 2 else "round1_traffic"
+    parts = ["# Round 1 — ncu evidence (large config: 65,536 candidates, L=64, d_model 256, 4 layers, bf16 projections)\n",
+             "Source: `scripts/gpu_official.sh` on one B200 via gpurun. Full captures: `ncu --set full --clock-control none "
+             "--import-source on -k regex:<kernel> -s 4 -c 1 python bench.py --steps 1 --warmup 3`; launch list: `ncu "
+             "--metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`. ncu times are "
+             "serialised and cold-cache: compare shares, not absolutes; bench.py's CUDA-event stage times are the live "
+             "numbers. (k_ex2 / k_tanh / k_ffma / k_ffma2 are bench.py's peak microbenchmarks, run outside the timed "
+             "region.)\n", "## Bench line of the same build\n"]
+    for f in ("bench_official.json", "bench_reference.json"):
+        p = os.path.join(OUT, f)
+        if os.path.exists(p):
+            parts.append("```json\n" + open(p).read().strip() + "\n```\n")
+    parts.append("## Launch list (all kernels of 2 timed + 3 warm-up steps + setup)\n")
+    parts.append(run("launches", os.path.join(OUT, "launches_official.csv")))
+    parts.append("## Per-kernel full captures\n")
+    reps = sorted(f for f in os.listdir(OUT) if f.startswith("prof_official_") and f.endswith(".ncu-rep"))
+    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_gemm_simt", "k_topk_chunk", "k_pool_bf16", "k_pack"]
+    reps.sort(key=lambda f: next((i for i, k in enumerate(order) if k in f), 99))
+    for f in reps:
+        parts.append(run("report", os.path.join(OUT, f)))
+    open(os.path.join(ROOT, "profiles", name + ".md"), "w").write("\n".join(parts))
+    # traffic per launch of the dominant kernels
+    traffic = {}
+    for key, rep in (("mixer", "k_mixer_fused"), ("in_proj", "k_gemm_tc"), ("out_proj", "k_gemm_ln")):
+        p = os.path.join(OUT, f"prof_official_{rep}.ncu-rep")
+        if not os.path.exists(p):
+            continue
+        csv = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv", "--metrics",
+                              "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+        lines = [l for l in csv.splitlines() if l.startswith('"')]
+        hdr = [h.strip('"') for h in lines[0].split('","')]
+        units = [h.strip('"') for h in lines[1].split('","')]
+        row = [h.strip('"') for h in lines[2].split('","')]
+        mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+
+        def val(m):
+            i = hdr.index(m)
+            return float(row[i].replace(",", "")) * mult.get(units[i], 1)
+        traffic[key] = {"kernel": row[hdr.index("Kernel Name")][:60], "dram_bytes_read": val("dram__bytes_read.sum"),
+                        "dram_bytes_write": val("dram__bytes_write.sum"),
+                        "source": f"profiles/{name}.md (prof_official_{rep}.ncu-rep)"}
+    if traffic:
+        json.dump(traffic, open(os.path.join(ROOT, "profiles", tname + ".json"), "w"), indent=1)
+    print("wrote", name, list(traffic))
+
+
+if __name__ == "__main__":
+    main()
