@@ -7,9 +7,11 @@
 //   s_t = exp(Delta A) s_{t-1} + (exp(Delta A) - 1)/A * B_t u_t        (Eqs. 4-5 with ZOH; R5)
 //   y_t = C_t . s_t + D u_t ;  g_t = y_t * SiLU(z_t)                   (R6; gate)
 //
-// Work decomposition: a persistent CTA of DI threads walks candidates (grid-stride); thread d owns
-// channel d and keeps its N SSM states in registers for the whole sequence.  Each candidate is
-// processed in chunks of 16 tokens:
+// Work decomposition: a persistent CTA of DI threads owns the packed rows of a contiguous range of
+// candidates (balanced by rows); thread d owns channel d and keeps its N SSM states in registers,
+// resetting them (and the conv window) at every candidate start.  The rows are processed in chunks
+// of 16 consecutive rows that may span candidates, so chunks are full (no per-candidate ragged
+// tail paying the x_proj / dt_proj / barrier cost of a whole chunk):
 //   0. the chunk's 16 rows of the in_proj output [x | z] (bf16, contiguous in the packed layout)
 //      arrive by one TMA bulk copy (cp.async.bulk) into a double buffer; the copy of the NEXT
 //      chunk is issued before this chunk is computed, so HBM latency is hidden;
@@ -156,47 +158,50 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     }
     __syncthreads();
 
-    // ---- chunk iterator over (candidate, t0) for this CTA (grid-stride over candidates)
-    auto first_valid = [&](int64_t i) -> int64_t {
-        for (; i < a.n; i += gridDim.x) {
-            const int T = a.lens[i];
-            if (T >= 1 && T <= a.max_len) return i;
+    // ---- row-chunk iterator: this CTA owns the packed rows of a contiguous candidate range
+    // [c0, c1), balanced by rows (binary search in cu); chunks are 16 consecutive rows that may
+    // span candidates (states and conv window reset at candidate starts), so no chunk is ragged
+    // except the CTA's last one.
+    const int64_t P = a.cu[a.n];
+    auto cand_at = [&](int64_t target) -> int64_t {   // first candidate i with cu[i] >= target
+        int64_t lo = 0, hi = a.n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (a.cu[mid] < target) lo = mid + 1; else hi = mid;
         }
-        return i;
+        return lo;
     };
-    // issue the copy of chunk (i, t0) into buffer b
-    auto issue = [&](int64_t i, int t0, int b) {
-        if (d == 0 && i < a.n) {
-            const int T = a.lens[i];
-            const int tc = min(kTC, T - t0);
-            const uint32_t bytes = (uint32_t)tc * 2 * DI * 2;
+    const int64_t c0 = cand_at(P * blockIdx.x / gridDim.x);
+    const int64_t c1 = cand_at(P * (blockIdx.x + 1) / gridDim.x);
+    const int64_t r_end = a.cu[c1];
+    int64_t r0 = a.cu[c0];
+    int64_t k_next = c0;   // next candidate whose start row is >= r0
+    auto issue = [&](int64_t r, int b) {
+        if (d == 0 && r < r_end) {
+            const uint32_t bytes = (uint32_t)(r_end - r < kTC ? r_end - r : kTC) * 2 * DI * 2;
             tc::mbar_arrive_expect_tx(&bar[b], bytes);
-            bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + (a.cu[i] + t0) * (int64_t)a.ldxz, bytes, &bar[b]);
+            bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + r * (int64_t)a.ldxz, bytes, &bar[b]);
         }
     };
-    int64_t cur_i = first_valid(blockIdx.x);
-    int cur_t0 = 0;
-    issue(cur_i, 0, 0);
+    issue(r0, 0);
     uint32_t parity = 0;  // bit b = phase parity of buffer b
     int buf = 0;
 
     float2 s[N / 2];
     float win[DC];
-    while (cur_i < a.n) {
-        const int T = a.lens[cur_i];
-        const int64_t base = a.cu[cur_i];
-        if (cur_t0 == 0) {
 #pragma unroll
-            for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+    for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
 #pragma unroll
-            for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+    for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+    while (r0 < r_end) {
+        const int tc = (int)(r_end - r0 < kTC ? r_end - r0 : kTC);
+        // rows of this chunk that start a candidate (zero-length candidates share a start row)
+        uint32_t starts = 0;
+        while (k_next < c1 && a.cu[k_next] < r0 + tc) {
+            starts |= 1u << (int)(a.cu[k_next] - r0);
+            ++k_next;
         }
-        const int tc = min(kTC, T - cur_t0);
-        // next chunk in this CTA's sequence -> prefetch into the other buffer
-        int64_t nxt_i = cur_i;
-        int nxt_t0 = cur_t0 + kTC;
-        if (nxt_t0 >= T) { nxt_i = first_valid(cur_i + gridDim.x); nxt_t0 = 0; }
-        issue(nxt_i, nxt_t0, buf ^ 1);
+        issue(r0 + kTC, buf ^ 1);   // prefetch the next chunk into the other buffer
 
         tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
         parity ^= 1u << buf;
@@ -205,7 +210,11 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         // ---- 1. causal conv + SiLU
         // (rows tt >= tc of the chunk are left stale: MMA rows are independent and never read back)
 #pragma unroll 4
-        for (int tt = 0; tt < (a.diag == 2 ? 0 : tc); ++tt) {
+        for (int tt = 0; tt < ((a.diag == 2 || a.diag == 3) ? 0 : tc); ++tt) {
+            if ((starts >> tt) & 1u) {
+#pragma unroll
+                for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+            }
             const float x = __bfloat162float(xz[tt * 2 * DI + d]);
             float acc = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
@@ -294,12 +303,16 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 4. selective scan + D skip + gate (packed fp32x2 arithmetic, MUFU.EX2 for exp)
-        __nv_bfloat16* gout = a.G + (base + cur_t0) * a.ldg + d;
+        __nv_bfloat16* gout = a.G + r0 * a.ldg + d;
         const float* up = u_s + d;
         const float* dlp = dl_s + d;
         const __nv_bfloat16* gzp = xz + DI + d;
         const float* bcp = dbc_s + a.R;
         for (int tt = 0; tt < (a.diag == 1 ? 0 : tc); ++tt) {
+            if ((starts >> tt) & 1u) {
+#pragma unroll
+                for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+            }
             const float u = *up;
             const float dl = *dlp;
             const float gz = silu_fast(__bfloat162float(*gzp));
@@ -353,8 +366,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         buf ^= 1;
-        cur_i = nxt_i;
-        cur_t0 = nxt_t0;
+        r0 += kTC;
     }
 }
 

@@ -20,7 +20,7 @@ struct MixerArgs {
     const int32_t* cu; const int32_t* lens;
     int64_t n;
     int DI, N, R, RP, d_conv, disc, max_len;
-    int diag;  // profiling diagnostics only: 1 = skip the scan phase, 2 = skip conv/x_proj/dt_proj
+    int diag;  // profiling diagnostics only: 1 = skip the scan phase, 2 = skip conv/x_proj/dt_proj, 3 = skip conv
 };
 
 cudaError_t launch_mixer_fused(const MixerArgs& a, int num_sms, cudaStream_t s);
