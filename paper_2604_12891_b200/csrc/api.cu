@@ -786,6 +786,8 @@ tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_w
     return TCL_OK;
 }
 
+static void free_train(tcl_model* m);
+
 tcl_status tcl_model_destroy(tcl_model* m) {
     if (!m) return TCL_OK;
     cudaSetDevice(m->device);
@@ -803,7 +805,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     if (m->rdu_scratch) cudaFree(m->rdu_scratch);
     if (m->eval_cols) cudaFree(m->eval_cols);
     if (m->ad_dev) cudaFree(m->ad_dev);
-    if (m->tr) { for (void* q : m->tr->allocs) cudaFree(q); delete m->tr; m->tr = nullptr; }
+    free_train(m);
     if (m->kb) tcl_model_destroy(m->kb);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
     for (auto ev : m->prof_pool) cudaEventDestroy(ev);
@@ -1103,6 +1105,10 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
 
 static void free_train(tcl_model* m) {
     if (!m->tr) return;
+    if (m->tr->graph) cudaGraphExecDestroy(m->tr->graph);
+    if (m->tr->gstream) cudaStreamDestroy(m->tr->gstream);
+    if (m->tr->ev_in) cudaEventDestroy(m->tr->ev_in);
+    if (m->tr->ev_out) cudaEventDestroy(m->tr->ev_out);
     for (void* p : m->tr->allocs) cudaFree(p);
     delete m->tr;
     m->tr = nullptr;
@@ -1158,23 +1164,29 @@ tcl_status tcl_train_init(tcl_model* m, int64_t n_max, float lr, float beta1, fl
     TT(dAlog_part, n_max * di * N); TT(dD_part, n_max * di); TT(gloss, n_max); TT(loss, 1);
     t->part_cap = (size_t)8 << 20;
     TT(part, (int64_t)t->part_cap);
+    TT(corr_dev, 2);
+    {
+        int* p = nullptr;
+        if ((st = dev_alloc(&p, 1)) != TCL_OK) { free_train(m); return st; }
+        t->allocs.push_back(p);
+        t->step_dev = p;
+    }
 #undef TT
+    CUDA_TRY(cudaMemset(t->step_dev, 0, sizeof(int)));
+    CUDA_TRY(cudaStreamCreateWithFlags(&t->gstream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&t->ev_in, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&t->ev_out, cudaEventDisableTiming));
     CUDA_TRY(cudaMemset(t->mA, 0, sizeof(float) * t->nW));
     CUDA_TRY(cudaMemset(t->vA, 0, sizeof(float) * t->nW));
     CUDA_TRY(cudaMemset(t->dDBC, 0, sizeof(float) * rows * m->ldbc));
     return TCL_OK;
 }
 
-tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, const float* latency,
-                          const int64_t* group_offsets, int64_t n_groups, int32_t max_group, int32_t apply_update,
-                          float* loss_dev, void* stream) {
-    if (!m || !m->tr) return set_error(TCL_ESTATE, "tcl_train_init was not called");
+// Enqueue one training step on stream s (validated arguments).
+static tcl_status train_enqueue(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, const float* latency,
+                                const int64_t* group_offsets, int64_t n_groups, int32_t max_group,
+                                int32_t apply_update, float* loss_dev, cudaStream_t s) {
     TrainState& t = *m->tr;
-    if (n < 2 || n > t.cap_n || n_groups < 1 || n_groups > n || max_group < 2 || max_group > 4096)
-        return set_error(TCL_EINVAL, "bad argument (2 <= n <= n_max, 1 <= n_groups <= n, 2 <= max_group <= 4096)");
-    if (!feats || !lens || !latency || !group_offsets) return set_error(TCL_EINVAL, "null pointer");
-    CUDA_TRY(cudaSetDevice(m->device));
-    cudaStream_t s = (cudaStream_t)stream;
     const tcl_dims& d = m->dims;
     Workspace& w = m->ws;
     const int L = d.max_len, dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
@@ -1325,8 +1337,7 @@ tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens,
     cs(t.dE1, e1, e1, G_(m->wp.enc_b1), false);
     // ---- Adam, then the derived copies the forward reads (padded W1, A * log2 e, 1 / A)
     if (apply_update) {
-        t.step += 1;
-        launch_adam(m->w_dev, t.g, t.mA, t.vA, t.nW, t.lr, t.b1, t.b2, t.eps, t.step, s); ++nl;
+        launch_adam(m->w_dev, t.g, t.mA, t.vA, t.nW, t.lr, t.b1, t.b2, t.eps, t.step_dev, t.corr_dev, s); nl += 2;
         launch_refresh_w1(m->wp.enc_W1, e1, d.d_in, kXld, m->W1p, s); ++nl;
         for (int l = 0; l < d.n_layer; ++l) {
             launch_refresh_a(m->wp.layers[l].A_log, di * N, m->A2 + (size_t)l * di * N, m->invA + (size_t)l * di * N, s);
@@ -1335,6 +1346,51 @@ tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens,
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "train_step");
+    return TCL_OK;
+}
+
+// One training step.  The ~110 launches of a step are captured once into a CUDA graph and
+// replayed while the call signature (pointers, sizes, flags) is unchanged; the graph runs on a
+// private stream ordered after / before the caller's stream by events.  TCL_TRAIN_GRAPH=0 (or
+// per-stage profiling) launches directly.
+tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, const float* latency,
+                          const int64_t* group_offsets, int64_t n_groups, int32_t max_group, int32_t apply_update,
+                          float* loss_dev, void* stream) {
+    if (!m || !m->tr) return set_error(TCL_ESTATE, "tcl_train_init was not called");
+    TrainState& t = *m->tr;
+    if (n < 2 || n > t.cap_n || n_groups < 1 || n_groups > n || max_group < 2 || max_group > 4096)
+        return set_error(TCL_EINVAL, "bad argument (2 <= n <= n_max, 1 <= n_groups <= n, 2 <= max_group <= 4096)");
+    if (!feats || !lens || !latency || !group_offsets) return set_error(TCL_EINVAL, "null pointer");
+    CUDA_TRY(cudaSetDevice(m->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    if (apply_update) t.step += 1;
+    static const bool use_graph = [] { const char* v = getenv("TCL_TRAIN_GRAPH"); return !(v && v[0] == '0'); }();
+    if (!use_graph || m->prof_on)
+        return train_enqueue(m, feats, lens, n, latency, group_offsets, n_groups, max_group, apply_update, loss_dev, s);
+    const TrainState::Key key{feats, lens, latency, group_offsets, loss_dev, n, n_groups, max_group, apply_update ? 1 : 0};
+    if (!t.graph || !(t.key == key)) {
+        if (t.graph) { cudaGraphExecDestroy(t.graph); t.graph = nullptr; }
+        const int64_t before = m->launches;
+        CUDA_TRY(cudaStreamBeginCapture(t.gstream, cudaStreamCaptureModeThreadLocal));
+        tcl_status st = train_enqueue(m, feats, lens, n, latency, group_offsets, n_groups, max_group, apply_update,
+                                      loss_dev, t.gstream);
+        cudaGraph_t g = nullptr;
+        cudaError_t e = cudaStreamEndCapture(t.gstream, &g);
+        t.graph_launches = m->launches - before;   // kernels per replay
+        m->launches = before;                      // counted per replay below
+        if (st != TCL_OK) { if (g) cudaGraphDestroy(g); return st; }
+        if (e != cudaSuccess) return cuda_error(e, "train graph capture");
+        e = cudaGraphInstantiate(&t.graph, g, 0);
+        cudaGraphDestroy(g);
+        if (e != cudaSuccess) { t.graph = nullptr; return cuda_error(e, "train graph instantiate"); }
+        t.key = key;
+    }
+    CUDA_TRY(cudaEventRecord(t.ev_in, s));
+    CUDA_TRY(cudaStreamWaitEvent(t.gstream, t.ev_in, 0));
+    CUDA_TRY(cudaGraphLaunch(t.graph, t.gstream));
+    CUDA_TRY(cudaEventRecord(t.ev_out, t.gstream));
+    CUDA_TRY(cudaStreamWaitEvent(s, t.ev_out, 0));
+    m->launches += t.graph_launches;
     return TCL_OK;
 }
 

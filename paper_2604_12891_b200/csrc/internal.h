@@ -49,6 +49,22 @@ struct TrainState {
           *dD_part = nullptr, *gloss = nullptr, *loss = nullptr;
     float* part = nullptr;
     size_t part_cap = 0;
+    int* step_dev = nullptr;       // Adam step counter (device; graph replays advance it)
+    float* corr_dev = nullptr;     // Adam bias corrections 1 - beta^t
+    // CUDA graph of one step, replayed while the call signature is unchanged
+    struct Key {
+        const void *feats, *lens, *lat, *off, *loss;
+        int64_t n, n_groups;
+        int max_group, apply;
+        bool operator==(const Key& o) const {
+            return feats == o.feats && lens == o.lens && lat == o.lat && off == o.off && loss == o.loss && n == o.n &&
+                   n_groups == o.n_groups && max_group == o.max_group && apply == o.apply;
+        }
+    } key{};
+    cudaGraphExec_t graph = nullptr;
+    int64_t graph_launches = 0;    // kernels per replay
+    cudaStream_t gstream = nullptr;
+    cudaEvent_t ev_in = nullptr, ev_out = nullptr;
     std::vector<void*> allocs;
 };
 

@@ -151,7 +151,7 @@ void launch_scan_bwd(const ScanBwdArgs& a, cudaStream_t s);
 cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64_t* off, int64_t n_groups,
                               int max_group, float sigma, float* dscores, float* gloss, float* loss, cudaStream_t s);
 void launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
-                 int step, cudaStream_t s);
+                 int* step_dev, float* corr_dev, cudaStream_t s);
 void launch_refresh_w1(const float* W1, int e1, int d_in, int ldp, float* W1p, cudaStream_t s);
 void launch_refresh_a(const float* alog, int diN, float* A2, float* invA, cudaStream_t s);
 

@@ -76,8 +76,17 @@ __global__ void k_reduce_parts(const float* __restrict__ part, int splits, int N
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= (int64_t)Nout * K) return;
     const int j = (int)(e / K), k = (int)(e - (int64_t)j * K);
+    // loads are independent of the (in-order) additions: unrolled so the L2 latencies overlap
     float s = 0.0f;
-    for (int p = 0; p < splits; ++p) s += part[(size_t)p * Nout * K + e];
+    int p = 0;
+    for (; p + 8 <= splits; p += 8) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = part[(size_t)(p + q) * Nout * K + e];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; p < splits; ++p) s += part[(size_t)p * Nout * K + e];
     out[(size_t)j * ldo + k] = s;
 }
 
@@ -90,7 +99,15 @@ __global__ void k_colsum(const float* __restrict__ dY, int lddy, int Ncol, const
     const int m_begin = blockIdx.y * rows_per_split;
     const int m_end = min(rows, m_begin + rows_per_split);
     float s = 0.0f;
-    for (int m = m_begin; m < m_end; ++m) s += dY[(int64_t)m * lddy + j];
+    int m = m_begin;
+    for (; m + 8 <= m_end; m += 8) {
+        float v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = dY[(int64_t)(m + q) * lddy + j];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s += v[q];
+    }
+    for (; m < m_end; ++m) s += dY[(int64_t)m * lddy + j];
     part[(size_t)blockIdx.y * Ncol + j] = s;
 }
 
@@ -220,6 +237,7 @@ __global__ void k_conv_wgrad(const float* __restrict__ dpre, const float* __rest
     const int rows = *p_rows;
     const int m_begin = blockIdx.y * rows_per_split, m_end = min(rows, m_begin + rows_per_split);
     float acc[9] = {};
+#pragma unroll 4
     for (int row = m_begin; row < m_end; ++row) {
         const float g = dpre[(int64_t)row * di + d];
         const int t = row - cu[row_cand[row]];
@@ -469,10 +487,18 @@ __global__ void k_loss_mean(const float* __restrict__ gloss, int64_t n_groups, f
 }
 
 // ---------------------------------------------------------------- Adam + derived weights
+// step counter and bias corrections live on the device, so a captured step graph replays correctly
+__global__ void k_adam_count(int* __restrict__ step, float b1, float b2, float* __restrict__ corr) {
+    const int t = ++*step;
+    corr[0] = 1.0f - powf(b1, (float)t);
+    corr[1] = 1.0f - powf(b2, (float)t);
+}
+
 __global__ void k_adam(float* __restrict__ w, const float* __restrict__ g, float* __restrict__ m, float* __restrict__ v,
-                       int64_t n, float lr, float b1, float b2, float eps, float c1, float c2) {
+                       int64_t n, float lr, float b1, float b2, float eps, const float* __restrict__ corr) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= n) return;
+    const float c1 = corr[0], c2 = corr[1];
     const float gg = g[e];
     const float mm = b1 * m[e] + (1.0f - b1) * gg;
     const float vv = b2 * v[e] + (1.0f - b2) * gg * gg;
@@ -591,17 +617,22 @@ cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64
     int P = 1;
     while (P < max_group) P <<= 1;
     const size_t smem = (size_t)P * 8 + (size_t)P * 4 * 4;
-    cudaError_t e = cudaFuncSetAttribute(trn::k_lambdarank, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
+    static bool attr = false;   // set once for the largest group (4096); never inside a graph capture
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(trn::k_lambdarank, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             4096 * (8 + 16));
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
     trn::k_lambdarank<<<(unsigned)n_groups, 1024, smem, s>>>(scores, lat, off, n_groups, sigma, dscores, gloss);
     trn::k_loss_mean<<<1, 1024, 0, s>>>(gloss, n_groups, loss);
     return cudaGetLastError();
 }
 
 void launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
-                 int step, cudaStream_t s) {
-    const float c1 = 1.0f - powf(b1, (float)step), c2 = 1.0f - powf(b2, (float)step);
-    trn::k_adam<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, g, m, v, n, lr, b1, b2, eps, c1, c2);
+                 int* step_dev, float* corr_dev, cudaStream_t s) {
+    trn::k_adam_count<<<1, 1, 0, s>>>(step_dev, b1, b2, corr_dev);
+    trn::k_adam<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, g, m, v, n, lr, b1, b2, eps, corr_dev);
 }
 
 void launch_refresh_w1(const float* W1, int e1, int d_in, int ldp, float* W1p, cudaStream_t s) {

@@ -123,3 +123,41 @@ def test_train_errors(torch_cuda):
     c = inputs.config("large")
     with pytest.raises(TclError):
         Model(inputs.make_weights(c["dims"], 1), c["dims"]).tcl_train_init(16)
+
+
+_STEPS_SCRIPT = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import inputs
+from paper_2604_12891_b200 import Model
+c = inputs.config("tiny"); d = c["dims"]
+w = inputs.make_weights(d, c["seed"])
+f, l = inputs.make_features(d, 32, 7, workload="tuning")
+lat = np.exp(np.random.default_rng(3).normal(-6, 0.7, 32)).astype(np.float32)
+off = np.arange(0, 33, 8, dtype=np.int64)
+m = Model(w, d)
+m.tcl_train_init(32, lr=1e-3)
+ft, lt, latt, offt = (torch.from_numpy(a).cuda() for a in (f, l, lat, off))
+loss = torch.zeros(1, device="cuda")
+for _ in range(3):
+    m.tcl_train_step(ft, lt, latt, offt, 8, True, loss)
+np.save(sys.argv[2], m.tcl_train_read("weights", w.size))
+'''
+
+
+def test_graph_replay_equals_direct_launches(torch_cuda, tmp_path):
+    """The captured step graph (default) and direct launches (TCL_TRAIN_GRAPH=0) give bit-identical
+    weights after 3 Adam steps (the step counter and bias corrections live on the device)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "steps.py"
+    script.write_text(_STEPS_SCRIPT)
+    out = {}
+    for mode in ("1", "0"):
+        env = dict(os.environ, TCL_TRAIN_GRAPH=mode)
+        path = tmp_path / f"w{mode}.npy"
+        subprocess.run([sys.executable, str(script), root, str(path)], check=True, env=env, timeout=300)
+        out[mode] = np.load(path)
+    assert np.array_equal(out["1"], out["0"])
