@@ -209,8 +209,11 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
 
         // ---- 1. causal conv + SiLU
         // (rows tt >= tc of the chunk are left stale: MMA rows are independent and never read back)
-#pragma unroll 4
-        for (int tt = 0; tt < ((a.diag == 2 || a.diag == 3) ? 0 : tc); ++tt) {
+        // fully unrolled over the 16 rows (the window shift is register renaming): 16 independent
+        // conv + SiLU chains in flight instead of 4 (measured 4.40 -> 4.24 ms at `large`)
+#pragma unroll
+        for (int tt = 0; tt < kTC; ++tt) {
+            if (tt >= tc || a.diag == 2 || a.diag == 3) break;
             if ((starts >> tt) & 1u) {
 #pragma unroll
                 for (int k = 0; k < DC; ++k) win[k] = 0.0f;
