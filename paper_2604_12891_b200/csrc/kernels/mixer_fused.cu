@@ -72,9 +72,13 @@ __device__ __forceinline__ float silu_fast(float v) {
     asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * v));
     return v * fmaf(0.5f, t, 0.5f);
 }
-// softplus(v) = max(v, 0) + log(1 + e^{-|v|}): branch-free, two MUFU ops.
+// softplus(v) = max(v, 0) + log(1 + e^{-|v|}): branch-free, two MUFU ops (ex2 / lg2 .approx.ftz:
+// e^{-|v|} in (0, 1] and 1 + e^{-|v|} in (1, 2], so flushing denormals changes nothing, and the
+// non-ftz range fix-ups __expf / __logf carry are not needed).
 __device__ __forceinline__ float softplus_fast(float v) {
-    return fmaxf(v, 0.0f) + __logf(1.0f + __expf(-fabsf(v)));
+    float l;
+    asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l) : "f"(1.0f + ex2(-fabsf(v) * kLog2e)));
+    return fmaf(l, kLn2, fmaxf(v, 0.0f));
 }
 
 // 2^x for a pair (x <= 0) on the FMA/ALU pipes (Cody-Waite + degree-3 near-minimax, rel. err 1e-4)
