@@ -50,12 +50,22 @@ struct MixerSmem {
     static constexpr int kUb = kDbc + kTC * kDbcld * 4;            // bf16  [16][DI + 8] (MMA A operand)
     static constexpr int kWx = kUb + kTC * kWxld * 2;              // bf16  [NXP][DI + 8]
     static constexpr int kBar = OCC == 2 ? kWx + NXP * kWxld * 2 : kUb;  // 2 mbarriers
-    static constexpr int kBytes = kBar + 16;
+    // candidate-start bits of the CTA's rows, 16 per chunk (OCC == 2 only; more chunks than this
+    // fall back to walking cu[] per chunk)
+    static constexpr int kStartWords = OCC == 2 ? 1024 : 0;
+    static constexpr int kStarts = kBar + 16;                      // u32 [kStartWords]
+    static constexpr int kBytes = kStarts + 4 * kStartWords;
 };
 
 __device__ __forceinline__ uint32_t pk_bf16(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(addr));
 }
 
 __device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
@@ -131,9 +141,12 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
     }
     constexpr int NT_DT = DI / 8 / NW;  // dt_proj n-tiles per warp
+    // W_dt fragments / b_dt held in registers for the whole launch (OCC == 2), or re-read from L1
+    // per chunk (OCC == 3)
+    constexpr bool kWdtReg = OCC == 2;
     uint32_t wdt[NT_DT][RP / 16][2];
 #pragma unroll
-    for (int j = 0; j < NT_DT && OCC == 2; ++j) {
+    for (int j = 0; j < NT_DT && kWdtReg; ++j) {
         const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
 #pragma unroll
         for (int ks = 0; ks < RP / 16; ++ks) {
@@ -143,7 +156,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     }
     float2 bdt[NT_DT];  // dt_proj bias of this thread's output columns
 #pragma unroll
-    for (int j = 0; j < NT_DT; ++j) bdt[j] = __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
+    for (int j = 0; j < NT_DT && kWdtReg; ++j) bdt[j] = __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
     float2 A2[N / 2], iA[N / 2];
 #pragma unroll
     for (int n = 0; n < N / 2; ++n) {
@@ -151,10 +164,10 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         iA[n] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + n);
     }
     const float Dv = __ldg(a.Dv + d);
-    const float bconv = __ldg(a.b_conv + d);
+    const float bconv = 0.5f * __ldg(a.b_conv + d);   // pre-halved for the SiLU below
     float wc[DC];
 #pragma unroll
-    for (int k = 0; k < DC; ++k) wc[k] = __ldg(a.w_conv + d * DC + k);
+    for (int k = 0; k < DC; ++k) wc[k] = 0.5f * __ldg(a.w_conv + d * DC + k);
     if (d == 0) {
         tc::mbar_init(&bar[0], 1);
         tc::mbar_init(&bar[1], 1);
@@ -187,9 +200,26 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
             bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + r * (int64_t)a.ldxz, bytes, &bar[b]);
         }
     };
+    // candidate starts of the CTA's rows as a bit array in shared memory, built once: the chunk
+    // loop then reads 16 bits per chunk instead of walking cu[] (dependent global loads on the
+    // critical path of every chunk)
+    uint32_t* st_w = reinterpret_cast<uint32_t*>(msm + L::kStarts);
+    const int64_t n_chunks = (r_end - r0 + kTC - 1) / kTC;
+    const bool bits = L::kStartWords > 0 && (n_chunks + 2) / 2 <= L::kStartWords;
+    if (bits) {
+        const int nw = (int)(n_chunks + 2) / 2;
+        for (int w = d; w < nw; w += DI) st_w[w] = 0u;
+        __syncthreads();
+        for (int64_t i = c0 + d; i < c1; i += DI) {
+            const int64_t off = a.cu[i] - r0;
+            atomicOr(&st_w[off >> 5], 1u << (off & 31));
+        }
+        __syncthreads();
+    }
     issue(r0, 0);
     uint32_t parity = 0;  // bit b = phase parity of buffer b
     int buf = 0;
+    int chunk = 0;
 
     float2 s[N / 2];
     float win[DC];
@@ -201,9 +231,13 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         const int tc = (int)(r_end - r0 < kTC ? r_end - r0 : kTC);
         // rows of this chunk that start a candidate (zero-length candidates share a start row)
         uint32_t starts = 0;
-        while (k_next < c1 && a.cu[k_next] < r0 + tc) {
-            starts |= 1u << (int)(a.cu[k_next] - r0);
-            ++k_next;
+        if (bits) {
+            starts = (st_w[chunk >> 1] >> ((chunk & 1) * 16)) & 0xFFFFu;
+        } else {
+            while (k_next < c1 && a.cu[k_next] < r0 + tc) {
+                starts |= 1u << (int)(a.cu[k_next] - r0);
+                ++k_next;
+            }
         }
         issue(r0 + kTC, buf ^ 1);   // prefetch the next chunk into the other buffer
 
@@ -215,38 +249,61 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         // (rows tt >= tc of the chunk are left stale: MMA rows are independent and never read back)
         // fully unrolled over the 16 rows (the window shift is register renaming): 16 independent
         // conv + SiLU chains in flight instead of 4 (measured 4.40 -> 4.24 ms at `large`)
-#pragma unroll
-        for (int tt = 0; tt < kTC; ++tt) {
-            if (tt >= tc || a.diag == 2 || a.diag == 3) break;
+        // SiLU(v) = h (1 + tanh h) with h = v / 2: the conv weights and bias are pre-halved (exact).
+        auto conv_tok = [&](int tt) {
             if ((starts >> tt) & 1u) {
 #pragma unroll
                 for (int k = 0; k < DC; ++k) win[k] = 0.0f;
             }
             const float x = __bfloat162float(xz[tt * 2 * DI + d]);
-            float acc = fmaf(wc[DC - 1], x, bconv);
+            float h = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
-            for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
+            for (int k = 0; k < DC - 1; ++k) h = fmaf(wc[DC - 2 - k], win[k], h);
 #pragma unroll
             for (int k = DC - 1; k > 0; --k) win[k] = win[k - 1];
             win[0] = x;
-            const float u = silu_fast(acc);
+            float th;
+            asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(h));
+            const float u = fmaf(h, th, h);
             u_s[tt * L::kUld + d] = u;
             if (OCC == 2) u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
+        };
+        if (a.diag != 2 && a.diag != 3) {
+            if (tc == kTC) {
+#pragma unroll
+                for (int tt = 0; tt < kTC; ++tt) conv_tok(tt);
+            } else {
+#pragma unroll
+                for (int tt = 0; tt < kTC; ++tt) {
+                    if (tt >= tc) break;
+                    conv_tok(tt);
+                }
+            }
         }
         __syncthreads();
         // ---- 2. x_proj on the tensor cores: dbc[16][NXP] = u[16][DI] . W_x^T
         for (int nt = warp; nt < (a.diag == 2 ? 0 : NXP / 8); nt += NW) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
             const __nv_bfloat16* wrow = OCC == 2 ? wx_s + (nt * 8 + g) * L::kWxld : a.Wx_b + (int64_t)(nt * 8 + g) * DI;
+            if (OCC == 2) {
+                // fragments by ldmatrix: A (16 x 16 of u) one x4 per k-step, B (8 rows of W_x) one
+                // x4 per two k-steps
+                const uint32_t a_addr = tc::smem_u32(u_b + (lane & 15) * L::kWxld + 8 * (lane >> 4));
+                const uint32_t b_addr = tc::smem_u32(wx_s + (nt * 8 + (lane & 7)) * L::kWxld + 8 * (lane >> 3));
 #pragma unroll 4
-            for (int k0 = 0; k0 < DI; k0 += 16) {
+                for (int k0 = 0; k0 < DI; k0 += 32) {
+                    uint32_t af[4], af2[4], bf[4];
+                    ldsm_x4(af, a_addr + k0 * 2);
+                    ldsm_x4(af2, a_addr + (k0 + 16) * 2);
+                    ldsm_x4(bf, b_addr + k0 * 2);
+                    mma_16816(acc, af, bf[0], bf[1]);
+                    mma_16816(acc, af2, bf[2], bf[3]);
+                }
+            }
+#pragma unroll 4
+            for (int k0 = 0; k0 < (OCC == 2 ? 0 : DI); k0 += 16) {
                 uint32_t af[4];
-                if (OCC == 2) {
-                    af[0] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 2 * tq);
-                    af[1] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 2 * tq);
-                    af[2] = *reinterpret_cast<const uint32_t*>(u_b + g * L::kWxld + k0 + 8 + 2 * tq);
-                    af[3] = *reinterpret_cast<const uint32_t*>(u_b + (g + 8) * L::kWxld + k0 + 8 + 2 * tq);
-                } else {
+                {
                     const float2 p0 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 2 * tq);
                     const float2 p1 = *reinterpret_cast<const float2*>(u_s + (g + 8) * L::kUld + k0 + 2 * tq);
                     const float2 p2 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 8 + 2 * tq);
@@ -256,14 +313,8 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                     af[2] = pk_bf16(p2.x, p2.y);
                     af[3] = pk_bf16(p3.x, p3.y);
                 }
-                uint32_t b0, b1;
-                if (OCC == 2) {
-                    b0 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 2 * tq);
-                    b1 = *reinterpret_cast<const uint32_t*>(wrow + k0 + 8 + 2 * tq);
-                } else {
-                    b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 2 * tq));
-                    b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 8 + 2 * tq));
-                }
+                const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 2 * tq));
+                const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 8 + 2 * tq));
                 mma_16816(acc, af, b0, b1);
             }
             const int c = nt * 8 + 2 * tq;
@@ -292,7 +343,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
                 for (int ks = 0; ks < RP / 16; ++ks) {
-                    if (OCC == 2) {
+                    if (kWdtReg) {
                         mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
                     } else {
                         const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
@@ -301,7 +352,8 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                     }
                 }
                 const int c = (warp + j * NW) * 8 + 2 * tq;
-                const float b0v = bdt[j].x, b1v = bdt[j].y;
+                const float2 bj = kWdtReg ? bdt[j] : __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
+                const float b0v = bj.x, b1v = bj.y;
                 *reinterpret_cast<float2*>(dl_s + g * DI + c) =
                     make_float2(softplus_fast(acc[0] + b0v), softplus_fast(acc[1] + b1v));
                 *reinterpret_cast<float2*>(dl_s + (g + 8) * DI + c) =
@@ -374,6 +426,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         __syncthreads();
         buf ^= 1;
         r0 += kTC;
+        ++chunk;
     }
 }
 

@@ -14,7 +14,7 @@ from typing import Optional, Tuple
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libtcl.so")
+LIB_PATH = os.environ.get("TCL_LIB") or os.path.join(HERE, "libtcl.so")  # TCL_LIB: A/B builds only
 
 STATUS = {0: "TCL_OK", -1: "TCL_EINVAL", -2: "TCL_ESHAPE", -3: "TCL_ELEN", -4: "TCL_ECUDA",
           -5: "TCL_ENOMEM", -6: "TCL_ENCCL", -7: "TCL_ESTATE"}
