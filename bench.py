@@ -115,10 +115,22 @@ def stage_model(d, P: int, n: int):
     dm, di, N, R = d.d_model, d.d_inner, d.d_state, d.dt_rank
     e1, e2 = d.enc_dims[0], d.enc_dims[1]
     act = 2 if d.precision == inputs.PREC_BF16_PROJ else 4
+    bf16 = d.precision == inputs.PREC_BF16_PROJ
+    nl = d.n_layer
+    if bf16:
+        # out_proj + fused LN (gemm_tc_ln): read g (bf16) and H (fp32); write H and LN_{l+1}(H) (bf16);
+        # the last layer writes only LN_f(H) (bf16, the head's input).  Average per layer.
+        out_bytes = (nl * (P * di * 2 + P * dm * 4) + (nl - 1) * (P * dm * 4 + P * dm * 2) + P * dm * 2) / nl
+        head_bytes = P * dm * 2 + n * 4             # pool reads LN_f(H) bf16
+        enc_bytes = P * 32 * 2 + P * dm * 4 + P * dm * 2   # X in; H and LN_0(H) out
+    else:
+        out_bytes = P * di * act + 2 * P * dm * 4
+        head_bytes = P * dm * 4 + n * 4
+        enc_bytes = P * 32 * act + P * dm * 4
     return {
         # pack: read the real rows of the padded fp32 features, write packed rows (32 cols)
         "pack": dict(bytes=P * d.d_in * 4 + P * 32 * act + n * 4),
-        "encoder": dict(flops=2 * P * (32 * e1 + e1 * e2 + e2 * dm), bytes=P * 32 * act + P * dm * 4),
+        "encoder": dict(flops=2 * P * (32 * e1 + e1 * e2 + e2 * dm), bytes=enc_bytes),
         "layernorm": dict(bytes=P * dm * 4 + P * dm * act),
         "in_proj": dict(flops=2 * P * dm * 2 * di, bytes=P * dm * act + P * 2 * di * act),
         "conv": dict(bytes=P * di * act + P * di * 4),
@@ -126,8 +138,8 @@ def stage_model(d, P: int, n: int):
         "dt_proj": dict(flops=2 * P * R * di, bytes=P * R * 4 + P * di * 4),
         # scan: u, delta, z in; g out (fp32) + B, C per token; N exps per (t, d)
         "scan": dict(bytes=P * di * (3 * 4 + act) + P * 2 * N * 4, exps=P * di * N),
-        "out_proj": dict(flops=2 * P * di * dm, bytes=P * di * act + 2 * P * dm * 4),
-        "head": dict(bytes=P * dm * 4 + n * 4),
+        "out_proj": dict(flops=2 * P * di * dm, bytes=out_bytes),
+        "head": dict(bytes=head_bytes),
         "mixer": dict(bytes=P * 2 * di * act + P * di * act, exps=P * di * N),
         "topk": dict(bytes=n * 4),
     }
@@ -302,6 +314,8 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         if "exps" in wk:
             entry["ex2_per_s"] = wk["exps"] * scale / (entry["ms_per_launch"] * 1e-3)
             entry["sfu_frac"] = entry["ex2_per_s"] / mb["ex2"]
+            if mb.get("scanmix"):
+                entry["scanmix_frac"] = entry["ex2_per_s"] / mb["scanmix"]
     dom = max(kernels, key=lambda kk: kernels[kk]["share"])
     de = kernels[dom]
     wk = work[dom]
@@ -320,6 +334,11 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
                 "traffic": traffic, "kernel": dom,
                 "peak_source": mb["source"],
                 "algorithmic_units_per_launch": wk["exps"] * units / calls,
+                # the scan's own instruction mix (2 MUFU.EX2 + 6 packed FMA-pipe ops per state pair,
+                # microbench k_scanmix at the mixer's 16 warps/SM) cannot reach the MUFU-only peak
+                "scan_mix": ({"peak": mb["scanmix"] / 1e12, "frac": de["ex2_per_s"] / mb["scanmix"],
+                              "unit": "Tex2/s", "source": "measured (microbench k_scanmix)"}
+                             if mb.get("scanmix") else None),
                 "hbm": {"achieved_gbs": de.get("gbs"), "peak_gbs": peaks["hbm"], "frac": de.get("hbm_frac"),
                         "algorithmic_bytes_per_launch": wk["bytes"] * units / calls}}
     elif "flops" in wk and d.precision == inputs.PREC_BF16_PROJ and dom in ("in_proj", "out_proj", "encoder"):
@@ -405,7 +424,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
             "kernels": kernels,
             "peaks": {"hbm_gbs": peaks["hbm"], "bf16_tflops": peaks["bf16"], "ex2_per_s": mb["ex2"],
                       "ffma_per_s": mb["ffma"], "ffma2_lanes_per_s": mb.get("ffma2"),
-                      "tanh_per_s": mb.get("tanh"), "source": peaks["source"], "issue_source": mb["source"]},
+                      "tanh_per_s": mb.get("tanh"), "scanmix_ex2_per_s": mb.get("scanmix"), "source": peaks["source"], "issue_source": mb["source"]},
         }
         print(json.dumps(line), flush=True)
     if world > 1:
@@ -434,8 +453,9 @@ def measured_issue_peaks():
         ffma = L.tclmb_run(1, 8192)
         ffma2 = L.tclmb_run(2, 8192)
         tanh = L.tclmb_run(3, 4096)
+        scanmix = L.tclmb_run(4, 2048)
         if ex2 > 0 and ffma > 0:
-            _MB = {"ex2": ex2, "ffma": ffma, "ffma2": ffma2, "tanh": tanh,
+            _MB = {"ex2": ex2, "ffma": ffma, "ffma2": ffma2, "tanh": tanh, "scanmix": scanmix if scanmix > 0 else None,
                    "source": "measured (microbench: 148x8 CTAs x 256 thr, 8 chains)"}
             return _MB
     except OSError:

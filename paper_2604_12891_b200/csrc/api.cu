@@ -1057,8 +1057,19 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
     }
     if (!m->copy_stream) CUDA_TRY(cudaStreamCreateWithFlags(&m->copy_stream, cudaStreamNonBlocking));
     // Pipeline: the copy stream uploads sub-chunk j+1 while the compute stream scores chunk j.
-    const int64_t sub = std::max<int64_t>(1, std::min<int64_t>(chunk_cap(m), 8192));
-    const int64_t nsub = (n + sub - 1) / sub;
+    // Host->device copies run ~3-4x faster than scoring per candidate, so the sub-chunks grow
+    // geometrically (x4): only the first, small copy is exposed, and the scoring runs as few,
+    // large launches (no per-launch ramp/tail of many small grids).
+    const int64_t cap = std::max<int64_t>(1, chunk_cap(m));
+    std::vector<int64_t> sub_off, sub_n;
+    for (int64_t off = 0, sz = std::min<int64_t>(cap, 4096); off < n;) {
+        const int64_t nc = std::min(sz, n - off);
+        sub_off.push_back(off);
+        sub_n.push_back(nc);
+        off += nc;
+        sz = std::min<int64_t>(cap, sz * 4);
+    }
+    const int64_t nsub = (int64_t)sub_off.size();
     while ((int64_t)m->chunk_events.size() < nsub) {
         cudaEvent_t ev;
         CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1069,7 +1080,7 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
     CUDA_TRY(cudaEventRecord(start_ev, s));
     CUDA_TRY(cudaStreamWaitEvent(m->copy_stream, start_ev, 0));
     for (int64_t j = 0; j < nsub; ++j) {
-        const int64_t off = j * sub, nc = std::min(sub, n - off);
+        const int64_t off = sub_off[j], nc = sub_n[j];
         CUDA_TRY(cudaMemcpyAsync(m->stage_feats + off * stride, feats_h + off * stride,
                                  (size_t)nc * stride * sizeof(float), cudaMemcpyHostToDevice, m->copy_stream));
         CUDA_TRY(cudaMemcpyAsync(m->stage_lens + off, lens_h + off, (size_t)nc * sizeof(int32_t),
@@ -1077,7 +1088,7 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
         CUDA_TRY(cudaEventRecord(m->chunk_events[j], m->copy_stream));
     }
     for (int64_t j = 0; j < nsub; ++j) {
-        const int64_t off = j * sub, nc = std::min(sub, n - off);
+        const int64_t off = sub_off[j], nc = sub_n[j];
         CUDA_TRY(cudaStreamWaitEvent(s, m->chunk_events[j], 0));
         tcl_status st = tcl_score(m, m->stage_feats + off * stride, m->stage_lens + off, nc,
                                   m->stage_scores + off, s);

@@ -30,9 +30,13 @@ constexpr int kThreads = 64 + 32 * kEpiWarps;
 template <int BN, int KB, int EPI>
 struct TcSmem {
     static constexpr bool kTmaStore = EPI < 3 && BN >= 128;          // bf16 out through TMA stores
-    static constexpr int kStgBytes = kTmaStore ? kEpiWarps * 2 * 32 * 128 : 0;  // 2 x [32 rows][128 B] per warp
+    // staging per epilogue warp: [32 rows][128 B] x kStgBufs (one TMA store per 64 columns; BN = 128
+    // issues a single store per tile and warp, so one buffer suffices and the smem goes to the A ring;
+    // a 128 KB weight slice also leaves room for only one)
     static constexpr int kBBytes = KB * BN * 128;
-    static constexpr int kStagesRaw = (200 * 1024 - kBBytes - kStgBytes) / kABytes;
+    static constexpr int kStgBufs = (BN <= 128 || kBBytes > 96 * 1024) ? 1 : 2;
+    static constexpr int kStgBytes = kTmaStore ? kEpiWarps * kStgBufs * 32 * 128 : 0;
+    static constexpr int kStagesRaw = (216 * 1024 - kBBytes - kStgBytes) / kABytes;
     static constexpr int kStages = kStagesRaw > 8 ? 8 : (kStagesRaw < 2 ? 2 : kStagesRaw);
     static constexpr int kOffB = 0;
     static constexpr int kOffA = kOffB + kBBytes;
@@ -41,6 +45,7 @@ struct TcSmem {
     static constexpr int kOffRed = kOffPar + 3 * BN * 4;              // LN partials [2][128] float2
     static constexpr int kOffBar = kOffRed + 2 * 128 * 8;
     static constexpr int kBytes = kOffBar + 256 + 1024;               // + barriers, + alignment slack
+    static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per block");
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -224,10 +229,13 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     }
                     if constexpr (S::kTmaStore) {
                         // chunk parity picks the 64-byte half of the 128-byte staged row
-                        const int buf = groups & 1;
-                        uint8_t* stg = smem + S::kOffStg + ((warp - 2) * 2 + buf) * (32 * 128);
-                        if ((k & 1) == 0 && groups >= 2) {  // buffer reuse: its store must have read smem
-                            if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                        const int buf = S::kStgBufs == 2 ? (groups & 1) : 0;
+                        uint8_t* stg = smem + S::kOffStg + ((warp - 2) * S::kStgBufs + buf) * (32 * 128);
+                        if ((k & 1) == 0 && groups >= (uint32_t)S::kStgBufs) {  // buffer reuse: its store must have read smem
+                            if (lane == 0) {
+                                if (S::kStgBufs == 2) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+                                else asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+                            }
                             __syncwarp();
                         }
 #pragma unroll

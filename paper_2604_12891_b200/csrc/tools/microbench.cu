@@ -64,8 +64,45 @@ __global__ void __launch_bounds__(256) k_tanh(float* out, int iters, float seed)
     if (s == 12345.f) out[0] = s;
 }
 
+// The selective scan's per-state instruction mix (mixer_fused.cu, ZOH): per pair of states one
+// FMUL2 for the exponent argument, two MUFU.EX2, FMUL2 x2 for v = B u / A, FADD2 + FFMA2 for the
+// update, FFMA2 for y += C s.  Its throughput is the achievable ceiling of the scan loop on this
+// chip (MUFU and the FMA pipe are both busy; neither reaches its solo peak).  Counts exps.
+__global__ void __launch_bounds__(256) k_scanmix(float* out, int iters, float seed) {
+    float2 s[8], A2[8], iA[8];
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+        s[n] = make_float2(0.f, 0.f);
+        A2[n] = make_float2(-seed * (2 * n + 1) * 1.01f, -seed * (2 * n + 2) * 0.99f);
+        iA[n] = make_float2(1.f / (2 * n + 1.5f), 1.f / (2 * n + 2.5f));
+    }
+    float dl = seed * threadIdx.x * 1e-3f, u = 0.1f * seed;
+    float2 y = make_float2(0.f, 0.f);
+    for (int i = 0; i < iters; ++i) {
+        const float2 dl2 = make_float2(dl, dl), u2 = make_float2(u, u);
+#pragma unroll
+        for (int n = 0; n < 8; ++n) {
+            const float2 x2 = __fmul2_rn(dl2, A2[n]);
+            float e0, e1;
+            asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e0) : "f"(x2.x));
+            asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(e1) : "f"(x2.y));
+            const float2 v = __fmul2_rn(__fmul2_rn(A2[n], u2), iA[n]);
+            const float2 t = __fadd2_rn(s[n], v);
+            s[n] = __ffma2_rn(make_float2(e0, e1), t, make_float2(-v.x, -v.y));
+            y = __ffma2_rn(iA[n], s[n], y);
+        }
+        dl += 1e-7f;
+        u += 1e-7f;
+    }
+    float acc = y.x + y.y;
+#pragma unroll
+    for (int n = 0; n < 8; ++n) acc += s[n].x + s[n].y;
+    if (acc == 12345.f) out[0] = acc;
+}
+
 extern "C" {
-// Returns ops/s over the whole chip (0: MUFU.EX2, 1: FFMA, 2: FFMA2 (2 per lane), 3: MUFU.TANH);
+// Returns ops/s over the whole chip (0: MUFU.EX2, 1: FFMA, 2: FFMA2 (2 per lane), 3: MUFU.TANH,
+// 4: exps of the scan instruction mix (16 per lane per iteration));
 // < 0 on error.
 double tclmb_run(int which, int iters) {
     int dev = 0, sms = 0;
@@ -82,7 +119,8 @@ double tclmb_run(int which, int iters) {
         if (which == 0) k_ex2<<<blocks, threads>>>(out, iters, 0.5f);
         else if (which == 1) k_ffma<<<blocks, threads>>>(out, iters, 0.5f);
         else if (which == 2) k_ffma2<<<blocks, threads>>>(out, iters, 0.5f);
-        else k_tanh<<<blocks, threads>>>(out, iters, 0.5f);
+        else if (which == 3) k_tanh<<<blocks, threads>>>(out, iters, 0.5f);
+        else k_scanmix<<<sms * 2, threads>>>(out, iters, 0.5f);   // 16 warps/SM, as the mixer
         cudaEventRecord(b);
     }
     cudaEventSynchronize(b);
@@ -93,6 +131,7 @@ double tclmb_run(int which, int iters) {
     cudaFree(out);
     if (cudaGetLastError() != cudaSuccess || ms <= 0) return -1;
     // lanes of work per second (FFMA2 counts 2 per lane)
+    if (which == 4) return (double)sms * 2 * threads * iters * 16 / (ms * 1e-3);
     return (double)blocks * threads * iters * 8 * (which == 2 ? 2 : 1) / (ms * 1e-3);
 }
 }
