@@ -91,6 +91,39 @@ def test_full_size_sampled_parity_large(torch_cuda, oracle):
     _check_scores(got[sample], ref, d.precision)
 
 
+def test_full_size_sampled_parity_rdu_mc(torch_cuda, oracle):
+    """BASELINE.json "RDU uncertainty" at full size: 16,384 candidates x 10 MC-dropout passes in one
+    tcl_score_mc call (the masks are keyed by global index, so a sampled candidate i is re-scored by
+    the oracle alone with index_base = i)."""
+    from paper_2604_12891_b200 import Model
+    c = inputs.config("rdu")
+    d, w, f, l = _setup("rdu")
+    assert len(l) == c["n"] == 16384
+    m = Model(w, d)
+    mean, var = _mc_gpu(torch_cuda, m, f, l, c["mc_passes"], 4321, index_base=0)
+    assert np.isfinite(mean).all() and (var >= 0).all()
+    rng = np.random.default_rng(1)
+    for i in rng.choice(len(l), 24, replace=False):
+        rm, rv = oracle.score_mc(d, w, f[i:i + 1], l[i:i + 1], c["mc_passes"], 4321, index_base=int(i))
+        _check_scores(mean[i:i + 1], rm, d.precision)
+        assert abs(var[i] - rv[0]) <= 2 * TOL[d.precision] * np.sqrt(max(rv[0], 1e-8)) + 1e-7
+
+
+def test_sampled_parity_long_131072(torch_cuda, oracle):
+    """BASELINE.json "long-range" at its per-GPU share on 8 GPUs (1,048,576 / 8 = 131,072 candidates,
+    L = 128): sampled candidates and the head of the top-k against the oracle."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("long", n=131072)
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    assert np.isfinite(got).all()
+    rng = np.random.default_rng(2)
+    sample = np.unique(np.concatenate([rng.choice(len(l), 12, replace=False),
+                                       np.argsort(-got, kind="stable")[:4]]))
+    ref = oracle.score(d, w, f[sample], l[sample])
+    _check_scores(got[sample], ref, d.precision)
+
+
 def test_padding_invariance_bitexact(torch_cuda):
     from paper_2604_12891_b200 import Model
     d, w, f, l = _setup("tiny")
