@@ -364,6 +364,18 @@ struct F32Run {
             launch_layernorm(H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s); ++m->launches;
         }
         gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
+        static const bool fused = [] { const char* v = getenv("TCL_F32_MIXER"); return !(v && v[0] == '0'); }();
+        if (fused && mixer_f32_supported(di, N, R, d.d_conv)) {
+            // conv + x_proj + dt_proj + scan in one kernel (mixer_f32.cu)
+            ProfScope ps(m, TCL_PROF_MIXER, s);
+            MixerF32Args a{};
+            a.XZ = w.XZ; a.ldxz = 2 * di; a.G = w.G; a.ldg = di;
+            a.A2 = col->A2 + (size_t)l * di * N; a.invA = col->invA + (size_t)l * di * N; a.Dv = q.Dv;
+            a.w_conv = q.w_conv; a.b_conv = q.b_conv; a.W_x = q.W_x; a.W_dt = q.W_dt; a.b_dt = q.b_dt;
+            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.R = R; a.disc = d.disc;
+            launch_mixer_f32(a, m->num_sms, s);   // errors surface through cudaGetLastError in forward_any
+            ++m->launches;
+        } else {
         {
             ProfScope ps(m, TCL_PROF_CONV, s);
             launch_conv_silu(w.XZ, 2 * di, q.w_conv, q.b_conv, di, d.d_conv, w.U, w.row_cand, w.cu,
@@ -380,6 +392,7 @@ struct F32Run {
         {
             ProfScope ps(m, TCL_PROF_SCAN, s);
             launch_scan(sa, s); ++m->launches;
+        }
         }
         if (site)
             gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ, w.Lat, m->ad_ld,
@@ -606,12 +619,11 @@ static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* l
         if (st != TCL_OK) return st;
         return debug_sync("forward_chunk_tc", s);
     }
-    if (m->kb) {
-        forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s);
-        return debug_sync("forward_chunk_kbac", s);
-    }
-    forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s);
-    return debug_sync("forward_chunk", s);
+    if (m->kb) forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s);
+    else forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s);
+    const cudaError_t e = cudaGetLastError();   // launch-configuration errors of the fp32 kernels
+    if (e != cudaSuccess) return cuda_error(e, m->kb ? "forward_chunk_kbac" : "forward_chunk");
+    return debug_sync(m->kb ? "forward_chunk_kbac" : "forward_chunk", s);
 }
 
 static int64_t chunk_cap(const tcl_model* m) {

@@ -72,6 +72,25 @@ struct ScanArgs {
 };
 void launch_scan(const ScanArgs& a, cudaStream_t s);
 
+// ---- fp32 path: conv + x_proj + dt_proj + scan fused in one persistent kernel (mixer_f32.cu) -----
+struct MixerF32Args {
+    const float* XZ; int ldxz;   // in_proj output [P][2 di] fp32: x = cols [0, di), z = [di, 2 di)
+    float* G; int ldg;           // gated output [P][di]
+    const float* A2;             // [di][N]  A * log2(e)
+    const float* invA;           // [di][N]  1 / A
+    const float* Dv;             // [di]
+    const float* w_conv;         // [di][d_conv]
+    const float* b_conv;         // [di]
+    const float* W_x;            // [R + 2N][di]
+    const float* W_dt;           // [di][R]
+    const float* b_dt;           // [di]
+    const int32_t* cu;           // [n + 1] packed row offsets (device)
+    int64_t n;
+    int DI, N, R, disc;
+};
+bool mixer_f32_supported(int di, int N, int R, int d_conv);
+cudaError_t launch_mixer_f32(const MixerF32Args& a, int num_sms, cudaStream_t s);
+
 // ---- head: LN_f + masked mean pool (warp per candidate) -> pooled [n][dm] -----------------------
 void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const float* lnf_b, float eps,
                  const int32_t* cu, const int32_t* lens, int max_len, int64_t n, float* pooled,

@@ -1,0 +1,314 @@
+// mixer_f32.cu -- the Mamba mixer of the fp32 path in ONE persistent kernel:
+//
+//   u   = SiLU(b_conv + causal depthwise conv_{d_conv}(x))            (R4)
+//   [dt_r | B | C] = u W_x^T                                           (R7)
+//   Delta = softplus(dt_r W_dt^T + b_dt)                               (R13)
+//   s_t = e^{Delta A} s_{t-1} + (e^{Delta A} - 1)/A B_t u_t            (Eqs. 4-5, ZOH; R5)
+//   y_t = C_t . s_t + D u_t ;  g_t = y_t SiLU(z_t)                     (R6)
+//
+// The fp32 configurations (tiny, tuning round, RDU uncertainty, the paper model) are small-width
+// models (d_inner 64-128, N 8-16) whose mixer is far too light for five separate launches with
+// their HBM round trips of u, [dt_r|B|C] and Delta (measured: 0.75 ms per layer and pass at the RDU
+// configuration).  Same work decomposition as the bf16 mixer (mixer_fused.cu): a persistent CTA of
+// DI threads owns the packed rows of a row-balanced contiguous candidate range and walks them in
+// chunks of 16 rows that may span candidates; thread d owns channel d (conv window and N states in
+// registers, reset at candidate starts).  Per chunk:
+//   0. the chunk's [x | z] rows (fp32) arrive by one cp.async.bulk into a double buffer, the next
+//      chunk's copy in flight while this one is computed;
+//   1. conv + SiLU -> u (smem);
+//   2. x_proj in fp32 FFMA: thread (row r, column group) accumulates its columns over K = DI with
+//      128-bit smem loads (the contraction is 16 x (R + 2N) x DI, far below tensor-core size, and
+//      the fp32 path's 1e-4 parity rules out TF32);
+//   3. dt_proj + softplus: thread d forms its own channel's Delta for the 16 rows (W_dt row in
+//      registers);
+//   4. the scan with the fp32 path's accurate ZOH (e^x - 1 by series where Ab - 1 would cancel).
+// Everything matches the unfused fp32 kernels (mixer.cu, gemm_simt.cu) op for op except the
+// summation order of x_proj.  HBM traffic: x, z in and g out only.
+#include <cstdlib>
+
+#include "../kernels.h"
+#include "../tc_ptx.cuh"
+
+namespace tcl {
+namespace f32m {
+
+constexpr int kTC = 16;  // rows per chunk
+
+template <int DI, int NX>
+struct Smem {
+    static constexpr int kNXP = (NX + 3) / 4 * 4;      // x_proj columns padded to a float4
+    static constexpr int kUld = DI + 4;                // +16 B per row: conflict-free float4 rows
+    static constexpr int kDbcld = kNXP + 4;
+    static constexpr int kXZ = 0;                                   // f32 [2][16][2 DI] (bulk dst)
+    static constexpr int kU = kXZ + 2 * kTC * 2 * DI * 4;           // f32 [16][DI + 4]
+    static constexpr int kDl = kU + kTC * kUld * 4;                 // f32 [16][DI]
+    static constexpr int kDbc = kDl + kTC * DI * 4;                 // f32 [16][NXP + 4]
+    static constexpr int kWx = kDbc + kTC * kDbcld * 4;             // f32 [NXP][DI]
+    static constexpr int kBar = kWx + kNXP * DI * 4;                // 2 mbarriers
+    static constexpr int kStartWords = 512;                         // candidate-start bits
+    static constexpr int kStarts = kBar + 16;
+    static constexpr int kBytes = kStarts + 4 * kStartWords;
+};
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            tc::smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
+        : "memory");
+}
+
+// Accurate e^x - 1 (x2 = x log2 e): series where Ab - 1 would cancel (as mixer.cu's fp32 scan).
+__device__ __forceinline__ float expm1_acc(float x2, float Ab) {
+    if (fabsf(x2) < 0.25f) {
+        const float x = x2 * kLn2;
+        return x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720, 1.0f / 120), 1.0f / 24),
+                                          1.0f / 6), 0.5f), 1.0f);
+    }
+    return Ab - 1.0f;
+}
+
+template <int DI, int N, int R, int DC, int DISC>
+__global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
+    constexpr int NX = R + 2 * N;
+    using L = Smem<DI, NX>;
+    constexpr int NXP = L::kNXP;
+    constexpr int CG = DI / kTC;                  // x_proj column groups
+    constexpr int CPG = (NXP + CG - 1) / CG;      // columns per group
+    extern __shared__ __align__(128) uint8_t msm[];
+    float* xz_s = reinterpret_cast<float*>(msm + L::kXZ);
+    float* u_s = reinterpret_cast<float*>(msm + L::kU);
+    float* dl_s = reinterpret_cast<float*>(msm + L::kDl);
+    float* dbc_s = reinterpret_cast<float*>(msm + L::kDbc);
+    float* wx_s = reinterpret_cast<float*>(msm + L::kWx);
+    uint64_t* bar = reinterpret_cast<uint64_t*>(msm + L::kBar);
+    uint32_t* st_w = reinterpret_cast<uint32_t*>(msm + L::kStarts);
+    const int d = threadIdx.x;
+
+    // ---- once per CTA: W_x (zero-padded rows) into smem, per-channel constants into registers
+    for (int idx = d; idx < NXP * DI; idx += DI) {
+        const int r = idx / DI;
+        wx_s[idx] = r < NX ? __ldg(a.W_x + idx) : 0.0f;
+    }
+    float wdt[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) wdt[r] = __ldg(a.W_dt + d * R + r);
+    const float bdt = __ldg(a.b_dt + d);
+    float A2[N], iA[N];
+#pragma unroll
+    for (int n = 0; n < N; ++n) {
+        A2[n] = __ldg(a.A2 + d * N + n);
+        iA[n] = __ldg(a.invA + d * N + n);
+    }
+    const float Dv = __ldg(a.Dv + d);
+    const float bconv = __ldg(a.b_conv + d);
+    float wc[DC];
+#pragma unroll
+    for (int k = 0; k < DC; ++k) wc[k] = __ldg(a.w_conv + d * DC + k);
+    if (d == 0) {
+        tc::mbar_init(&bar[0], 1);
+        tc::mbar_init(&bar[1], 1);
+        tc::fence_mbar_init();
+    }
+
+    // ---- rows of this CTA: a row-balanced contiguous candidate range [c0, c1)
+    const int64_t P = a.cu[a.n];
+    auto cand_at = [&](int64_t target) -> int64_t {
+        int64_t lo = 0, hi = a.n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (a.cu[mid] < target) lo = mid + 1; else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t c0 = cand_at(P * blockIdx.x / gridDim.x);
+    const int64_t c1 = cand_at(P * (blockIdx.x + 1) / gridDim.x);
+    const int64_t r_end = a.cu[c1];
+    int64_t r0 = a.cu[c0];
+    const int64_t n_chunks = (r_end - r0 + kTC - 1) / kTC;
+    const bool bits = (n_chunks + 2) / 2 <= L::kStartWords;
+    if (bits) {
+        for (int w = d; w < (int)(n_chunks + 2) / 2; w += DI) st_w[w] = 0u;
+    }
+    __syncthreads();
+    if (bits) {
+        for (int64_t i = c0 + d; i < c1; i += DI) {
+            const int64_t off = a.cu[i] - r0;
+            atomicOr(&st_w[off >> 5], 1u << (off & 31));
+        }
+    }
+    __syncthreads();
+    int64_t k_next = c0;
+    auto issue = [&](int64_t r, int b) {
+        if (d == 0 && r < r_end) {
+            const uint32_t bytes = (uint32_t)(r_end - r < kTC ? r_end - r : kTC) * 2 * DI * 4;
+            tc::mbar_arrive_expect_tx(&bar[b], bytes);
+            bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + r * (int64_t)a.ldxz, bytes, &bar[b]);
+        }
+    };
+    issue(r0, 0);
+    uint32_t parity = 0;
+    int buf = 0;
+    int chunk = 0;
+
+    float s[N];
+    float win[DC];
+#pragma unroll
+    for (int n = 0; n < N; ++n) s[n] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+    while (r0 < r_end) {
+        const int tc = (int)(r_end - r0 < kTC ? r_end - r0 : kTC);
+        uint32_t starts = 0;
+        if (bits) {
+            starts = (st_w[chunk >> 1] >> ((chunk & 1) * 16)) & 0xFFFFu;
+        } else {
+            while (k_next < c1 && a.cu[k_next] < r0 + tc) {
+                starts |= 1u << (int)(a.cu[k_next] - r0);
+                ++k_next;
+            }
+        }
+        issue(r0 + kTC, buf ^ 1);
+        tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
+        parity ^= 1u << buf;
+        const float* xz = xz_s + buf * kTC * 2 * DI;
+
+        // ---- 1. causal conv + SiLU (rows >= tc: u = 0, so x_proj of the stale rows stays finite)
+#pragma unroll
+        for (int tt = 0; tt < kTC; ++tt) {
+            float u = 0.0f;
+            if (tt < tc) {
+                if ((starts >> tt) & 1u) {
+#pragma unroll
+                    for (int k = 0; k < DC; ++k) win[k] = 0.0f;
+                }
+                const float x = xz[tt * 2 * DI + d];
+                float acc = fmaf(wc[DC - 1], x, bconv);
+#pragma unroll
+                for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
+#pragma unroll
+                for (int k = DC - 1; k > 0; --k) win[k] = win[k - 1];
+                win[0] = x;
+                u = silu(acc);
+            }
+            u_s[tt * L::kUld + d] = u;
+        }
+        __syncthreads();
+        // ---- 2. x_proj: dbc[16][NX] = u[16][DI] . W_x^T (fp32 FFMA, float4 smem loads)
+        {
+            const int r = d % kTC, cg = d / kTC;
+            float acc[CPG];
+#pragma unroll
+            for (int j = 0; j < CPG; ++j) acc[j] = 0.0f;
+            const float4* urow = reinterpret_cast<const float4*>(u_s + r * L::kUld);
+#pragma unroll 4
+            for (int k4 = 0; k4 < DI / 4; ++k4) {
+                const float4 uv = urow[k4];
+#pragma unroll
+                for (int j = 0; j < CPG; ++j) {
+                    const int c = cg * CPG + j;
+                    if (c < NXP) {
+                        const float4 wv = reinterpret_cast<const float4*>(wx_s + c * DI)[k4];
+                        acc[j] = fmaf(uv.x, wv.x, acc[j]);
+                        acc[j] = fmaf(uv.y, wv.y, acc[j]);
+                        acc[j] = fmaf(uv.z, wv.z, acc[j]);
+                        acc[j] = fmaf(uv.w, wv.w, acc[j]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < CPG; ++j) {
+                const int c = cg * CPG + j;
+                if (c < NXP) dbc_s[r * L::kDbcld + c] = acc[j];
+            }
+        }
+        __syncthreads();
+        // ---- 3. dt_proj + softplus: thread d, its channel, the chunk's rows
+#pragma unroll 4
+        for (int tt = 0; tt < kTC; ++tt) {
+            float acc = bdt;
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc = fmaf(dbc_s[tt * L::kDbcld + q], wdt[q], acc);
+            dl_s[tt * DI + d] = softplus(acc);
+        }
+        // ---- 4. selective scan + D skip + gate (each thread reads only its own u / Delta)
+        float* gout = a.G + r0 * a.ldg + d;
+        for (int tt = 0; tt < tc; ++tt) {
+            if ((starts >> tt) & 1u) {
+#pragma unroll
+                for (int n = 0; n < N; ++n) s[n] = 0.0f;
+            }
+            const float u = u_s[tt * L::kUld + d];
+            const float dl = dl_s[tt * DI + d];
+            const float z = xz[tt * 2 * DI + DI + d];
+            const float* Bt = dbc_s + tt * L::kDbcld + R;
+            const float* Ct = Bt + N;
+            float y = 0.0f;
+            if (DISC == 1) {  // Euler-B
+                const float du = dl * u;
+#pragma unroll
+                for (int n = 0; n < N; ++n) {
+                    const float Ab = ex2(dl * A2[n]);
+                    s[n] = fmaf(Ab, s[n], du * Bt[n]);
+                    y = fmaf(Ct[n], s[n], y);
+                }
+            } else {          // ZOH, accurate e^x - 1
+#pragma unroll
+                for (int n = 0; n < N; ++n) {
+                    const float x2 = dl * A2[n];
+                    const float Ab = ex2(x2);
+                    const float v = (Bt[n] * u) * iA[n];
+                    s[n] = fmaf(Ab, s[n], expm1_acc(x2, Ab) * v);
+                    y = fmaf(Ct[n], s[n], y);
+                }
+            }
+            y = fmaf(Dv, u, y);
+            gout[(int64_t)tt * a.ldg] = y * silu(z);
+        }
+        __syncthreads();   // the next chunk overwrites u_s / dl_s / dbc_s and this xz buffer
+        buf ^= 1;
+        r0 += kTC;
+        ++chunk;
+    }
+}
+
+template <int DI, int N, int R, int DISC>
+static cudaError_t launch_k(const MixerF32Args& a, int num_sms, cudaStream_t s) {
+    constexpr int smem = Smem<DI, R + 2 * N>::kBytes;
+    static_assert(smem <= 232448, "mixer_f32 shared memory");
+    auto kern = k_mixer_f32<DI, N, R, 4, DISC>;
+    static int bps = 0;
+    if (!bps) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, DI, smem);
+        if (e != cudaSuccess || bps < 1) bps = 1;
+    }
+    int64_t grid = (int64_t)num_sms * bps;
+    if (grid > a.n) grid = a.n;
+    kern<<<(unsigned)grid, DI, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int DI, int N, int R>
+static cudaError_t launch_disc(const MixerF32Args& a, int num_sms, cudaStream_t s) {
+    return a.disc == 1 ? launch_k<DI, N, R, 1>(a, num_sms, s) : launch_k<DI, N, R, 0>(a, num_sms, s);
+}
+
+}  // namespace f32m
+
+bool mixer_f32_supported(int di, int N, int R, int d_conv) {
+    if (d_conv != 4) return false;
+    return (di == 64 && R == 4 && (N == 8 || N == 16)) || (di == 128 && R == 8 && (N == 8 || N == 16)) ||
+           (di == 256 && R == 16 && (N == 8 || N == 16));
+}
+
+cudaError_t launch_mixer_f32(const MixerF32Args& a, int num_sms, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+    if (a.DI == 64 && a.R == 4) return a.N == 16 ? f32m::launch_disc<64, 16, 4>(a, num_sms, s) : f32m::launch_disc<64, 8, 4>(a, num_sms, s);
+    if (a.DI == 128 && a.R == 8) return a.N == 16 ? f32m::launch_disc<128, 16, 8>(a, num_sms, s) : f32m::launch_disc<128, 8, 8>(a, num_sms, s);
+    if (a.DI == 256 && a.R == 16) return a.N == 16 ? f32m::launch_disc<256, 16, 16>(a, num_sms, s) : f32m::launch_disc<256, 8, 16>(a, num_sms, s);
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace tcl

@@ -66,7 +66,11 @@ void launch_lens_prefix(const int32_t* lens, int64_t n, int32_t max_len, int32_t
     k_lens_prefix<<<1, 1024, 0, s>>>(lens, n, max_len, cu, err);
 }
 
-// One warp per candidate: lane c copies column c of each real row (padded slots never read).
+// One warp per candidate.  The candidate's real rows are one contiguous run of T * d_in floats in
+// the padded input, so the warp streams it as float2 pairs (consecutive lanes, consecutive 8-byte
+// loads; d_in is even, so a pair never straddles two rows) and scatters each pair to its packed
+// row (bf16x2 or float2), then zero-fills the pad columns [d_in, ldx) of its rows.  Padded slots
+// t >= T are never read.
 __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
                                               const int32_t* __restrict__ lens,
                                               const int32_t* __restrict__ cu, int64_t n, int L,
@@ -79,17 +83,37 @@ __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
     const int32_t T = lens[i];
     if (T < 1 || T > L) return;
     const int64_t row0 = cu[i];
-    const float* src = feats + i * (int64_t)L * d_in;
-#pragma unroll 4
-    for (int t = 0; t < T; ++t) {
-        const int64_t row = row0 + t;
-        for (int c = lane; c < ldx; c += 32) {
-            const float v = c < d_in ? __ldg(src + t * d_in + c) : 0.0f;
-            if (X) X[row * ldx + c] = v;
-            if (Xb) Xb[row * ldx + c] = __float2bfloat16_rn(v);
+    if (d_in & 1) {   // odd feature width: column per lane
+        const float* srcs = feats + i * (int64_t)L * d_in;
+        for (int t = 0; t < T; ++t) {
+            const int64_t row = row0 + t;
+            for (int c = lane; c < ldx; c += 32) {
+                const float v = c < d_in ? __ldg(srcs + t * d_in + c) : 0.0f;
+                if (X) X[row * ldx + c] = v;
+                if (Xb) Xb[row * ldx + c] = __float2bfloat16_rn(v);
+            }
+            if (lane == 0) row_cand[row] = (int32_t)i;
         }
-        if (lane == 0) row_cand[row] = (int32_t)i;
+        return;
     }
+    const int hp = d_in >> 1;                       // pairs per row
+    const float2* src = reinterpret_cast<const float2*>(feats + i * (int64_t)L * d_in);
+    const int npairs = T * hp;
+    for (int p = lane; p < npairs; p += 32) {
+        const int t = p / hp, c = 2 * (p - t * hp);
+        const float2 v = __ldg(src + p);
+        const int64_t o = (row0 + t) * ldx + c;
+        if (X) *reinterpret_cast<float2*>(X + o) = v;
+        if (Xb) *reinterpret_cast<__nv_bfloat162*>(Xb + o) = __floats2bfloat162_rn(v.x, v.y);
+    }
+    const int pad = (ldx - d_in) >> 1;             // zero pairs per row
+    for (int p = lane; p < T * pad; p += 32) {
+        const int t = p / pad, c = d_in + 2 * (p - t * pad);
+        const int64_t o = (row0 + t) * ldx + c;
+        if (X) *reinterpret_cast<float2*>(X + o) = make_float2(0.f, 0.f);
+        if (Xb) *reinterpret_cast<__nv_bfloat162*>(Xb + o) = __floats2bfloat162_rn(0.f, 0.f);
+    }
+    for (int t = lane; t < T; t += 32) row_cand[row0 + t] = (int32_t)i;
 }
 
 void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int64_t n, int L,
