@@ -100,8 +100,115 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
     }
 }
 
+// Wide variant for N >= 128 (in_proj, out_proj, the encoder's 2nd/3rd linears of the fp32 path):
+// tile 128x128x8, 256 threads, 8x8 outputs per thread (rows ty*4 + {0..3, 64..67}, columns
+// tx*4 + {0..3, 64..67}: four 128-bit smem loads feed 64 FFMA per k step), smem double-buffered
+// with register prefetch of the next k-block (one barrier per k-block).  The k order of every
+// output is the same sequential 0..K-1 FFMA chain as k_gemm_simt, so results are bit-identical.
+constexpr int BM2 = 128, BN2 = 128, BK2 = 8;
+
+__device__ __forceinline__ void epi_store(const GemmArgs& a, int gm, int gn, float acc, int cand, int token) {
+    float v = acc + (a.bias ? __ldg(a.bias + gn) : 0.0f);
+    float* dst = a.Y + (int64_t)gm * a.ldy + gn;
+    if (a.Ypre) a.Ypre[(int64_t)gm * a.ldy + gn] = v;
+    switch (a.epi) {
+        case EPI_SILU:
+            v = silu(v);
+            if (a.drop.enabled) v = dropout_keep(a.drop, gn, token, a.site, cand) ? v * a.drop.scale : 0.0f;
+            break;
+        case EPI_SOFTPLUS: v = softplus(v); break;
+        case EPI_RESID: v = *dst + v; break;
+        default: break;
+    }
+    *dst = v;
+}
+
+__global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
+    __shared__ __align__(16) float As[2][BK2][BM2 + 4];
+    __shared__ __align__(16) float Ws[2][BK2][BN2 + 4];
+    const int rows = a.p_rows ? *a.p_rows : a.rows_const;
+    const int m0 = blockIdx.x * BM2;
+    if (m0 >= rows) return;
+    const int n0 = blockIdx.y * BN2;
+    const int tid = threadIdx.x;
+    const int tx = tid & 15, ty = tid >> 4;
+    // loader: 128 rows x 8 k = 1024 floats = 256 threads x float4 (row tid/2, k offset 4*(tid&1))
+    const int lr = tid >> 1, lk = (tid & 1) * 4;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
+
+    const int k_end = a.K + a.K2;
+    auto load = [&](int k0, float4& xv, float4& wv) {
+        const bool second = k0 >= a.K;
+        const float* X = second ? a.X2 : a.X;
+        const float* W = second ? a.W2 : a.W;
+        const int ldx = second ? a.ldx2 : a.ldx, ldw = second ? a.ldw2 : a.ldw;
+        const int kk_end = second ? a.K2 : a.K;
+        const int gm = m0 + lr, gk = (second ? k0 - a.K : k0) + lk, gn = n0 + lr;
+        xv = make_float4(0.f, 0.f, 0.f, 0.f);
+        wv = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (gm < rows && gk < kk_end) xv = *reinterpret_cast<const float4*>(X + (int64_t)gm * ldx + gk);
+        if (gn < a.N && gk < kk_end) wv = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
+    };
+    auto stash = [&](int b, const float4& xv, const float4& wv) {
+        As[b][lk + 0][lr] = xv.x; As[b][lk + 1][lr] = xv.y; As[b][lk + 2][lr] = xv.z; As[b][lk + 3][lr] = xv.w;
+        Ws[b][lk + 0][lr] = wv.x; Ws[b][lk + 1][lr] = wv.y; Ws[b][lk + 2][lr] = wv.z; Ws[b][lk + 3][lr] = wv.w;
+    };
+    float4 xv, wv;
+    load(0, xv, wv);
+    stash(0, xv, wv);
+    __syncthreads();
+    int b = 0;
+    for (int k0 = 0; k0 < k_end; k0 += BK2) {
+        const bool more = k0 + BK2 < k_end;
+        if (more) load(k0 + BK2, xv, wv);    // global loads in flight during this k-block's math
+#pragma unroll
+        for (int kk = 0; kk < BK2; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4 + 64]);
+            const float4 w0 = *reinterpret_cast<const float4*>(&Ws[b][kk][tx * 4]);
+            const float4 w1 = *reinterpret_cast<const float4*>(&Ws[b][kk][tx * 4 + 64]);
+            const float ar[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            const float wr[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(ar[i], wr[j], acc[i][j]);
+        }
+        if (more) {
+            stash(b ^ 1, xv, wv);   // the other buffer: last read before the previous barrier
+            __syncthreads();
+            b ^= 1;
+        }
+    }
+
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const int gm = m0 + ty * 4 + (i & 3) + (i >> 2) * 64;
+        if (gm >= rows) continue;
+        int cand = 0, token = 0;
+        if (a.epi == EPI_SILU && a.drop.enabled) {
+            cand = a.rows_are_cands ? gm : a.row_cand[gm];
+            token = a.rows_are_cands ? 0 : gm - a.cu[cand];
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const int gn = n0 + tx * 4 + (j & 3) + (j >> 2) * 64;
+            if (gn < a.N) epi_store(a, gm, gn, acc[i][j], cand, token);
+        }
+    }
+}
+
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
     if (a.max_rows <= 0) return;
+    if (a.N >= 128 && !a.wT && (a.K % BK2) == 0 && (a.K2 % BK2) == 0) {
+        dim3 grid2((a.max_rows + BM2 - 1) / BM2, (a.N + BN2 - 1) / BN2);
+        k_gemm_simt128<<<grid2, 256, 0, s>>>(a);
+        return;
+    }
     dim3 grid((a.max_rows + BM - 1) / BM, (a.N + BN - 1) / BN);
     k_gemm_simt<<<grid, 256, 0, s>>>(a);
 }

@@ -1,5 +1,6 @@
-# One full bench line (N=1, default config) + the ncu evidence kept under profiles/.
+# GPU tests, one full bench line (N=1, default config) + the ncu evidence kept under profiles/.
 cd $GRAFT_REPO_ROOT
+timeout 1200 python -m pytest tests -m gpu -x -q 2>&1 | tail -3
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
 python bench.py > gpurun_out/bench_official.json 2> gpurun_out/bench_official.err; tail -2 gpurun_out/bench_official.err
 cat gpurun_out/bench_official.json
