@@ -195,9 +195,39 @@ __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
             token = a.rows_are_cands ? 0 : gm - a.cu[cand];
         }
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            const int gn = n0 + tx * 4 + (j & 3) + (j >> 2) * 64;
-            if (gn < a.N) epi_store(a, gm, gn, acc[i][j], cand, token);
+        for (int jh = 0; jh < 2; ++jh) {
+            const int gn0 = n0 + tx * 4 + jh * 64;
+            if (gn0 + 3 < a.N && !a.Ypre && (a.ldy & 3) == 0 && (reinterpret_cast<uintptr_t>(a.Y) & 15) == 0) {
+                // 4 consecutive columns: one 128-bit load / store
+                float v[4];
+                const float4 bv = a.bias ? make_float4(__ldg(a.bias + gn0), __ldg(a.bias + gn0 + 1), __ldg(a.bias + gn0 + 2),
+                                                       __ldg(a.bias + gn0 + 3))
+                                         : make_float4(0.f, 0.f, 0.f, 0.f);
+                v[0] = acc[i][jh * 4 + 0] + bv.x; v[1] = acc[i][jh * 4 + 1] + bv.y;
+                v[2] = acc[i][jh * 4 + 2] + bv.z; v[3] = acc[i][jh * 4 + 3] + bv.w;
+                float4* dst = reinterpret_cast<float4*>(a.Y + (int64_t)gm * a.ldy + gn0);
+                if (a.epi == EPI_RESID) {
+                    const float4 o = *dst;
+                    v[0] = o.x + v[0]; v[1] = o.y + v[1]; v[2] = o.z + v[2]; v[3] = o.w + v[3];
+                } else if (a.epi == EPI_SILU) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        v[q] = silu(v[q]);
+                        if (a.drop.enabled)
+                            v[q] = dropout_keep(a.drop, gn0 + q, token, a.site, cand) ? v[q] * a.drop.scale : 0.0f;
+                    }
+                } else if (a.epi == EPI_SOFTPLUS) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) v[q] = softplus(v[q]);
+                }
+                *dst = make_float4(v[0], v[1], v[2], v[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int gn = gn0 + q;
+                    if (gn < a.N) epi_store(a, gm, gn, acc[i][jh * 4 + q], cand, token);
+                }
+            }
         }
     }
 }

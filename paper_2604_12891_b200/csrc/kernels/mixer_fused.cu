@@ -113,7 +113,7 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0>
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0, int SU = 1>
 __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     // OCC == 3: lean variant (W_x fragments from L1, no bf16 copy of u, W_dt per chunk) so that
     // three CTAs fit per SM (<= 85 registers, <= 75 KB shared memory).
@@ -362,19 +362,21 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 4. selective scan + D skip + gate (packed fp32x2 arithmetic, MUFU.EX2 for exp)
-        __nv_bfloat16* gout = a.G + r0 * a.ldg + d;
+        __nv_bfloat16* gout = a.G + r0 * DI + d;   // ldg == DI (checked at launch)
         const float* up = u_s + d;
         const float* dlp = dl_s + d;
         const __nv_bfloat16* gzp = xz + DI + d;
         const float* bcp = dbc_s + a.R;
-        for (int tt = 0; tt < (a.diag == 1 ? 0 : tc); ++tt) {
+        // one token of the scan; the row pointers advance by compile-time strides (G rows are DI
+        // wide on this path), so in the unrolled full-chunk loop every access is base + immediate
+        auto scan_tok = [&](int tt) {
             if ((starts >> tt) & 1u) {
 #pragma unroll
                 for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
             }
-            const float u = *up;
-            const float dl = *dlp;
-            const float gz = silu_fast(__bfloat162float(*gzp));
+            const float u = up[0];
+            const float dl = dlp[0];
+            const float gz = silu_fast(__bfloat162float(gzp[0]));
             const float4* B4 = reinterpret_cast<const float4*>(bcp);
             const float4* C4 = reinterpret_cast<const float4*>(bcp + N);
             const float2 dl2 = make_float2(dl, dl);
@@ -416,12 +418,24 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                 }
             }
             const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
-            *gout = __float2bfloat16_rn(y * gz);
+            gout[0] = __float2bfloat16_rn(y * gz);
             up += L::kUld;
             dlp += DI;
             gzp += 2 * DI;
             bcp += L::kDbcld;
-            gout += a.ldg;
+            gout += DI;
+        };
+        if (a.diag != 1) {
+            if (tc == kTC && SU > 1) {
+#pragma unroll 1
+                for (int t0 = 0; t0 < kTC; t0 += SU) {
+#pragma unroll
+                    for (int j = 0; j < SU; ++j) scan_tok(t0 + j);
+                }
+            } else {
+#pragma unroll 1
+                for (int tt = 0; tt < tc; ++tt) scan_tok(tt);
+            }
         }
         __syncthreads();
         buf ^= 1;
@@ -430,10 +444,11 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     }
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0>
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0, int SU = 1>
 static cudaError_t mixer_launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
     constexpr int smem = MixerSmem<DI, NXP, OCC>::kBytes;
-    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC, OCC, OFF>;
+    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC, OCC, OFF, SU>;
+    if (a.ldg != DI) return cudaErrorInvalidValue;
     static int blocks_per_sm = 0;
     if (!blocks_per_sm) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -457,6 +472,10 @@ static cudaError_t mixer_launch(const MixerArgs& a, int num_sms, cudaStream_t s)
                            : mixer_launch_k<DI, N, RP, NXP, 4, 0, 3>(a, num_sms, s);
     if (a.disc == 0 && N == 16 && off == 1) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 1>(a, num_sms, s);
     if (a.disc == 0 && N == 16 && off == 2) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 2>(a, num_sms, s);
+    // scan tokens per unrolled step of a full chunk (measured at `large`: 1 -> 4.14 ms, 2 -> 4.03,
+    // 4 -> 4.08-4.12, 16 -> 4.24 with spills); TCL_MIXER_SU=1 restores the rolled loop
+    static const int su = [] { const char* v = getenv("TCL_MIXER_SU"); return v ? atoi(v) : 2; }();
+    if (a.disc == 0 && su == 2) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 0, 2>(a, num_sms, s);
     return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1, 2>(a, num_sms, s)
                        : mixer_launch_k<DI, N, RP, NXP, 4, 0, 2>(a, num_sms, s);
 }
