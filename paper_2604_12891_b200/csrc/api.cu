@@ -535,6 +535,17 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
     auto kb_of = [](int K) { return (K + 63) / 64; };
     {
         ProfScope ps(m, TCL_PROF_ENCODER, s);
+        static const bool fused12 = [] { const char* v = getenv("TCL_ENC12"); return !(v && v[0] == '0'); }();
+        if (fused12 && enc12_supported(e1, e2, d.d_in)) {
+            // linears 1 and 2 chained: E1 stays in shared memory (gemm_tc_enc.cu)
+            EncParams ep{};
+            ep.p_rows = P; ep.b1 = m->wp.enc_b1; ep.b2 = m->wp.enc_b2; ep.drop = drop;
+            ep.row_cand = w.row_cand; ep.cu = w.cu;
+            if ((e = launch_enc12(w.tmXb, m->tmW1, m->tmW2, w.tmE2o, ep, e1, e2, m->num_sms, s)) != cudaSuccess)
+                return cuda_error(e, "enc12");
+            ++nl;
+            if (debug_sync("enc12", s) != TCL_OK) return TCL_ECUDA;
+        } else {
         TcGemmParams p = base();
         p.epi = TC_EPI_BF16; p.bias = m->wp.enc_b1; p.act_silu = 1; p.out = E1b; p.ldo = e1;
         p.drop.enabled = drop.enabled; p.site = 0;
@@ -545,6 +556,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         if ((e = launch_gemm_tc(w.tmE1b, m->tmW2, w.tmE2o, p, e2, kb_of(e1), m->num_sms, s)) != cudaSuccess) return cuda_error(e, "enc2");
         ++nl;
         if (debug_sync("enc2", s) != TCL_OK) return TCL_ECUDA;
+        }
         TcGemmParams q = base();
         q.epi = TC_EPI_RESID_LN; q.bias = m->wp.enc_b3; q.residual = 0; q.H = w.H; q.ldh = dm;
         q.out = (d.n_layer > 0 || dm >= 128) ? w.Ab : nullptr; q.ldo = dm;

@@ -29,6 +29,19 @@ struct TcGemmParams {
     DropoutCtx drop; int site; const int32_t* row_cand; const int32_t* cu;
 };
 
+// Encoder linears 1 + 2 chained in one kernel (gemm_tc_enc.cu): E2 = SiLU(SiLU(X W1^T + b1) W2^T + b2)
+struct EncParams {
+    const int32_t* p_rows;       // device: number of packed rows
+    const float* b1; const float* b2;
+    DropoutCtx drop;             // sites 0 (E1) and 1 (E2) when enabled
+    const int32_t* row_cand; const int32_t* cu;
+};
+bool enc12_supported(int e1, int e2, int d_in);
+// X: [rows][32] bf16 (box {64, 128}); W1: [e1][32] (box {64, e1}); W2: [e2][e1] (box {64, e2});
+// E2: bf16 output map (box {64, 32}).
+cudaError_t launch_enc12(const CUtensorMap& x, const CUtensorMap& w1, const CUtensorMap& w2, const CUtensorMap& e2,
+                         const EncParams& p, int e1n, int e2n, int num_sms, cudaStream_t s);
+
 // 2-D bf16 tensor map, 128B swizzle, box {box_inner (<= 64), box_outer (<= 256)}.
 bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                     uint32_t box_inner, uint32_t box_outer);
