@@ -23,6 +23,14 @@ __device__ __forceinline__ float rcp(float x) {
 }
 // SiLU(v) = v * sigmoid(v) (reading R1).  One MUFU.EX2 + one MUFU.RCP.
 __device__ __forceinline__ float silu(float v) { return v * rcp(1.0f + ex2(-v * kLog2e)); }
+// bf16-path SiLU: h (1 + tanh h), h = v / 2 -- one MUFU.TANH (tanh.approx, relative error ~2^-11,
+// below the bf16 rounding of the output it feeds).
+__device__ __forceinline__ float silu_tanh(float v) {
+    const float h = 0.5f * v;
+    float t;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(h));
+    return fmaf(h, t, h);
+}
 // softplus(v) = log(1 + e^v) (reading R13): v > 20 -> v (error < 2.1e-9); log1pf for accuracy.
 __device__ __forceinline__ float softplus(float v) {
     return v > 20.0f ? v : log1pf(__expf(v));

@@ -217,8 +217,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     for (int j = 0; j < 32; j += 2) {
                         float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
                         if (EPI >= 1) {
-                            v0 = silu(v0 + s_bias[c * 32 + j]);
-                            v1 = silu(v1 + s_bias[c * 32 + j + 1]);
+                            v0 = silu_tanh(v0 + s_bias[c * 32 + j]);
+                            v1 = silu_tanh(v1 + s_bias[c * 32 + j + 1]);
                         }
                         if (EPI == 2) {
                             const int n = n_tile * BN + c * 32 + j;

@@ -9,10 +9,12 @@
 // shared memory in the 128B-swizzled K-major layout the second MMA reads, so the HBM traffic per
 // row is the 64-byte feature row in and the e2-wide bf16 row out (the unfused pair also wrote and
 // re-read E1).  Persistent CTA per SM, warp-specialised like gemm_tc.cu: warp 0 = TMA producer
-// (W1, W2 once; X row tiles through a 3-stage ring), warp 1 = TMEM allocator + single-thread MMA
+// (W1, W2 once; X row tiles through a 2-stage ring), warp 1 = TMEM allocator + single-thread MMA
 // issuer, warps 2..9 = epilogue (warp w drains TMEM lanes 32 (w % 4) .., column half (w - 2) / 4).
-// TMEM: acc1 double-buffered (2 x e1 columns), acc2 (e2 columns); MMA1 of tile j+1 is issued
-// before MMA2 of tile j, so it overlaps the E1 epilogue.
+// TMEM: acc1 double-buffered (2 x e1 columns), acc2 (e2 columns); E1 double-buffered in shared
+// memory.  MMA1 of tile j+1 is issued before MMA2 of tile j, and the epilogue warps form E1 of tile
+// j+1 while MMA2 of tile j runs, then drain E2 of tile j.  SiLU in both epilogues is the one-MUFU
+// tanh form (h (1 + tanh h), h = v/2): the two SiLUs per E1/E2 element are the epilogue's cost.
 #include <cuda_bf16.h>
 
 #include "../kernels_tc.h"
@@ -24,7 +26,7 @@ namespace enc {
 constexpr int kBM = 128;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * kEpiWarps;
-constexpr int kXStages = 3;
+constexpr int kXStages = 2;
 
 template <int E1N, int E2N>
 struct Smem {
@@ -32,8 +34,9 @@ struct Smem {
     static constexpr int kOffW1 = 0;                            // [E1N rows][128 B]
     static constexpr int kOffW2 = kOffW1 + E1N * 128;           // kKB1 x [E2N rows][128 B]
     static constexpr int kOffX = kOffW2 + kKB1 * E2N * 128;     // kXStages x [128 rows][128 B]
-    static constexpr int kOffE1 = kOffX + kXStages * kBM * 128; // kKB1 x [128 rows][128 B]
-    static constexpr int kOffStg = kOffE1 + kKB1 * kBM * 128;   // kEpiWarps x [32 rows][128 B]
+    static constexpr int kOffE1 = kOffX + kXStages * kBM * 128; // [2] x kKB1 x [128 rows][128 B]
+    static constexpr int kE1Bytes = kKB1 * kBM * 128;
+    static constexpr int kOffStg = kOffE1 + 2 * kE1Bytes;       // kEpiWarps x [32 rows][128 B]
     static constexpr int kOffPar = kOffStg + kEpiWarps * 32 * 128;
     static constexpr int kOffBar = kOffPar + (E1N + E2N) * 4;
     static constexpr int kBytes = kOffBar + 256 + 1024;
@@ -71,8 +74,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
     uint64_t* xempty = xfull + kXStages;    // [kXStages]
     uint64_t* a1full = xempty + kXStages;   // [2]
     uint64_t* a1empty = a1full + 2;         // [2]
-    uint64_t* e1full = a1empty + 2;
-    uint64_t* a2full = e1full + 1;
+    uint64_t* e1full = a1empty + 2;         // [2] (E1 smem double buffer)
+    uint64_t* a2full = e1full + 2;
     uint64_t* a2empty = a2full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a2empty + 1);
 
@@ -85,7 +88,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
         tc::mbar_init(bfull, 1);
         for (int st = 0; st < kXStages; ++st) { tc::mbar_init(&xfull[st], 1); tc::mbar_init(&xempty[st], 1); }
         for (int a = 0; a < 2; ++a) { tc::mbar_init(&a1full[a], 1); tc::mbar_init(&a1empty[a], kEpiWarps); }
-        tc::mbar_init(e1full, kEpiWarps);
+        tc::mbar_init(&e1full[0], kEpiWarps);
+        tc::mbar_init(&e1full[1], kEpiWarps);
         tc::mbar_init(a2full, 1);
         tc::mbar_init(a2empty, kEpiWarps);
         tc::fence_mbar_init();
@@ -141,16 +145,16 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
             if (n_my > 0) mma1(0);
             for (int j = 0; j < n_my; ++j) {
                 if (j + 1 < n_my) mma1(j + 1);
-                tc::mbar_wait(e1full, j & 1);         // E1 of tile j in shared memory
+                tc::mbar_wait(&e1full[j & 1], (j >> 1) & 1);   // E1 of tile j in shared memory
                 tc::mbar_wait(a2empty, (j & 1) ^ 1);  // acc2 drained (tile j-1)
                 tc::tc_fence_after();
 #pragma unroll
                 for (int kb = 0; kb < KB1; ++kb)
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        tc::mma_bf16(t_acc2, tc::sw128_kmajor_desc(aE1 + kb * kBM * 128 + k * 32),
+                        tc::mma_bf16(t_acc2, tc::sw128_kmajor_desc(aE1 + (j & 1) * S::kE1Bytes + kb * kBM * 128 + k * 32),
                                      tc::sw128_kmajor_desc(aW2 + kb * E2N * 128 + k * 32), id2, (kb | k) != 0);
-                tc::mma_commit(a2full);                // also: E1 smem free again
+                tc::mma_commit(a2full);                // also: E1 buffer j & 1 free again
             }
         }
         __syncwarp();
@@ -161,12 +165,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
         const int r = quarter * 32 + lane;          // tile row = TMEM lane
         uint8_t* stg = smem + S::kOffStg + (warp - 2) * (32 * 128);
         uint32_t stores = 0;
-        for (int j = 0; j < n_my; ++j) {
-            const int m = blockIdx.x + j * gridDim.x;
-            const int row = m * kBM + r;
-            const bool valid = row < rows;
-            int cand = 0, token = 0;
-            if (DROP && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
+        auto rowinfo = [&](int j, int& m, int& row, int& cand, int& token) {
+            m = blockIdx.x + j * gridDim.x;
+            row = m * kBM + r;
+            cand = 0; token = 0;
+            if (DROP && row < rows) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
+        };
+        auto epi1 = [&](int j) {
+            int m, row, cand, token;
+            rowinfo(j, m, row, cand, token);
             // ---- E1 = SiLU(acc1 + b1) (+ dropout site 0) -> bf16 -> swizzled smem (MMA2's A)
             tc::mbar_wait(&a1full[j & 1], (j >> 1) & 1);
             tc::tc_fence_after();
@@ -179,8 +186,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
                 uint32_t pk[16];
 #pragma unroll
                 for (int q = 0; q < 32; q += 2) {
-                    float x0 = silu(__uint_as_float(v[q]) + s_b1[c * 32 + q]);
-                    float x1 = silu(__uint_as_float(v[q + 1]) + s_b1[c * 32 + q + 1]);
+                    float x0 = silu_tanh(__uint_as_float(v[q]) + s_b1[c * 32 + q]);
+                    float x1 = silu_tanh(__uint_as_float(v[q + 1]) + s_b1[c * 32 + q + 1]);
                     if (DROP) {
                         x0 = drop_apply_enc(p.drop, x0, c * 32 + q, token, 0, cand);
                         x1 = drop_apply_enc(p.drop, x1, c * 32 + q + 1, token, 0, cand);
@@ -189,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
                 }
                 const int kb = (c * 32) / 64;               // K-block of MMA2
                 const int piece0 = ((c * 32) % 64) / 8;      // first 16-byte piece of the 128-byte row
-                uint8_t* dst = sE1 + kb * kBM * 128 + r * 128;
+                uint8_t* dst = sE1 + (j & 1) * S::kE1Bytes + kb * kBM * 128 + r * 128;
 #pragma unroll
                 for (int q = 0; q < 4; ++q)
                     *reinterpret_cast<uint4*>(dst + (((piece0 + q) ^ (r & 7)) << 4)) =
@@ -198,7 +205,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
             tc::fence_proxy_async();     // generic-proxy smem writes -> visible to tcgen05.mma
             tc::tc_fence_before();
             __syncwarp();
-            if (lane == 0) { tc::mbar_arrive(e1full); tc::mbar_arrive(&a1empty[j & 1]); }
+            if (lane == 0) { tc::mbar_arrive(&e1full[j & 1]); tc::mbar_arrive(&a1empty[j & 1]); }
+        };
+        auto epi2 = [&](int j) {
+            int m, row, cand, token;
+            rowinfo(j, m, row, cand, token);
             // ---- E2 = SiLU(acc2 + b2) (+ dropout site 1) -> bf16 -> TMA store
             tc::mbar_wait(a2full, j & 1);
             tc::tc_fence_after();
@@ -211,8 +222,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
                 uint32_t pk[16];
 #pragma unroll
                 for (int q = 0; q < 32; q += 2) {
-                    float x0 = silu(__uint_as_float(v[q]) + s_b2[c * 32 + q]);
-                    float x1 = silu(__uint_as_float(v[q + 1]) + s_b2[c * 32 + q + 1]);
+                    float x0 = silu_tanh(__uint_as_float(v[q]) + s_b2[c * 32 + q]);
+                    float x1 = silu_tanh(__uint_as_float(v[q + 1]) + s_b2[c * 32 + q + 1]);
                     if (DROP) {
                         x0 = drop_apply_enc(p.drop, x0, c * 32 + q, token, 1, cand);
                         x1 = drop_apply_enc(p.drop, x1, c * 32 + q + 1, token, 1, cand);
@@ -247,6 +258,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
             tc::tc_fence_before();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(a2empty);
+        };
+        // E1 of tile j+1 is formed while MMA2 of tile j runs (its E1 buffer was freed by MMA2 of j-1)
+        if (n_my > 0) epi1(0);
+        for (int j = 0; j < n_my; ++j) {
+            if (j + 1 < n_my) epi1(j + 1);
+            epi2(j);
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }

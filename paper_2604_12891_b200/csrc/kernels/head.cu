@@ -6,8 +6,6 @@
 #include <cuda_bf16.h>
 #include <math.h>
 
-#include <type_traits>
-
 #include "../kernels.h"
 
 namespace tcl {
@@ -198,53 +196,11 @@ __global__ void __launch_bounds__(256) k_pool_bf16(const __nv_bfloat16* __restri
         *reinterpret_cast<float2*>(pooled + i * dm + 2 * (lane + 32 * j)) = make_float2(acc[2 * j], acc[2 * j + 1]);
 }
 
-// Same reduction with one vector load per lane and row: lane owns E = dm / 32 consecutive columns
-// (E = 8: a 16-byte load, the warp reads a 512-byte row in one instruction).  Rows are summed in
-// the same order as k_pool_bf16, so the result is bit-identical.
-template <int E>
-__global__ void __launch_bounds__(256) k_pool_bf16v(const __nv_bfloat16* __restrict__ F, int ldf,
-                                                    const int32_t* __restrict__ cu,
-                                                    const int32_t* __restrict__ lens, int max_len, int64_t n,
-                                                    float* __restrict__ pooled) {
-    constexpr int dm = 32 * E;
-    using V = typename std::conditional<E == 8, uint4, typename std::conditional<E == 4, uint2, uint32_t>::type>::type;
-    const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (i >= n) return;
-    const int T = lens[i];
-    float acc[E];
-#pragma unroll
-    for (int j = 0; j < E; ++j) acc[j] = 0.0f;
-    if (T >= 1 && T <= max_len) {
-        const __nv_bfloat16* f = F + (int64_t)cu[i] * ldf + E * lane;
-#pragma unroll 4
-        for (int t = 0; t < T; ++t) {
-            union { V v; __nv_bfloat162 h[E / 2]; } u;
-            u.v = *reinterpret_cast<const V*>(f + (int64_t)t * ldf);
-#pragma unroll
-            for (int j = 0; j < E / 2; ++j) {
-                const float2 fv = __bfloat1622float2(u.h[j]);
-                acc[2 * j] += fv.x;
-                acc[2 * j + 1] += fv.y;
-            }
-        }
-        const float invT = 1.0f / (float)T;
-#pragma unroll
-        for (int j = 0; j < E; ++j) acc[j] *= invT;
-    }
-    float* o = pooled + i * dm + E * lane;
-#pragma unroll
-    for (int j = 0; j < E; j += 2) *reinterpret_cast<float2*>(o + j) = make_float2(acc[j], acc[j + 1]);
-}
-
 void launch_pool_bf16(const void* F, int ldf, int dm, const int32_t* cu, const int32_t* lens, int max_len,
                       int64_t n, float* pooled, cudaStream_t s) {
     if (n == 0) return;
     dim3 grid((unsigned)((n + 7) / 8));
     const auto* f = reinterpret_cast<const __nv_bfloat16*>(F);
-    const bool vec_ok = (ldf % 8) == 0 && (reinterpret_cast<uintptr_t>(F) & 15) == 0;
-    if (vec_ok && dm == 256) { k_pool_bf16v<8><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); return; }
-    if (vec_ok && dm == 128) { k_pool_bf16v<4><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); return; }
     switch (dm / 64) {
         case 1: k_pool_bf16<1><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
         case 2: k_pool_bf16<2><<<grid, 256, 0, s>>>(f, ldf, cu, lens, max_len, n, pooled); break;
