@@ -506,6 +506,15 @@ static tcl_status debug_sync(const char* where, cudaStream_t s) {
     return TCL_OK;
 }
 
+// TCL_MIXER=ws selects the warp-specialised mixer variant (mixer_ws.cu) on the bf16 path
+static int mixer_kind_env() {
+    static const int k = [] {
+        const char* v = getenv("TCL_MIXER");
+        return (v && std::string(v) == "ws") ? 1 : 0;
+    }();
+    return k;
+}
+
 // The bf16 projection path (precision == TCL_PREC_BF16_PROJ): tcgen05 GEMMs with fused
 // epilogues for the encoder / in_proj / out_proj(+LN), one fused mixer kernel per layer.
 static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
@@ -574,6 +583,9 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
+            // the fused mixer's gate SiLU(z) is applied here (HBM-bound epilogue, idle SFU) instead of
+            // in the SFU-bound scan; the warp-specialised variant still gates z itself
+            p.silu_from = (mixer_kind_env() == 1 && di >= 128) ? 0 : di;
             // cluster multicast of A across the N-tile CTAs: correct but measured slower (1.40 vs
             // 0.81 ms at `large`: 4 KB slices + cluster-coupled stalls), so opt-in only
             static const int use_mc = [] { const char* v = getenv("TCL_MCAST"); return (v && v[0] == '1') ? 1 : 0; }();
@@ -594,10 +606,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
             static const int diag = [] { const char* v = getenv("TCL_MIXER_DIAG"); return v ? atoi(v) : 0; }();
             a.diag = diag;
-            static const int mixer_kind = [] {
-                const char* v = getenv("TCL_MIXER");   // "ws": warp-specialised variant
-                return (v && std::string(v) == "ws") ? 1 : 0;
-            }();
+            const int mixer_kind = mixer_kind_env();
             e = (mixer_kind == 1 && di >= 128) ? launch_mixer_ws(a, m->num_sms, s) : launch_mixer_fused(a, m->num_sms, s);
             if (e != cudaSuccess) return cuda_error(e, "mixer");
             ++nl;

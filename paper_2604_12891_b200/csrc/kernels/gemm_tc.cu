@@ -213,9 +213,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     tc::tmem_ld32(tbase + c * 32, r);
                     tc::tmem_ld_wait();
                     uint32_t pk[16];
+                    const bool gate = EPI == 0 && p.silu_from > 0 && n_tile * BN + c * 32 >= p.silu_from;
 #pragma unroll
                     for (int j = 0; j < 32; j += 2) {
                         float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
+                        if (EPI == 0 && gate) {
+                            v0 = silu_tanh(v0);
+                            v1 = silu_tanh(v1);
+                        }
                         if (EPI >= 1) {
                             v0 = silu_tanh(v0 + s_bias[c * 32 + j]);
                             v1 = silu_tanh(v1 + s_bias[c * 32 + j + 1]);

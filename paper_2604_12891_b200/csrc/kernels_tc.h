@@ -23,6 +23,8 @@ struct TcGemmParams {
     // TC_EPI_RESID_LN: H = (residual ? H : 0) + acc (+ bias); out = bf16(LN(H) * g + b)
     float* H; int ldh; int residual;
     int skip_h_store;
+    int silu_from;               // EPI_BF16 without bias: columns >= silu_from (> 0) leave as SiLU(acc)
+                                 // (in_proj: the mixer's gate SiLU(z) formed in this HBM-bound epilogue)
     int mcast;                   // EPI_BF16, n_tiles in {2, 4}: the n_tiles CTAs of a cluster share each
                                  // A tile via TMA multicast (A map box {64, 128 / n_tiles})            // RESID_LN (gemm_tc_ln): do not write H back (last layer: only LN_f(H) is consumed)
     const float* ln_g; const float* ln_b; float eps;
