@@ -165,6 +165,10 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
     m->nxp = round_up(R + 2 * N, 8);
     m->rp = R <= 16 ? 16 : 32;
     m->bn_in = std::min(128, 2 * di);  // 4 N tiles at di = 256: B slice 64 KB, 8-stage A ring
+    if (const char* v = getenv("TCL_BN_IN")) {   // A/B experiments only
+        const int b = atoi(v);
+        if ((b == 128 || b == 256) && b <= 2 * di) m->bn_in = b;
+    }
     HostW h = host_offsets(d, wh);
     if ((st = upload_bf16(m, h.W1, e1, d.d_in, e1, kXld, &m->W1b)) != TCL_OK) return st;
     if ((st = upload_bf16(m, h.W2, e2, e1, e2, e1, &m->W2b)) != TCL_OK) return st;
@@ -920,8 +924,8 @@ tcl_status tcl_topk(tcl_model* m, const float* scores, int64_t n, int32_t k, int
     unsigned long long* keys = m->topk_tmp;                 // k keys
     unsigned long long* tmp = m->topk_tmp + k;
     ProfScope ps(m, TCL_PROF_TOPK, s);
-    m->launches += launch_topk_keys(scores, n, k, index_base, keys, tmp, s);
-    m->launches += launch_topk_merge(keys, k, k, idx, top, tmp, s);
+    m->launches += launch_topk_keys(scores, n, k, index_base, keys, tmp, s);   // sorted best k, 0-padded
+    m->launches += launch_topk_decode(keys, k, idx, top, s);
     CUDA_TRY(cudaGetLastError());
     return TCL_OK;
 }
@@ -1095,7 +1099,7 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
     // large launches (no per-launch ramp/tail of many small grids).
     const int64_t cap = std::max<int64_t>(1, chunk_cap(m));
     std::vector<int64_t> sub_off, sub_n;
-    for (int64_t off = 0, sz = std::min<int64_t>(cap, 4096); off < n;) {
+    for (int64_t off = 0, sz = std::min<int64_t>(cap, 2048); off < n;) {
         const int64_t nc = std::min(sz, n - off);
         sub_off.push_back(off);
         sub_n.push_back(nc);

@@ -131,6 +131,8 @@ size_t topk_tmp_keys(int64_t n, int k);
 int launch_topk_keys(const float* scores, int64_t n, int k, int64_t index_base,
                      unsigned long long* out_keys, unsigned long long* tmp, cudaStream_t s);
 // Top-k of `count` keys -> decoded (idx, score) [k].  tmp: k + topk_tmp_keys(count, k) keys.
+// decode k keys that are already the sorted top-k (0-padded) into (index, score)
+int launch_topk_decode(const unsigned long long* keys, int k, int64_t* idx, float* score, cudaStream_t s);
 int launch_topk_merge(const unsigned long long* keys, int64_t count, int k, int64_t* idx,
                       float* score, unsigned long long* tmp, cudaStream_t s);
 

@@ -58,14 +58,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Accurate e^x - 1 (x2 = x log2 e): series where Ab - 1 would cancel (as mixer.cu's fp32 scan).
+// Accurate e^x - 1 (x2 = x log2 e): the degree-6 series where Ab - 1 would cancel (|x2| < 0.25, as
+// mixer.cu's fp32 scan), selected without a branch: |Delta A| straddles the threshold across the
+// states of one warp, so a branch would run both paths serially anyway.
 __device__ __forceinline__ float expm1_acc(float x2, float Ab) {
-    if (fabsf(x2) < 0.25f) {
-        const float x = x2 * kLn2;
-        return x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720, 1.0f / 120), 1.0f / 24),
-                                          1.0f / 6), 0.5f), 1.0f);
-    }
-    return Ab - 1.0f;
+    const float x = x2 * kLn2;
+    const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720, 1.0f / 120), 1.0f / 24),
+                                                1.0f / 6), 0.5f), 1.0f);
+    return fabsf(x2) < 0.25f ? ser : Ab - 1.0f;
 }
 
 template <int DI, int N, int R, int DC, int DISC>

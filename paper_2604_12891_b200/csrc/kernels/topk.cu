@@ -120,6 +120,11 @@ int launch_topk_keys(const float* scores, int64_t n, int k, int64_t index_base, 
     return tournament(scores, nullptr, n, k, index_base, out_keys, tmp, s);
 }
 
+int launch_topk_decode(const u64* keys, int k, int64_t* idx, float* score, cudaStream_t s) {
+    k_topk_decode<<<(k + 255) / 256, 256, 0, s>>>(keys, k, idx, score);
+    return 1;
+}
+
 int launch_topk_merge(const u64* keys, int64_t count, int k, int64_t* idx, float* score, u64* tmp,
                       cudaStream_t s) {
     u64* fin = tmp;  // k keys, then the tournament scratch
