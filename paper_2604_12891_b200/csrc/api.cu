@@ -1099,7 +1099,9 @@ tcl_status tcl_score_host(tcl_model* m, const float* feats_h, const int32_t* len
     // large launches (no per-launch ramp/tail of many small grids).
     const int64_t cap = std::max<int64_t>(1, chunk_cap(m));
     std::vector<int64_t> sub_off, sub_n;
-    for (int64_t off = 0, sz = std::min<int64_t>(cap, 2048); off < n;) {
+    // (small batches are one launch sequence: splitting them costs more in launch-bound kernels
+    // than the exposed copy of the whole batch)
+    for (int64_t off = 0, sz = std::min<int64_t>(cap, n <= 16384 ? n : 4096); off < n;) {
         const int64_t nc = std::min(sz, n - off);
         sub_off.push_back(off);
         sub_n.push_back(nc);
