@@ -156,6 +156,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0)
+    ap.add_argument("--precision", choices=["config", "fp32", "bf16"], default="config",
+                    help="override the configuration's precision (fp32 path / bf16 projections)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -165,6 +167,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     cfg = inputs.config(args.config)
+    if args.precision != "config":
+        cfg = dict(cfg, dims=cfg["dims"].replace(
+            precision=inputs.PREC_BF16_PROJ if args.precision == "bf16" else inputs.PREC_FP32))
     d = cfg["dims"]
     n = args.n or cfg["n"]
     if args.config == "long" and not args.n:
@@ -411,6 +416,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.config], "config": args.config,
+                       "precision": "bf16 projections" if d.precision == inputs.PREC_BF16_PROJ else "fp32",
                        "n_per_gpu": n, "global_n": n * world, "packed_tokens_per_gpu": P,
                        "max_len": d.max_len, "d_model": d.d_model, "n_layer": d.n_layer,
                        "d_state": d.d_state, "topk": k, "mc_passes": mc,

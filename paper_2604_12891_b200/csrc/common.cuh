@@ -69,6 +69,18 @@ __device__ __forceinline__ bool dropout_keep(const DropoutCtx& d, int unit, int 
     return word >= d.thr;
 }
 
+// The keep words of units [4 g, 4 g + 3] from one Philox call (dropout_keep(d, u, ...) reads word
+// u & 3 of the call for unit4 = u & ~3): epilogues that own 4 consecutive units draw once.
+__device__ __forceinline__ u32x4 dropout_words(const DropoutCtx& d, int unit4, int token, int site,
+                                               int64_t cand) {
+    u32x4 c = {(uint32_t)unit4 >> 2, ((uint32_t)token << 2) | (uint32_t)site, (uint32_t)d.pass,
+               (uint32_t)(d.index_base + cand)};
+    return philox4x32_10(c, (uint32_t)d.seed, (uint32_t)(d.seed >> 32));
+}
+__device__ __forceinline__ float dropout_apply_word(const DropoutCtx& d, float v, uint32_t word) {
+    return word >= d.thr ? v * d.scale : 0.0f;
+}
+
 __device__ __forceinline__ float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);

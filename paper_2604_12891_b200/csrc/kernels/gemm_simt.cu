@@ -74,9 +74,11 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
         const int gm = m0 + ty * 4 + i;
         if (gm >= rows) continue;
         int cand = 0, token = 0;
+        u32x4 wd = {0u, 0u, 0u, 0u};
         if (a.epi == EPI_SILU && a.drop.enabled) {
             cand = a.rows_are_cands ? gm : a.row_cand[gm];
             token = a.rows_are_cands ? 0 : gm - a.cu[cand];
+            wd = dropout_words(a.drop, n0 + tx * 4, token, a.site, cand);   // this thread's 4 units
         }
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -89,7 +91,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
                 case EPI_SILU:
                     v = silu(v);
                     if (a.drop.enabled)
-                        v = dropout_keep(a.drop, gn, token, a.site, cand) ? v * a.drop.scale : 0.0f;
+                        v = dropout_apply_word(a.drop, v, j == 0 ? wd.x : j == 1 ? wd.y : j == 2 ? wd.z : wd.w);
                     break;
                 case EPI_SOFTPLUS: v = softplus(v); break;
                 case EPI_RESID: v = *dst + v; break;
@@ -211,10 +213,13 @@ __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
                     v[0] = o.x + v[0]; v[1] = o.y + v[1]; v[2] = o.z + v[2]; v[3] = o.w + v[3];
                 } else if (a.epi == EPI_SILU) {
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        v[q] = silu(v[q]);
-                        if (a.drop.enabled)
-                            v[q] = dropout_keep(a.drop, gn0 + q, token, a.site, cand) ? v[q] * a.drop.scale : 0.0f;
+                    for (int q = 0; q < 4; ++q) v[q] = silu(v[q]);
+                    if (a.drop.enabled) {   // gn0 % 4 == 0: one Philox draw for the 4 units
+                        const u32x4 wd = dropout_words(a.drop, gn0, token, a.site, cand);
+                        v[0] = dropout_apply_word(a.drop, v[0], wd.x);
+                        v[1] = dropout_apply_word(a.drop, v[1], wd.y);
+                        v[2] = dropout_apply_word(a.drop, v[2], wd.z);
+                        v[3] = dropout_apply_word(a.drop, v[3], wd.w);
                     }
                 } else if (a.epi == EPI_SOFTPLUS) {
 #pragma unroll

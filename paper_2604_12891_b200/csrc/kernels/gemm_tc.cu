@@ -54,9 +54,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // MC-dropout keep test kept out of line: the hot epilogues stay small (no I-cache pressure).
-__device__ __noinline__ float drop_apply(const DropoutCtx& d, float v, int unit, int token, int site,
-                                         int64_t cand) {
-    return dropout_keep(d, unit, token, site, cand) ? v * d.scale : 0.0f;
+__device__ __noinline__ u32x4 drop_words(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
+    return dropout_words(d, unit4, token, site, cand);
 }
 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
@@ -215,22 +214,23 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     uint32_t pk[16];
                     const bool gate = EPI == 0 && p.silu_from > 0 && n_tile * BN + c * 32 >= p.silu_from;
 #pragma unroll
-                    for (int j = 0; j < 32; j += 2) {
-                        float v0 = __uint_as_float(r[j]), v1 = __uint_as_float(r[j + 1]);
-                        if (EPI == 0 && gate) {
-                            v0 = silu_tanh(v0);
-                            v1 = silu_tanh(v1);
+                    for (int j = 0; j < 32; j += 4) {
+                        float x[4];
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            x[e] = __uint_as_float(r[j + e]);
+                            if (EPI == 0 && gate) x[e] = silu_tanh(x[e]);
+                            if (EPI >= 1) x[e] = silu_tanh(x[e] + s_bias[c * 32 + j + e]);
                         }
-                        if (EPI >= 1) {
-                            v0 = silu_tanh(v0 + s_bias[c * 32 + j]);
-                            v1 = silu_tanh(v1 + s_bias[c * 32 + j + 1]);
+                        if (EPI == 2) {   // one Philox draw for the 4 consecutive units
+                            const u32x4 wd = drop_words(p.drop, n_tile * BN + c * 32 + j, token, p.site, cand);
+                            x[0] = dropout_apply_word(p.drop, x[0], wd.x);
+                            x[1] = dropout_apply_word(p.drop, x[1], wd.y);
+                            x[2] = dropout_apply_word(p.drop, x[2], wd.z);
+                            x[3] = dropout_apply_word(p.drop, x[3], wd.w);
                         }
-                        if (EPI == 2) {
-                            const int n = n_tile * BN + c * 32 + j;
-                            v0 = drop_apply(p.drop, v0, n, token, p.site, cand);
-                            v1 = drop_apply(p.drop, v1, n + 1, token, p.site, cand);
-                        }
-                        pk[j / 2] = pack_bf16x2(v0, v1);
+                        pk[j / 2] = pack_bf16x2(x[0], x[1]);
+                        pk[j / 2 + 1] = pack_bf16x2(x[2], x[3]);
                     }
                     if constexpr (S::kTmaStore) {
                         // chunk parity picks the 64-byte half of the 128-byte staged row

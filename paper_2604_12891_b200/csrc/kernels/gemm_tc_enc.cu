@@ -48,9 +48,9 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
-__device__ __noinline__ float drop_apply_enc(const DropoutCtx& d, float v, int unit, int token, int site,
-                                             int64_t cand) {
-    return dropout_keep(d, unit, token, site, cand) ? v * d.scale : 0.0f;
+// one Philox draw per 4 consecutive units (kept out of line: small hot epilogues)
+__device__ __noinline__ u32x4 drop_words_enc(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
+    return dropout_words(d, unit4, token, site, cand);
 }
 
 template <int E1N, int E2N, bool DROP>
@@ -185,14 +185,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
                 tc::tmem_ld_wait();
                 uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 32; q += 2) {
-                    float x0 = silu_tanh(__uint_as_float(v[q]) + s_b1[c * 32 + q]);
-                    float x1 = silu_tanh(__uint_as_float(v[q + 1]) + s_b1[c * 32 + q + 1]);
+                for (int q = 0; q < 32; q += 4) {
+                    float x[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x[e] = silu_tanh(__uint_as_float(v[q + e]) + s_b1[c * 32 + q + e]);
                     if (DROP) {
-                        x0 = drop_apply_enc(p.drop, x0, c * 32 + q, token, 0, cand);
-                        x1 = drop_apply_enc(p.drop, x1, c * 32 + q + 1, token, 0, cand);
+                        const u32x4 wd = drop_words_enc(p.drop, c * 32 + q, token, 0, cand);
+                        x[0] = dropout_apply_word(p.drop, x[0], wd.x);
+                        x[1] = dropout_apply_word(p.drop, x[1], wd.y);
+                        x[2] = dropout_apply_word(p.drop, x[2], wd.z);
+                        x[3] = dropout_apply_word(p.drop, x[3], wd.w);
                     }
-                    pk[q / 2] = pack_bf16x2(x0, x1);
+                    pk[q / 2] = pack_bf16x2(x[0], x[1]);
+                    pk[q / 2 + 1] = pack_bf16x2(x[2], x[3]);
                 }
                 const int kb = (c * 32) / 64;               // K-block of MMA2
                 const int piece0 = ((c * 32) % 64) / 8;      // first 16-byte piece of the 128-byte row
@@ -221,14 +226,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
                 tc::tmem_ld_wait();
                 uint32_t pk[16];
 #pragma unroll
-                for (int q = 0; q < 32; q += 2) {
-                    float x0 = silu_tanh(__uint_as_float(v[q]) + s_b2[c * 32 + q]);
-                    float x1 = silu_tanh(__uint_as_float(v[q + 1]) + s_b2[c * 32 + q + 1]);
+                for (int q = 0; q < 32; q += 4) {
+                    float x[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) x[e] = silu_tanh(__uint_as_float(v[q + e]) + s_b2[c * 32 + q + e]);
                     if (DROP) {
-                        x0 = drop_apply_enc(p.drop, x0, c * 32 + q, token, 1, cand);
-                        x1 = drop_apply_enc(p.drop, x1, c * 32 + q + 1, token, 1, cand);
+                        const u32x4 wd = drop_words_enc(p.drop, c * 32 + q, token, 1, cand);
+                        x[0] = dropout_apply_word(p.drop, x[0], wd.x);
+                        x[1] = dropout_apply_word(p.drop, x[1], wd.y);
+                        x[2] = dropout_apply_word(p.drop, x[2], wd.z);
+                        x[3] = dropout_apply_word(p.drop, x[3], wd.w);
                     }
-                    pk[q / 2] = pack_bf16x2(x0, x1);
+                    pk[q / 2] = pack_bf16x2(x[0], x[1]);
+                    pk[q / 2 + 1] = pack_bf16x2(x[2], x[3]);
                 }
                 const int k = c - half * (E2N / 64);        // chunk within this warp's columns
                 if ((k & 1) == 0 && stores > 0) {            // staging reuse: previous store read it

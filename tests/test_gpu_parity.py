@@ -75,6 +75,22 @@ def test_score_parity_bf16_large_small_batch(torch_cuda, oracle):
     assert rho > 0.99
 
 
+@pytest.mark.parametrize("name", ["tuning", "rdu", "paper"])
+def test_bf16_path_on_fp32_configs(torch_cuda, oracle, name):
+    """The d_model-128 configurations run through the bf16-projection path (tcgen05 encoder, in_proj,
+    out_proj + LN, fused mixer at d_inner 128, N 8) within that path's 2e-2 bound, MC included."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup(name, n=512)
+    d = d.replace(precision=inputs.PREC_BF16_PROJ)
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    ref = oracle.score(d, w, f, l)
+    _check_scores(got, ref, d.precision)
+    mean, var = _mc_gpu(torch_cuda, m, f[:64], l[:64], 4, 77, index_base=3)
+    rm, rv = oracle.score_mc(d, w, f[:64], l[:64], 4, 77, index_base=3)
+    _check_scores(mean, rm, d.precision)
+
+
 def test_full_size_sampled_parity_large(torch_cuda, oracle):
     """BASELINE.json full size (65,536 candidates, the bench configuration); the oracle scores a
     sample of candidates one by one, plus every top-k member."""
