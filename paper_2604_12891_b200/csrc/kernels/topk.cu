@@ -91,7 +91,9 @@ static int chunk_for(int k) { return k <= 512 ? 2048 : (k <= 1024 ? 4096 : kTopk
 static int tournament(const float* scores, const u64* keys, int64_t count, int k,
                       int64_t index_base, u64* out, u64* tmp, cudaStream_t s) {
     int launched = 0;
-    const int C = chunk_for(k);
+    // a set that fits one CTA's chunk is selected in a single round (no cross-CTA tournament)
+    const int64_t need = count > k ? count : k;   // the chunk must also hold the k outputs
+    const int C = need <= 2048 ? 2048 : need <= 4096 ? 4096 : need <= kTopkChunk ? kTopkChunk : chunk_for(k);
     const int64_t blocks0 = (count + C - 1) / C;
     u64* buf[2] = {tmp, tmp + blocks0 * k + kTopkChunk};
     int which = 0;

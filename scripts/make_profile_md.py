@@ -27,7 +27,7 @@ def main():
              "--metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`. ncu times are "
              "serialised and cold-cache: compare shares, not absolutes; bench.py's CUDA-event stage times are the live "
              "numbers. (k_ex2 / k_tanh / k_ffma / k_ffma2 are bench.py's peak microbenchmarks, run outside the timed "
-             "region.)\n", "## Bench line of the same build\n"]
+             "region; k_pack / k_pool_bf16 captures use -s 3.)\n", "## Bench line of the same build\n"]
     for f in ("bench_official.json", "bench_reference.json"):
         p = os.path.join(OUT, f)
         if os.path.exists(p):
@@ -36,7 +36,7 @@ def main():
     parts.append(run("launches", os.path.join(OUT, "launches_official.csv")))
     parts.append("## Per-kernel full captures\n")
     reps = sorted(f for f in os.listdir(OUT) if f.startswith("prof_official_") and f.endswith(".ncu-rep"))
-    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_gemm_simt", "k_topk_chunk", "k_pool_bf16", "k_pack"]
+    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_simt", "k_topk_chunk", "k_pool_bf16", "k_pack"]
     reps.sort(key=lambda f: next((i for i, k in enumerate(order) if k in f), 99))
     for f in reps:
         parts.append(run("report", os.path.join(OUT, f)))
