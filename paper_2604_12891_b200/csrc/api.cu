@@ -335,6 +335,11 @@ struct F32Run {
     cudaStream_t s;
     const int32_t* lens;
     int64_t n;
+    // one-column forward at d_model 128: the LayerNorm that follows a GEMM writing the residual
+    // stream (LN_0 after the encoder, LN_{l+1} after out_proj_l) runs in that GEMM's epilogue
+    bool fuse_ln = false;
+    const float* ln_g = nullptr;   // set by the caller of gemm(..., EPI_RESID_LN / EPI_LN, ...)
+    const float* ln_b = nullptr;
 
     // Y = epi(X W^T [+ X2 W2^T] + b) over the packed rows (or over the n candidates: cands = true)
     void gemm(const float* X, int ldx, const float* W, int ldw, const float* b, float* Y, int ldy, int K,
@@ -342,6 +347,9 @@ struct F32Run {
               const float* W2 = nullptr, int K2 = 0, bool cands = false, bool dropout = true) const {
         ProfScope ps(m, kind, s);
         GemmArgs g{};
+        if (epi == EPI_RESID_LN || epi == EPI_LN) {
+            g.ln_g = ln_g; g.ln_b = ln_b; g.ln_eps = m->dims.ln_eps; g.Y2 = m->ws.A; g.ldy2 = Nout;
+        }
         g.X = X; g.ldx = ldx; g.W = W; g.ldw = ldw; g.bias = b; g.Y = Y; g.ldy = ldy;
         g.K = K; g.N = Nout; g.epi = epi; g.drop = drop; g.site = site;
         if (cands) { g.max_rows = (int)n; g.rows_const = (int)n; g.rows_are_cands = 1; }
@@ -363,9 +371,10 @@ struct F32Run {
         Workspace& w = m->ws;
         const int dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
         const LayerPtrs& q = col->wp.layers[l];
-        {
+        if (!fuse_ln) {   // (fused: the previous GEMM's epilogue already wrote LN_l(H) into A)
             ProfScope ps(m, TCL_PROF_LAYERNORM, s);
-            launch_layernorm(H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s); ++m->launches;
+            launch_layernorm(H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s,
+                             /*gemm_epilogue_order=*/true); ++m->launches;
         }
         gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
         static const bool fused = [] { const char* v = getenv("TCL_F32_MIXER"); return !(v && v[0] == '0'); }();
@@ -398,11 +407,17 @@ struct F32Run {
             launch_scan(sa, s); ++m->launches;
         }
         }
-        if (site)
+        if (site) {
             gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ, w.Lat, m->ad_ld,
                  site->Ua, m->ad_ld);
-        else
+        } else if (fuse_ln && l + 1 < d.n_layer) {
+            F32Run r2 = *this;
+            r2.ln_g = col->wp.layers[l + 1].ln_w;
+            r2.ln_b = col->wp.layers[l + 1].ln_b;
+            r2.gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID_LN, -1, TCL_PROF_OUT_PROJ);
+        } else {
             gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ);
+        }
     }
 };
 
@@ -494,7 +509,16 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     float* E2 = w.Delta;
     r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
     r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
-    r.gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER);
+    static const bool fuse_env = [] { const char* v = getenv("TCL_F32_FUSE_LN"); return !(v && v[0] == '0'); }();
+    r.fuse_ln = fuse_env && dm == 128 && d.n_layer > 0;
+    if (r.fuse_ln) {
+        F32Run r0 = r;
+        r0.ln_g = m->wp.layers[0].ln_w;
+        r0.ln_b = m->wp.layers[0].ln_b;
+        r0.gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_LN, -1, TCL_PROF_ENCODER);
+    } else {
+        r.gemm(E2, e2, m->wp.enc_W3, e2, m->wp.enc_b3, w.H, dm, e2, dm, EPI_NONE, -1, TCL_PROF_ENCODER);
+    }
     for (int l = 0; l < d.n_layer; ++l) r.layer(m, l, w.H, nullptr);
     run_head(m, lens, n, scores, drop, mc_mean, s);
 }

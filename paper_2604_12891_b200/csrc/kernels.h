@@ -21,7 +21,9 @@ void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int
                  int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s);
 
 // ---- SIMT fp32 GEMM with fused epilogues ------------------------------------------------------
-enum Epi : int { EPI_NONE = 0, EPI_SILU = 1, EPI_SOFTPLUS = 2, EPI_RESID = 3 };
+enum Epi : int { EPI_NONE = 0, EPI_SILU = 1, EPI_SOFTPLUS = 2, EPI_RESID = 3,
+                 // N == 128 only (one CTA column owns whole rows): Y (+)= acc + b, then Y2 = LN(Y) (next pre-norm)
+                 EPI_RESID_LN = 4, EPI_LN = 5 };
 struct GemmArgs {
     const float* X; int ldx;        // [M][K]
     const float* W; int ldw;        // [N][K] (PyTorch [out][in])
@@ -42,13 +44,16 @@ struct GemmArgs {
     // training: wT != 0 reads W transposed (element (j, k) at W[k * ldw + j], i.e. Y = X W);
     // Ypre != nullptr also stores the pre-activation (before the epilogue) at Ypre[m * ldy + j]
     int wT; float* Ypre;
+    // EPI_RESID_LN / EPI_LN: the LayerNorm that follows (affine, biased variance), output Y2
+    const float* ln_g; const float* ln_b; float ln_eps; float* Y2; int ldy2;
 };
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s);
 
 // ---- LayerNorm rows (fp32 in, fp32 out and/or bf16 out) ---------------------------------------
 void launch_layernorm(const float* H, int ldh, int dm, const float* g, const float* b, float eps,
                       float* Y, void* Ybf16, int ldy, int max_rows, const int32_t* p_rows,
-                      cudaStream_t s);
+                      cudaStream_t s,
+                      bool gemm_epilogue_order = false);
 
 // ---- causal depthwise conv + SiLU (a5) --------------------------------------------------------
 // X [P][ldx] (x part = first di columns) -> U [P][di]

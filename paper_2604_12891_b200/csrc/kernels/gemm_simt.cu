@@ -5,6 +5,8 @@
 // FFMA accumulation in a fixed k order: a row's result never depends on the other rows of the
 // tile, so scores are batch-invariant (reading R19).
 // Tile 64x64x16, 256 threads, 4x4 outputs per thread, operands staged k-major in shared memory.
+#include <cstdlib>
+
 #include "../kernels.h"
 
 namespace tcl {
@@ -107,7 +109,7 @@ __global__ void __launch_bounds__(256) k_gemm_simt(GemmArgs a) {
 // tx*4 + {0..3, 64..67}: four 128-bit smem loads feed 64 FFMA per k step), smem double-buffered
 // with register prefetch of the next k-block (one barrier per k-block).  The k order of every
 // output is the same sequential 0..K-1 FFMA chain as k_gemm_simt, so results are bit-identical.
-constexpr int BM2 = 128, BN2 = 128, BK2 = 8;
+constexpr int BM2 = 128, BN2 = 128;
 
 __device__ __forceinline__ void epi_store(const GemmArgs& a, int gm, int gn, float acc, int cand, int token) {
     float v = acc + (a.bias ? __ldg(a.bias + gn) : 0.0f);
@@ -125,50 +127,61 @@ __device__ __forceinline__ void epi_store(const GemmArgs& a, int gm, int gn, flo
     *dst = v;
 }
 
+// BK: k depth per shared-memory stage (8 or 16); SEG2: the KB + AC lateral K segment is present.
+template <int BK, bool SEG2>
 __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
-    __shared__ __align__(16) float As[2][BK2][BM2 + 4];
-    __shared__ __align__(16) float Ws[2][BK2][BN2 + 4];
+    constexpr int NV = BK / 8;   // float4 loads per thread and operand per stage
+    __shared__ __align__(16) float As[2][BK][BM2 + 4];
+    __shared__ __align__(16) float Ws[2][BK][BN2 + 4];
     const int rows = a.p_rows ? *a.p_rows : a.rows_const;
     const int m0 = blockIdx.x * BM2;
     if (m0 >= rows) return;
     const int n0 = blockIdx.y * BN2;
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
-    // loader: 128 rows x 8 k = 1024 floats = 256 threads x float4 (row tid/2, k offset 4*(tid&1))
-    const int lr = tid >> 1, lk = (tid & 1) * 4;
+    // loader: 128 rows x BK k = 256 threads x NV float4 (row tid/2, k offset (tid&1) * BK/2)
+    const int lr = tid >> 1, lk = (tid & 1) * (BK / 2);
     float acc[8][8];
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
         for (int j = 0; j < 8; ++j) acc[i][j] = 0.0f;
 
-    const int k_end = a.K + a.K2;
-    auto load = [&](int k0, float4& xv, float4& wv) {
-        const bool second = k0 >= a.K;
+    const int k_end = a.K + (SEG2 ? a.K2 : 0);
+    float4 xv[NV], wv[NV];
+    auto load = [&](int k0) {
+        const bool second = SEG2 && k0 >= a.K;
         const float* X = second ? a.X2 : a.X;
         const float* W = second ? a.W2 : a.W;
         const int ldx = second ? a.ldx2 : a.ldx, ldw = second ? a.ldw2 : a.ldw;
         const int kk_end = second ? a.K2 : a.K;
-        const int gm = m0 + lr, gk = (second ? k0 - a.K : k0) + lk, gn = n0 + lr;
-        xv = make_float4(0.f, 0.f, 0.f, 0.f);
-        wv = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (gm < rows && gk < kk_end) xv = *reinterpret_cast<const float4*>(X + (int64_t)gm * ldx + gk);
-        if (gn < a.N && gk < kk_end) wv = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
+        const int gm = m0 + lr, gn = n0 + lr;
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int gk = (second ? k0 - a.K : k0) + lk + 4 * v;
+            xv[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            wv[v] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (gm < rows && gk < kk_end) xv[v] = *reinterpret_cast<const float4*>(X + (int64_t)gm * ldx + gk);
+            if (gn < a.N && gk < kk_end) wv[v] = __ldg(reinterpret_cast<const float4*>(W + (int64_t)gn * ldw + gk));
+        }
     };
-    auto stash = [&](int b, const float4& xv, const float4& wv) {
-        As[b][lk + 0][lr] = xv.x; As[b][lk + 1][lr] = xv.y; As[b][lk + 2][lr] = xv.z; As[b][lk + 3][lr] = xv.w;
-        Ws[b][lk + 0][lr] = wv.x; Ws[b][lk + 1][lr] = wv.y; Ws[b][lk + 2][lr] = wv.z; Ws[b][lk + 3][lr] = wv.w;
+    auto stash = [&](int b) {
+#pragma unroll
+        for (int v = 0; v < NV; ++v) {
+            const int k = lk + 4 * v;
+            As[b][k + 0][lr] = xv[v].x; As[b][k + 1][lr] = xv[v].y; As[b][k + 2][lr] = xv[v].z; As[b][k + 3][lr] = xv[v].w;
+            Ws[b][k + 0][lr] = wv[v].x; Ws[b][k + 1][lr] = wv[v].y; Ws[b][k + 2][lr] = wv[v].z; Ws[b][k + 3][lr] = wv[v].w;
+        }
     };
-    float4 xv, wv;
-    load(0, xv, wv);
-    stash(0, xv, wv);
+    load(0);
+    stash(0);
     __syncthreads();
     int b = 0;
-    for (int k0 = 0; k0 < k_end; k0 += BK2) {
-        const bool more = k0 + BK2 < k_end;
-        if (more) load(k0 + BK2, xv, wv);    // global loads in flight during this k-block's math
+    for (int k0 = 0; k0 < k_end; k0 += BK) {
+        const bool more = k0 + BK < k_end;
+        if (more) load(k0 + BK);    // global loads in flight during this k-block's math
 #pragma unroll
-        for (int kk = 0; kk < BK2; ++kk) {
+        for (int kk = 0; kk < BK; ++kk) {
             const float4 a0 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4]);
             const float4 a1 = *reinterpret_cast<const float4*>(&As[b][kk][ty * 4 + 64]);
             const float4 w0 = *reinterpret_cast<const float4*>(&Ws[b][kk][tx * 4]);
@@ -181,12 +194,59 @@ __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
                 for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(ar[i], wr[j], acc[i][j]);
         }
         if (more) {
-            stash(b ^ 1, xv, wv);   // the other buffer: last read before the previous barrier
+            stash(b ^ 1);   // the other buffer: last read before the previous barrier
             __syncthreads();
             b ^= 1;
         }
     }
 
+    if (a.epi == EPI_RESID_LN || a.epi == EPI_LN) {
+        // whole 128-wide rows in this CTA: the 16 threads of a half-warp (same ty) hold one row's
+        // 128 columns (8 each) -> two-pass mean / variance by 16-lane shuffles, as norm.cu
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int gm = m0 + ty * 4 + (i & 3) + (i >> 2) * 64;
+            const bool valid = gm < rows;
+            float v[8];
+#pragma unroll
+            for (int jh = 0; jh < 2; ++jh) {
+                const int gn0 = tx * 4 + jh * 64;
+                float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+                float* dst = a.Y + (int64_t)gm * a.ldy + gn0;
+                if (valid && a.epi == EPI_RESID_LN) o = *reinterpret_cast<const float4*>(dst);
+                const float b0 = a.bias ? __ldg(a.bias + gn0) : 0.f, b1 = a.bias ? __ldg(a.bias + gn0 + 1) : 0.f,
+                            b2 = a.bias ? __ldg(a.bias + gn0 + 2) : 0.f, b3 = a.bias ? __ldg(a.bias + gn0 + 3) : 0.f;
+                v[jh * 4 + 0] = o.x + (acc[i][jh * 4 + 0] + b0);
+                v[jh * 4 + 1] = o.y + (acc[i][jh * 4 + 1] + b1);
+                v[jh * 4 + 2] = o.z + (acc[i][jh * 4 + 2] + b2);
+                v[jh * 4 + 3] = o.w + (acc[i][jh * 4 + 3] + b3);
+                if (valid) *reinterpret_cast<float4*>(dst) = make_float4(v[jh * 4], v[jh * 4 + 1], v[jh * 4 + 2], v[jh * 4 + 3]);
+            }
+            float sm = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sm += v[q];
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+            const float mean = sm * (1.0f / 128);
+            float sq = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { const float t = v[q] - mean; sq = fmaf(t, t, sq); }
+#pragma unroll
+            for (int o = 1; o < 16; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+            const float rstd = rsqrtf(sq * (1.0f / 128) + a.ln_eps);
+            if (valid) {
+#pragma unroll
+                for (int jh = 0; jh < 2; ++jh) {
+                    const int c = tx * 4 + jh * 64;
+                    float r[4];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) r[q] = (v[jh * 4 + q] - mean) * rstd * __ldg(a.ln_g + c + q) + __ldg(a.ln_b + c + q);
+                    *reinterpret_cast<float4*>(a.Y2 + (int64_t)gm * a.ldy2 + c) = make_float4(r[0], r[1], r[2], r[3]);
+                }
+            }
+        }
+        return;
+    }
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
         const int gm = m0 + ty * 4 + (i & 3) + (i >> 2) * 64;
@@ -239,9 +299,14 @@ __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
 
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
     if (a.max_rows <= 0) return;
-    if (a.N >= 128 && !a.wT && (a.K % BK2) == 0 && (a.K2 % BK2) == 0) {
+    static const int bk = [] { const char* v = getenv("TCL_SIMT_BK"); return (v && atoi(v) == 8) ? 8 : 16; }();
+    const bool ln = a.epi == EPI_RESID_LN || a.epi == EPI_LN;
+    if (ln && (a.N != 128 || a.wT || (a.K % 16) != 0 || (a.K2 % 16) != 0)) return;   // callers guarantee
+    if (a.N >= 128 && !a.wT && (a.K % 16) == 0 && (a.K2 % 16) == 0) {
         dim3 grid2((a.max_rows + BM2 - 1) / BM2, (a.N + BN2 - 1) / BN2);
-        k_gemm_simt128<<<grid2, 256, 0, s>>>(a);
+        if (a.K2 > 0) k_gemm_simt128<16, true><<<grid2, 256, 0, s>>>(a);
+        else if (bk == 16) k_gemm_simt128<16, false><<<grid2, 256, 0, s>>>(a);
+        else k_gemm_simt128<8, false><<<grid2, 256, 0, s>>>(a);
         return;
     }
     dim3 grid((a.max_rows + BM - 1) / BM, (a.N + BN - 1) / BN);
