@@ -312,9 +312,12 @@ def test_mc_parity(torch_cuda, oracle, name):
 
 
 # ------------------------------------------------------------------------------------ host e2e
-def test_score_host_matches_device(torch_cuda):
+@pytest.mark.parametrize("n", [1000, 20000, 70000])
+def test_score_host_matches_device(torch_cuda, n):
+    """tcl_score_host (pinned host buffers, pipelined sub-chunks: one for n <= 16,384, else
+    4,096, 16,384, ...) is bit-identical to tcl_score on device-resident inputs."""
     from paper_2604_12891_b200 import Model
-    d, w, f, l = _setup("tuning", n=20000)
+    d, w, f, l = _setup("tuning", n=n)
     m = Model(w, d)
     s_dev = _gpu_score(torch_cuda, m, f, l)
     s_host, idx, top = m.tcl_score_host(f, l, k=64)
