@@ -50,8 +50,11 @@ typedef enum {
 
 /* Arithmetic of the projections (in_proj, out_proj, encoder linears 2-3).
  *   FP32:      every GEMM in fp32 on the CUDA cores (FFMA); score within 1e-4*max(1,|ref|).
- *   BF16_PROJ: bf16 operands on the tcgen05 tensor cores with fp32 accumulation (TMEM);
- *              residual stream, norms, conv, scan and head stay fp32; within 2e-2*max(1,|ref|). */
+ *   BF16_PROJ: bf16 operands on the tcgen05 tensor cores with fp32 accumulation (TMEM); the
+ *              activations between kernels are bf16 (features, encoder hidden states, LN
+ *              outputs, x and SiLU(z), the gated scan output), SiLU / tanh / exp use the MUFU
+ *              approximations; the residual stream, norm statistics, conv, scan state and head
+ *              stay fp32; score within 2e-2*max(1,|ref|). */
 typedef enum { TCL_PREC_FP32 = 0, TCL_PREC_BF16_PROJ = 1 } tcl_precision;
 
 /* Discretisation of B ("a discretization method", reading R5):
