@@ -111,20 +111,6 @@ void launch_welford(const float* score, const int32_t* lens, int max_len, int64_
 void launch_mask_invalid(const int32_t* lens, int max_len, int64_t n, float* scores, cudaStream_t s);
 
 // ---- head: LN_f, masked mean, decoder (a9) ----------------------------------------------------
-struct HeadArgs {
-    const float* H; int ldh; int dm;
-    const float* lnf_w; const float* lnf_b; float eps;
-    const float* W1; const float* b1; int h1;
-    const float* W2; const float* b2; int h2;
-    const float* W3; const float* b3;
-    const int32_t* cu; const int32_t* lens; int max_len;
-    int64_t n;
-    float* scores;
-    DropoutCtx drop;
-    // MC accumulation (Welford) when mean != nullptr: pass index = drop.pass
-    float* mean; float* m2;
-};
-void launch_head(const HeadArgs& a, cudaStream_t s);
 void launch_mc_finalize(const float* m2, int64_t n, int passes, float* var, cudaStream_t s);
 
 // ---- top-k ------------------------------------------------------------------------------------

@@ -2,109 +2,15 @@
 // over the T real tokens (reading R9), decoder of three linears 64,32,1 with SiLU
 // after the first two (reading R1), plus the MC-dropout sites dec h1/h2 and the
 // per-candidate Welford accumulation over passes (reading R17).
-// One CTA (8 warps) per candidate; every reduction has a fixed order -> batch-invariant scores.
+// The pool kernels reduce each candidate's rows in order t = 0..T-1 (one warp per candidate); the
+// decoder runs as three small GEMMs over the candidates (gemm_simt.cu); every reduction has a
+// fixed order -> batch-invariant scores.
 #include <cuda_bf16.h>
 #include <math.h>
 
 #include "../kernels.h"
 
 namespace tcl {
-
-template <int PER>  // dm = 32 * PER
-__global__ void __launch_bounds__(256) k_head(HeadArgs a) {
-    constexpr int dm = 32 * PER;
-    __shared__ float red[8][dm];
-    __shared__ float pooled[dm];
-    __shared__ float hid1[256];
-    __shared__ float hid2[256];
-    const int64_t i = blockIdx.x;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int T = a.lens[i];
-    if (T < 1 || T > a.max_len) {  // reading R16: invalid length -> NaN (device flag set by pack)
-        if (threadIdx.x == 0) {
-            if (a.mean) { a.mean[i] = NAN; a.m2[i] = NAN; }
-            else a.scores[i] = NAN;
-        }
-        return;
-    }
-    const int64_t base = a.cu[i];
-    float acc[PER];
-#pragma unroll
-    for (int j = 0; j < PER; ++j) acc[j] = 0.0f;
-    for (int t = warp; t < T; t += 8) {
-        const float* hrow = a.H + (base + t) * a.ldh;
-        float v[PER];
-        float s = 0.f;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) { v[j] = hrow[lane + 32 * j]; s += v[j]; }
-        const float mean = warp_sum(s) * (1.0f / dm);
-        float q = 0.f;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) { float d = v[j] - mean; q = fmaf(d, d, q); }
-        const float rstd = rsqrtf(warp_sum(q) * (1.0f / dm) + a.eps);
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int c = lane + 32 * j;
-            acc[j] += (v[j] - mean) * rstd * __ldg(a.lnf_w + c) + __ldg(a.lnf_b + c);
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < PER; ++j) red[warp][lane + 32 * j] = acc[j];
-    __syncthreads();
-    const float invT = 1.0f / (float)T;
-    for (int c = threadIdx.x; c < dm; c += blockDim.x) {
-        float s = 0.f;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) s += red[w][c];
-        pooled[c] = s * invT;
-    }
-    __syncthreads();
-    // decoder layer 1 (dm -> h1), SiLU, dropout site 2
-    for (int j = warp; j < a.h1; j += 8) {
-        const float* wr = a.W1 + (int64_t)j * dm;
-        float s = 0.f;
-#pragma unroll
-        for (int k = 0; k < PER; ++k) s = fmaf(__ldg(wr + lane + 32 * k), pooled[lane + 32 * k], s);
-        s = warp_sum(s);
-        if (lane == 0) {
-            float v = silu(s + __ldg(a.b1 + j));
-            if (a.drop.enabled) v = dropout_keep(a.drop, j, 0, 2, i) ? v * a.drop.scale : 0.0f;
-            hid1[j] = v;
-        }
-    }
-    __syncthreads();
-    // decoder layer 2 (h1 -> h2), SiLU, dropout site 3
-    for (int j = warp; j < a.h2; j += 8) {
-        const float* wr = a.W2 + (int64_t)j * a.h1;
-        float s = 0.f;
-        for (int k = lane; k < a.h1; k += 32) s = fmaf(__ldg(wr + k), hid1[k], s);
-        s = warp_sum(s);
-        if (lane == 0) {
-            float v = silu(s + __ldg(a.b2 + j));
-            if (a.drop.enabled) v = dropout_keep(a.drop, j, 0, 3, i) ? v * a.drop.scale : 0.0f;
-            hid2[j] = v;
-        }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        float s = 0.f;
-        for (int k = lane; k < a.h2; k += 32) s = fmaf(__ldg(a.W3 + k), hid2[k], s);
-        s = warp_sum(s) + __ldg(a.b3);
-        if (lane == 0) {
-            if (a.mean) {  // Welford over passes (pass = a.drop.pass)
-                const int p = a.drop.pass;
-                const float m_old = p == 0 ? 0.0f : a.mean[i];
-                const float q_old = p == 0 ? 0.0f : a.m2[i];
-                const float delta = s - m_old;
-                const float m_new = m_old + delta / (float)(p + 1);
-                a.mean[i] = m_new;
-                a.m2[i] = q_old + delta * (s - m_new);
-            } else {
-                a.scores[i] = s;
-            }
-        }
-    }
-}
 
 // LN_f of every real row and the masked mean over the candidate's T rows; one warp per candidate
 // (8 candidates per CTA), rows summed in order t = 0..T-1 -> batch-invariant.
@@ -241,22 +147,6 @@ __global__ void k_mask_invalid(const int32_t* __restrict__ lens, int max_len, in
 void launch_mask_invalid(const int32_t* lens, int max_len, int64_t n, float* scores, cudaStream_t s) {
     if (n == 0) return;
     k_mask_invalid<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lens, max_len, n, scores);
-}
-
-void launch_head(const HeadArgs& a, cudaStream_t s) {
-    if (a.n == 0) return;
-    dim3 grid((unsigned)a.n);
-    switch (a.dm / 32) {
-        case 1: k_head<1><<<grid, 256, 0, s>>>(a); break;
-        case 2: k_head<2><<<grid, 256, 0, s>>>(a); break;
-        case 3: k_head<3><<<grid, 256, 0, s>>>(a); break;
-        case 4: k_head<4><<<grid, 256, 0, s>>>(a); break;
-        case 5: k_head<5><<<grid, 256, 0, s>>>(a); break;
-        case 6: k_head<6><<<grid, 256, 0, s>>>(a); break;
-        case 7: k_head<7><<<grid, 256, 0, s>>>(a); break;
-        case 8: k_head<8><<<grid, 256, 0, s>>>(a); break;
-        default: break;
-    }
 }
 
 __global__ void k_mc_finalize(const float* __restrict__ m2, int64_t n, int passes,
