@@ -50,6 +50,106 @@ __global__ void __launch_bounds__(1024) k_topk_chunk(const float* __restrict__ s
     for (int j = threadIdx.x; j < k; j += blockDim.x) out[(int64_t)blockIdx.x * k + j] = sk[j];
 }
 
+// k <= 256: each CTA takes a chunk of up to 8,192 keys and selects its k-th largest key by an
+// MSB-first radix select (8-bit digits; shared-memory histograms; stops once the boundary digit
+// holds exactly the keys still needed), gathers the keys above it and sorts only those k keys -- far
+// fewer barrier rounds than a full bitonic sort of the chunk.  One CTA finishes a tuning round
+// (~4,096 candidates); 65,536 take two rounds (8 CTAs, then 1).  Keys are unique except the 0
+// padding, so the selection is exact and integer-only (bit-exact).
+template <bool FROM_SCORES>
+__global__ void __launch_bounds__(1024) k_topk_radix(const float* __restrict__ scores,
+                                                     const u64* __restrict__ keys_in, int64_t count,
+                                                     int64_t index_base, int k, u64* __restrict__ out) {
+    constexpr int PER = 8;
+    __shared__ uint32_t hist[256];
+    __shared__ u64 sel[256];
+    __shared__ u64 s_prefix;
+    __shared__ int s_kk, s_done, s_ngt;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t lo = (int64_t)blockIdx.x * (PER * 1024);
+    out += (int64_t)blockIdx.x * k;
+    u64 v[PER];
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int64_t i = lo + tid + (int64_t)j * 1024;
+        v[j] = i < count ? (FROM_SCORES ? make_key(scores[i], (uint32_t)(index_base + i)) : keys_in[i]) : 0ull;
+    }
+    u64 prefix = 0;
+    int kk = k, done = 0;
+    for (int byte = 7; byte >= 0 && !done; --byte) {
+        const u64 hmask = byte == 7 ? 0ull : (~0ull << (8 * (byte + 1)));
+        if (tid < 256) hist[tid] = 0;
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if ((v[j] & hmask) == prefix) atomicAdd(&hist[(uint32_t)(v[j] >> (8 * byte)) & 0xFFu], 1u);
+        __syncthreads();
+        if (tid < 32) {
+            uint32_t c[8], sum = 0;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { c[q] = hist[8 * lane + q]; sum += c[q]; }
+            uint32_t incl = sum;   // keys in digits >= 8 lane
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_down_sync(0xffffffffu, incl, o);
+                if (lane + o < 32) incl += t;
+            }
+            const uint32_t excl = incl - sum;   // keys in digits above this lane's
+            if (excl < (uint32_t)kk && (uint32_t)kk <= incl) {
+                uint32_t run = excl;
+#pragma unroll
+                for (int q = 7; q >= 0; --q) {
+                    if (run + c[q] >= (uint32_t)kk) {
+                        s_prefix = prefix | ((u64)(8 * lane + q) << (8 * byte));
+                        s_kk = kk - (int)run;
+                        s_done = (c[q] == (uint32_t)(kk - (int)run)) ? 1 : 0;   // the whole bin is taken
+                        break;
+                    }
+                    run += c[q];
+                }
+            }
+        }
+        __syncthreads();
+        prefix = s_prefix;
+        kk = s_kk;
+        done = s_done;
+    }
+    // threshold: keys whose top bytes match `prefix` on the resolved digits (done) or equal it
+    if (tid == 0) s_ngt = 0;
+    __syncthreads();
+    if (done) {   // every key >= prefix is selected (exactly k of them)
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (v[j] >= prefix) sel[atomicAdd(&s_ngt, 1)] = v[j];
+        __syncthreads();
+    } else {      // prefix is the k-th key itself; kk copies of it are needed (only 0 repeats)
+#pragma unroll
+        for (int j = 0; j < PER; ++j)
+            if (v[j] > prefix) sel[atomicAdd(&s_ngt, 1)] = v[j];
+        __syncthreads();
+        if (tid < kk) sel[k - kk + tid] = prefix;
+        __syncthreads();
+    }
+    // sort the k selected keys descending (bitonic over the next power of two, 0-padded)
+    int K2 = 1;
+    while (K2 < k) K2 <<= 1;
+    if (tid >= k && tid < K2) sel[tid] = 0ull;
+    __syncthreads();
+    for (int size = 2; size <= K2; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (tid < K2 / 2) {
+                const int a = 2 * stride * (tid / stride) + (tid % stride);
+                const int b = a + stride;
+                const bool desc = (a & size) == 0;
+                const u64 x = sel[a], y = sel[b];
+                if ((x < y) == desc) { sel[a] = y; sel[b] = x; }
+            }
+            __syncthreads();
+        }
+    }
+    if (tid < k) out[tid] = sel[tid];
+}
+
 __global__ void k_topk_decode(const u64* __restrict__ keys, int k, int64_t* __restrict__ idx,
                               float* __restrict__ score) {
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -91,6 +191,28 @@ static int chunk_for(int k) { return k <= 512 ? 2048 : (k <= 1024 ? 4096 : kTopk
 static int tournament(const float* scores, const u64* keys, int64_t count, int k,
                       int64_t index_base, u64* out, u64* tmp, cudaStream_t s) {
     int launched = 0;
+    if (k <= 256) {   // radix-select rounds over 8,192-key chunks until one chunk remains
+        const int64_t blocks0 = (count + kTopkChunk - 1) / kTopkChunk;
+        u64* rb[2] = {tmp, tmp + blocks0 * k};
+        int w = 0;
+        const u64* src = keys;
+        bool from_scores = scores != nullptr;
+        int64_t cur = count;
+        for (;;) {
+            int64_t blocks = (cur + kTopkChunk - 1) / kTopkChunk;
+            if (blocks < 1) blocks = 1;
+            u64* dst = blocks == 1 ? out : rb[w];
+            if (from_scores) k_topk_radix<true><<<(unsigned)blocks, 1024, 0, s>>>(scores, nullptr, cur, index_base, k, dst);
+            else k_topk_radix<false><<<(unsigned)blocks, 1024, 0, s>>>(nullptr, src, cur, 0, k, dst);
+            ++launched;
+            if (blocks == 1) break;
+            cur = blocks * k;
+            src = dst;
+            w ^= 1;
+            from_scores = false;
+        }
+        return launched;
+    }
     // a set that fits one CTA's chunk is selected in a single round (no cross-CTA tournament)
     const int64_t need = count > k ? count : k;   // the chunk must also hold the k outputs
     const int C = need <= 2048 ? 2048 : need <= 4096 ? 4096 : need <= kTopkChunk ? kTopkChunk : chunk_for(k);
