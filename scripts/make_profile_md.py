@@ -36,7 +36,7 @@ def main():
     parts.append(run("launches", os.path.join(OUT, "launches_official.csv")))
     parts.append("## Per-kernel full captures\n")
     reps = sorted(f for f in os.listdir(OUT) if f.startswith("prof_official_") and f.endswith(".ncu-rep"))
-    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_simt", "k_topk_chunk", "k_pool_bf16", "k_pack"]
+    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_simt", "k_topk_radix", "k_pool_bf16", "k_pack"]
     reps.sort(key=lambda f: next((i for i, k in enumerate(order) if k in f), 99))
     for f in reps:
         parts.append(run("report", os.path.join(OUT, f)))
