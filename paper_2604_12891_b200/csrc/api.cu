@@ -270,7 +270,8 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
         const int nt_in = 2 * di / m->bn_in;
         if (nt_in == 2 || nt_in == 4)
-            ok = ok && make_tmap_bf16(&w.tmAbS, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128 / nt_in);
+            ok = ok && make_tmap_bf16(&w.tmAbS, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128 / nt_in) &&
+                 make_tmap_bf16(&w.tmAbS2, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 64);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
@@ -614,11 +615,17 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             // the fused mixer's gate SiLU(z) is applied here (HBM-bound epilogue, idle SFU) instead of
             // in the SFU-bound scan; the warp-specialised variant still gates z itself
             p.silu_from = (mixer_kind_env() == 1 && di >= 128) ? 0 : di;
-            // cluster multicast of A across the N-tile CTAs: correct but measured slower (1.40 vs
-            // 0.81 ms at `large`: 4 KB slices + cluster-coupled stalls), so opt-in only
-            static const int use_mc = [] { const char* v = getenv("TCL_MCAST"); return (v && v[0] == '1') ? 1 : 0; }();
-            p.mcast = use_mc && (p.n_tiles == 2 || p.n_tiles == 4);
-            if ((e = launch_gemm_tc(p.mcast ? w.tmAbS : w.tmAb, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
+            static const int nostore = [] { const char* v = getenv("TCL_DIAG_NOSTORE"); return v ? atoi(v) : 0; }();
+            p.diag_nostore = nostore;
+            // A tiles shared by TMA multicast inside clusters of 2 CTAs (N tiles 2j, 2j+1 of the same
+            // row tile; each CTA fetches 64 of the 128 rows): the read side is bound by the L2->SM
+            // traffic of the 4x re-read A tile (measured 0.60 ms with the stores disabled), and
+            // pairs halve it: 0.725 -> 0.666 ms at `large`.  TCL_MCAST=1: clusters of all 4 N
+            // tiles (1.16 ms: cluster-coupled stalls); TCL_MCAST=0: no multicast.
+            static const int use_mc = [] { const char* v = getenv("TCL_MCAST"); return v ? atoi(v) : 2; }();
+            p.mcast = (use_mc == 1 || use_mc == 2) && (p.n_tiles == 2 || p.n_tiles == 4) ? use_mc : 0;
+            const CUtensorMap& amap = p.mcast == 2 ? w.tmAbS2 : p.mcast ? w.tmAbS : w.tmAb;
+            if ((e = launch_gemm_tc(amap, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "in_proj");
             ++nl;
             if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;

@@ -100,6 +100,7 @@ struct Workspace {
     float* Lat = nullptr;         // [rows][ad_ld] SiLU(V h^KB + c), columns >= a stay zero
     float* pooled_k = nullptr;    // [cap_n][dm]
     float* dh1k = nullptr;        // [cap_n][h1]
+    CUtensorMap tmAbS2;                                // in_proj A half-slices for 2-CTA cluster multicast (box {64, 64})
     CUtensorMap tmAbS;                                 // in_proj A slices for cluster multicast (box {64, 128/n_tiles})                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
     std::vector<void*> allocs;
 };

@@ -131,8 +131,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
                     } else {  // this CTA fetches 128/CL rows of the A k-block for the whole cluster
                         constexpr int SL = kBM / CL;
-                        tc::tma_load_2d_mcast(sA + stage * kABytes + n_tile * SL * 128, &tmA, kb * 64,
-                                              m * kBM + n_tile * SL, &full[stage], (uint16_t)((1u << CL) - 1));
+                        const int cr = (int)tc::cluster_ctarank();   // this CTA's slice of the k-block
+                        tc::tma_load_2d_mcast(sA + stage * kABytes + cr * SL * 128, &tmA, kb * 64,
+                                              m * kBM + cr * SL, &full[stage], (uint16_t)((1u << CL) - 1));
                     }
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
@@ -253,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         if (k & 1) {
                             tc::fence_proxy_async();
                             __syncwarp();
-                            if (lane == 0) {
+                            if (lane == 0 && !p.diag_nostore) {
                                 asm volatile(
                                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                                     ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(n_tile * BN + (c - 1) * 32),
@@ -450,6 +451,7 @@ static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const 
     if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
     if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
     if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
+    if (p.mcast == 2 && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
     if (p.mcast && p.n_tiles == 4) return launch_impl<BN, KB, 0, 4>(a, b, c, p, grid, s);
     if (p.mcast && p.n_tiles == 2) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
     return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);

@@ -23,6 +23,7 @@ struct TcGemmParams {
     // TC_EPI_RESID_LN: H = (residual ? H : 0) + acc (+ bias); out = bf16(LN(H) * g + b)
     float* H; int ldh; int residual;
     int skip_h_store;
+    int diag_nostore;            // profiling only: skip the output stores
     int silu_from;               // EPI_BF16 without bias: columns >= silu_from (> 0) leave as SiLU(acc)
                                  // (in_proj: the mixer's gate SiLU(z) formed in this HBM-bound epilogue)
     int mcast;                   // EPI_BF16, n_tiles in {2, 4}: the n_tiles CTAs of a cluster share each
