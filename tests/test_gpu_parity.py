@@ -212,7 +212,8 @@ def _topk_gpu(torch, m, s, k, index_base=0):
 
 
 @pytest.mark.parametrize("n,k", [(1, 1), (100, 16), (8192, 64), (8193, 64), (65536, 64),
-                                 (300000, 1024), (50, 64), (20000, 4096)])
+                                 (300000, 1024), (50, 64), (20000, 4096),
+                                 (8192, 256), (100000, 256), (100000, 257), (1000000, 64)])
 def test_topk_bitexact_vs_stable_sort(torch_cuda, n, k):
     from paper_2604_12891_b200 import Model
     d, w, _, _ = _setup("tiny", n=2)
