@@ -58,16 +58,6 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-// Accurate e^x - 1 (x2 = x log2 e): the degree-6 series where Ab - 1 would cancel (|x2| < 0.25, as
-// mixer.cu's fp32 scan), selected without a branch: |Delta A| straddles the threshold across the
-// states of one warp, so a branch would run both paths serially anyway.
-__device__ __forceinline__ float expm1_acc(float x2, float Ab) {
-    const float x = x2 * kLn2;
-    const float ser = x * fmaf(x, fmaf(x, fmaf(x, fmaf(x, fmaf(x, 1.0f / 720, 1.0f / 120), 1.0f / 24),
-                                                1.0f / 6), 0.5f), 1.0f);
-    return fabsf(x2) < 0.25f ? ser : Ab - 1.0f;
-}
-
 // softplus(v) = max(v, 0) + log1p(y), y = e^{-|v|} in (0, 1] (reading R13): y on MUFU.EX2 (relative
 // error ~2^-22), log1p(y) = y * P6(y) (Chebyshev fit of log1p(y)/y on [0, 1], relative error
 // 3.1e-6 in fp32 Horner form) -- about a tenth of log1pf(expf(v))'s instructions; the resulting
@@ -81,6 +71,21 @@ __device__ __forceinline__ float softplus_f32(float v) {
     p = fmaf(p, y, -0.49982548f);
     p = fmaf(p, y, 0.99999708f);
     return fmaf(y, p, fmaxf(v, 0.0f));
+}
+
+// Accurate e^x - 1 for a pair of states (x2 = x log2 e): the degree-6 series where Ab - 1 would
+// cancel (|x2| < 0.25, as mixer.cu's fp32 scan), as a packed FFMA2 / FMUL2 Horner chain with a
+// per-lane select (no branch: |Delta A| straddles the threshold across the states of one warp).
+__device__ __forceinline__ float2 expm1_acc2(float2 x2, float2 Ab) {
+    const float2 x = __fmul2_rn(x2, make_float2(kLn2, kLn2));
+    float2 p = __ffma2_rn(x, make_float2(1.0f / 720, 1.0f / 720), make_float2(1.0f / 120, 1.0f / 120));
+    p = __ffma2_rn(p, x, make_float2(1.0f / 24, 1.0f / 24));
+    p = __ffma2_rn(p, x, make_float2(1.0f / 6, 1.0f / 6));
+    p = __ffma2_rn(p, x, make_float2(0.5f, 0.5f));
+    p = __ffma2_rn(p, x, make_float2(1.0f, 1.0f));
+    const float2 ser = __fmul2_rn(x, p);
+    const float2 am1 = __fadd2_rn(Ab, make_float2(-1.0f, -1.0f));
+    return make_float2(fabsf(x2.x) < 0.25f ? ser.x : am1.x, fabsf(x2.y) < 0.25f ? ser.y : am1.y);
 }
 
 template <int DI, int N, int R, int DC, int DISC>
@@ -109,11 +114,11 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
 #pragma unroll
     for (int r = 0; r < R; ++r) wdt[r] = __ldg(a.W_dt + d * R + r);
     const float bdt = __ldg(a.b_dt + d);
-    float A2[N], iA[N];
+    float2 A2v[N / 2], iAv[N / 2];   // state pairs: packed fp32x2 arithmetic in the ZOH scan
 #pragma unroll
-    for (int n = 0; n < N; ++n) {
-        A2[n] = __ldg(a.A2 + d * N + n);
-        iA[n] = __ldg(a.invA + d * N + n);
+    for (int p = 0; p < N / 2; ++p) {
+        A2v[p] = __ldg(reinterpret_cast<const float2*>(a.A2 + d * N) + p);
+        iAv[p] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + p);
     }
     const float Dv = __ldg(a.Dv + d);
     const float bconv = __ldg(a.b_conv + d);
@@ -166,10 +171,10 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
     int buf = 0;
     int chunk = 0;
 
-    float s[N];
+    float2 sv[N / 2];
     float win[DC];
 #pragma unroll
-    for (int n = 0; n < N; ++n) s[n] = 0.0f;
+    for (int p = 0; p < N / 2; ++p) sv[p] = make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < DC; ++k) win[k] = 0.0f;
     while (r0 < r_end) {
@@ -251,7 +256,7 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
         for (int tt = 0; tt < tc; ++tt) {
             if ((starts >> tt) & 1u) {
 #pragma unroll
-                for (int n = 0; n < N; ++n) s[n] = 0.0f;
+                for (int p = 0; p < N / 2; ++p) sv[p] = make_float2(0.f, 0.f);
             }
             const float u = u_s[tt * L::kUld + d];
             const float dl = dl_s[tt * DI + d];
@@ -262,20 +267,34 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
             if (DISC == 1) {  // Euler-B
                 const float du = dl * u;
 #pragma unroll
-                for (int n = 0; n < N; ++n) {
-                    const float Ab = ex2(dl * A2[n]);
-                    s[n] = fmaf(Ab, s[n], du * Bt[n]);
-                    y = fmaf(Ct[n], s[n], y);
+                for (int p = 0; p < N / 2; ++p) {
+                    const float Ab0 = ex2(dl * A2v[p].x), Ab1 = ex2(dl * A2v[p].y);
+                    sv[p].x = fmaf(Ab0, sv[p].x, du * Bt[2 * p]);
+                    y = fmaf(Ct[2 * p], sv[p].x, y);
+                    sv[p].y = fmaf(Ab1, sv[p].y, du * Bt[2 * p + 1]);
+                    y = fmaf(Ct[2 * p + 1], sv[p].y, y);
                 }
-            } else {          // ZOH, accurate e^x - 1
+            } else {          // ZOH, accurate e^x - 1, state pairs in packed fp32x2 (FFMA2 / FMUL2)
+                const float2 dl2 = make_float2(dl, dl), u2 = make_float2(u, u);
+                float2 y2 = make_float2(0.f, 0.f);
+                const float4* B4 = reinterpret_cast<const float4*>(Bt);
+                const float4* C4 = reinterpret_cast<const float4*>(Ct);
 #pragma unroll
-                for (int n = 0; n < N; ++n) {
-                    const float x2 = dl * A2[n];
-                    const float Ab = ex2(x2);
-                    const float v = (Bt[n] * u) * iA[n];
-                    s[n] = fmaf(Ab, s[n], expm1_acc(x2, Ab) * v);
-                    y = fmaf(Ct[n], s[n], y);
+                for (int q = 0; q < N / 4; ++q) {
+                    const float4 b4 = B4[q], c4 = C4[q];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int p = 2 * q + h;
+                        const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
+                        const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+                        const float2 x2 = __fmul2_rn(dl2, A2v[p]);
+                        const float2 Ab = make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 v = __fmul2_rn(__fmul2_rn(bb, u2), iAv[p]);
+                        sv[p] = __ffma2_rn(Ab, sv[p], __fmul2_rn(expm1_acc2(x2, Ab), v));
+                        y2 = __ffma2_rn(cc, sv[p], y2);
+                    }
                 }
+                y = y2.x + y2.y;
             }
             y = fmaf(Dv, u, y);
             gout[(int64_t)tt * a.ldg] = y * silu(z);
