@@ -50,7 +50,7 @@ __global__ void __launch_bounds__(1024) k_topk_chunk(const float* __restrict__ s
     for (int j = threadIdx.x; j < k; j += blockDim.x) out[(int64_t)blockIdx.x * k + j] = sk[j];
 }
 
-// k <= 256: each CTA takes a chunk of up to 8,192 keys and selects its k-th largest key by an
+// k <= 1024: each CTA takes a chunk of up to 8,192 keys and selects its k-th largest key by an
 // MSB-first radix select (8-bit digits; shared-memory histograms; stops once the boundary digit
 // holds exactly the keys still needed), gathers the keys above it and sorts only those k keys -- far
 // fewer barrier rounds than a full bitonic sort of the chunk.  One CTA finishes a tuning round
@@ -62,7 +62,7 @@ __global__ void __launch_bounds__(1024) k_topk_radix(const float* __restrict__ s
                                                      int64_t index_base, int k, u64* __restrict__ out) {
     constexpr int PER = 8;
     __shared__ uint32_t hist[256];
-    __shared__ u64 sel[256];
+    __shared__ u64 sel[1024];
     __shared__ u64 s_prefix;
     __shared__ int s_kk, s_done, s_ngt;
     const int tid = threadIdx.x, lane = tid & 31;
@@ -191,7 +191,7 @@ static int chunk_for(int k) { return k <= 512 ? 2048 : (k <= 1024 ? 4096 : kTopk
 static int tournament(const float* scores, const u64* keys, int64_t count, int k,
                       int64_t index_base, u64* out, u64* tmp, cudaStream_t s) {
     int launched = 0;
-    if (k <= 256) {   // radix-select rounds over 8,192-key chunks until one chunk remains
+    if (k <= 1024) {   // radix-select rounds over 8,192-key chunks until one chunk remains
         const int64_t blocks0 = (count + kTopkChunk - 1) / kTopkChunk;
         u64* rb[2] = {tmp, tmp + blocks0 * k};
         int w = 0;
