@@ -181,7 +181,9 @@ tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_w
  * beta1, beta2, eps (paper: Adam, lr 7e-4) and the LambdaRank scale sigma_rank (1).
  * tcl_train_step runs one step on a batch already on the device: feats/lens as tcl_score,
  * latency_dev [n] the measured latencies (> 0), group_offsets_dev [n_groups+1] int64 CSR groups
- * (one tuning task each; 2 <= members <= max_group <= 4096), the loss
+ * (one tuning task each; 2 <= members <= max_group <= 4096; a group outside that range, or outside
+ * [0, n), contributes nothing and makes tcl_sync_error return TCL_ESHAPE; candidates outside every
+ * group get a zero score gradient), the loss
  *   L = mean_g sum_{y_i > y_j} |G_i - G_j| |1/D_i - 1/D_j| log2(1 + e^{-sigma (s_i - s_j)}),
  *   y = min latency of the group / latency, G = (2^y - 1) / maxDCG, D = log2(1 + predicted rank)
  * (fp32) goes to loss_dev [1] (may be NULL), the gradient of every weight (canonical blob layout)
@@ -230,6 +232,16 @@ tcl_status tcl_rdu_select(tcl_model* model, const float* pool_scores_dev, const 
                           int64_t n_pool, const float* labeled_scores_dev, int64_t n_labeled, int32_t n_ops,
                           int32_t budget_total, int64_t* selected_idx_dev, int32_t* n_selected_dev,
                           void* stream);
+
+/* Per-model options.
+ *   TCL_OPT_GRAPHS (default 1): replay the launch sequence of a repeated call (same pointers,
+ *     sizes, seeds and stream-independent arguments: tcl_score, tcl_score_mc, tcl_topk,
+ *     tcl_train_step) from a CUDA graph captured on its second occurrence; 0 launches every
+ *     kernel directly.  Results are bit-identical either way (tested); graphs only remove the
+ *     host launch cost and the inter-kernel gaps of the small, launch-bound configurations.
+ * Returns TCL_EINVAL for an unknown option or value. */
+typedef enum { TCL_OPT_GRAPHS = 1 } tcl_option;
+tcl_status tcl_set_option(tcl_model* model, int32_t option, int64_t value);
 
 /* Synchronise `stream`, then return (and clear) the sticky device error of the model. */
 tcl_status tcl_sync_error(tcl_model* model, void* stream);

@@ -164,11 +164,8 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
     cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
     m->nxp = round_up(R + 2 * N, 8);
     m->rp = R <= 16 ? 16 : 32;
-    m->bn_in = std::min(128, 2 * di);  // 4 N tiles at di = 256: B slice 64 KB, 8-stage A ring
-    if (const char* v = getenv("TCL_BN_IN")) {   // A/B experiments only
-        const int b = atoi(v);
-        if ((b == 128 || b == 256) && b <= 2 * di) m->bn_in = b;
-    }
+    // 4 N tiles at di = 256: B slice 64 KB, 8-stage A ring (BN = 256 measured slower)
+    m->bn_in = std::min(128, 2 * di);
     HostW h = host_offsets(d, wh);
     if ((st = upload_bf16(m, h.W1, e1, d.d_in, e1, kXld, &m->W1b)) != TCL_OK) return st;
     if ((st = upload_bf16(m, h.W2, e2, e1, e2, e1, &m->W2b)) != TCL_OK) return st;
@@ -270,13 +267,13 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
         const int nt_in = 2 * di / m->bn_in;
         if (nt_in == 2 || nt_in == 4)
-            ok = ok && make_tmap_bf16(&w.tmAbS, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 128 / nt_in) &&
-                 make_tmap_bf16(&w.tmAbS2, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 64);
+            ok = ok && make_tmap_bf16(&w.tmAbS2, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 64);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
     w.cap_n = chunk_n;
     w.rows = rows;
+    ++m->ws_gen;   // captured graphs that baked in the old buffers are stale now
     return TCL_OK;
 }
 
@@ -378,8 +375,7 @@ struct F32Run {
                              /*gemm_epilogue_order=*/true); ++m->launches;
         }
         gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
-        static const bool fused = [] { const char* v = getenv("TCL_F32_MIXER"); return !(v && v[0] == '0'); }();
-        if (fused && mixer_f32_supported(di, N, R, d.d_conv)) {
+        if (mixer_f32_supported(di, N, R, d.d_conv)) {
             // conv + x_proj + dt_proj + scan in one kernel (mixer_f32.cu)
             ProfScope ps(m, TCL_PROF_MIXER, s);
             MixerF32Args a{};
@@ -510,8 +506,7 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     float* E2 = w.Delta;
     r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
     r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
-    static const bool fuse_env = [] { const char* v = getenv("TCL_F32_FUSE_LN"); return !(v && v[0] == '0'); }();
-    r.fuse_ln = fuse_env && dm == 128 && d.n_layer > 0;
+    r.fuse_ln = dm == 128 && d.n_layer > 0;
     if (r.fuse_ln) {
         F32Run r0 = r;
         r0.ln_g = m->wp.layers[0].ln_w;
@@ -533,15 +528,6 @@ static tcl_status debug_sync(const char* where, cudaStream_t s) {
     if (e != cudaSuccess) return cuda_error(e, where);
     fprintf(stderr, "[tcl] %s ok\n", where);
     return TCL_OK;
-}
-
-// TCL_MIXER=ws selects the warp-specialised mixer variant (mixer_ws.cu) on the bf16 path
-static int mixer_kind_env() {
-    static const int k = [] {
-        const char* v = getenv("TCL_MIXER");
-        return (v && std::string(v) == "ws") ? 1 : 0;
-    }();
-    return k;
 }
 
 // The bf16 projection path (precision == TCL_PREC_BF16_PROJ): tcgen05 GEMMs with fused
@@ -573,8 +559,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
     auto kb_of = [](int K) { return (K + 63) / 64; };
     {
         ProfScope ps(m, TCL_PROF_ENCODER, s);
-        static const bool fused12 = [] { const char* v = getenv("TCL_ENC12"); return !(v && v[0] == '0'); }();
-        if (fused12 && enc12_supported(e1, e2, d.d_in)) {
+        if (enc12_supported(e1, e2, d.d_in)) {
             // linears 1 and 2 chained: E1 stays in shared memory (gemm_tc_enc.cu)
             EncParams ep{};
             ep.p_rows = P; ep.b1 = m->wp.enc_b1; ep.b2 = m->wp.enc_b2; ep.drop = drop;
@@ -613,18 +598,15 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
             // the fused mixer's gate SiLU(z) is applied here (HBM-bound epilogue, idle SFU) instead of
-            // in the SFU-bound scan; the warp-specialised variant still gates z itself
-            p.silu_from = (mixer_kind_env() == 1 && di >= 128) ? 0 : di;
-            static const int nostore = [] { const char* v = getenv("TCL_DIAG_NOSTORE"); return v ? atoi(v) : 0; }();
-            p.diag_nostore = nostore;
+            // in the SFU-bound scan
+            p.silu_from = di;
             // A tiles shared by TMA multicast inside clusters of 2 CTAs (N tiles 2j, 2j+1 of the same
             // row tile; each CTA fetches 64 of the 128 rows): the read side is bound by the L2->SM
             // traffic of the 4x re-read A tile (measured 0.60 ms with the stores disabled), and
-            // pairs halve it: 0.725 -> 0.666 ms at `large`.  TCL_MCAST=1: clusters of all 4 N
-            // tiles (1.16 ms: cluster-coupled stalls); TCL_MCAST=0: no multicast.
-            static const int use_mc = [] { const char* v = getenv("TCL_MCAST"); return v ? atoi(v) : 2; }();
-            p.mcast = (use_mc == 1 || use_mc == 2) && (p.n_tiles == 2 || p.n_tiles == 4) ? use_mc : 0;
-            const CUtensorMap& amap = p.mcast == 2 ? w.tmAbS2 : p.mcast ? w.tmAbS : w.tmAb;
+            // pairs halve it: 0.725 -> 0.666 ms at `large` (clusters of all 4 N tiles: 1.16 ms,
+            // cluster-coupled stalls).
+            p.mcast = (p.n_tiles == 2 || p.n_tiles == 4) ? 1 : 0;
+            const CUtensorMap& amap = p.mcast ? w.tmAbS2 : w.tmAb;
             if ((e = launch_gemm_tc(amap, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
                 return cuda_error(e, "in_proj");
             ++nl;
@@ -639,10 +621,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
             a.cu = w.cu; a.lens = lens; a.n = n;
             a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
-            static const int diag = [] { const char* v = getenv("TCL_MIXER_DIAG"); return v ? atoi(v) : 0; }();
-            a.diag = diag;
-            const int mixer_kind = mixer_kind_env();
-            e = (mixer_kind == 1 && di >= 128) ? launch_mixer_ws(a, m->num_sms, s) : launch_mixer_fused(a, m->num_sms, s);
+            e = launch_mixer_fused(a, m->num_sms, s);
             if (e != cudaSuccess) return cuda_error(e, "mixer");
             ++nl;
             if (debug_sync("mixer", s) != TCL_OK) return TCL_ECUDA;
@@ -1036,6 +1015,16 @@ tcl_status tcl_sync_error(tcl_model* m, void* stream) {
 
 int64_t tcl_launch_count(const tcl_model* m) { return m ? m->launches : 0; }
 
+tcl_status tcl_set_option(tcl_model* m, int32_t option, int64_t value) {
+    if (!m) return set_error(TCL_EINVAL, "null model");
+    if (option == TCL_OPT_GRAPHS) {
+        if (value != 0 && value != 1) return set_error(TCL_EINVAL, "TCL_OPT_GRAPHS takes 0 or 1");
+        m->use_graphs = (int)value;
+        return TCL_OK;
+    }
+    return set_error(TCL_EINVAL, "unknown option");
+}
+
 tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t rows, int64_t cols) {
     if (!m || !name || !out || rows < 0 || cols < 1) return set_error(TCL_EINVAL, "bad argument");
     CUDA_TRY(cudaSetDevice(m->device));
@@ -1340,8 +1329,8 @@ static tcl_status train_enqueue(tcl_model* m, const float* feats, const int32_t*
     fgemm(t.d1, h1, m->wp.dec_W2, m->wp.dec_b2, t.d2, h1, h2, EPI_SILU, t.d2pre, true);
     fgemm(t.d2, h2, m->wp.dec_W3, m->wp.dec_b3, t.scores, h2, 1, EPI_NONE, nullptr, true);
     // ---- LambdaRank loss and dL/ds (Eq. 6)
-    cudaError_t e = launch_lambdarank(t.scores, latency, group_offsets, n_groups, max_group, t.sigma, t.ds, t.gloss,
-                                      t.loss, s);
+    cudaError_t e = launch_lambdarank(t.scores, latency, group_offsets, n_groups, max_group, n, t.sigma, t.ds,
+                                      t.gloss, t.loss, m->d_err, s);
     if (e != cudaSuccess) return cuda_error(e, "lambdarank");
     nl += 2;
     if (loss_dev) CUDA_TRY(cudaMemcpyAsync(loss_dev, t.loss, sizeof(float), cudaMemcpyDeviceToDevice, s));
@@ -1431,9 +1420,9 @@ static tcl_status train_enqueue(tcl_model* m, const float* feats, const int32_t*
 }
 
 // One training step.  The ~110 launches of a step are captured once into a CUDA graph and
-// replayed while the call signature (pointers, sizes, flags) is unchanged; the graph runs on a
-// private stream ordered after / before the caller's stream by events.  TCL_TRAIN_GRAPH=0 (or
-// per-stage profiling) launches directly.
+// replayed while the call signature (pointers, sizes, flags) and the workspace are unchanged; the
+// graph runs on a private stream ordered after / before the caller's stream by events.
+// tcl_set_option(TCL_OPT_GRAPHS, 0) (or per-stage profiling) launches directly.
 tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, const float* latency,
                           const int64_t* group_offsets, int64_t n_groups, int32_t max_group, int32_t apply_update,
                           float* loss_dev, void* stream) {
@@ -1445,10 +1434,12 @@ tcl_status tcl_train_step(tcl_model* m, const float* feats, const int32_t* lens,
     CUDA_TRY(cudaSetDevice(m->device));
     cudaStream_t s = (cudaStream_t)stream;
     if (apply_update) t.step += 1;
-    static const bool use_graph = [] { const char* v = getenv("TCL_TRAIN_GRAPH"); return !(v && v[0] == '0'); }();
-    if (!use_graph || m->prof_on)
+    if (!m->use_graphs || m->prof_on)
         return train_enqueue(m, feats, lens, n, latency, group_offsets, n_groups, max_group, apply_update, loss_dev, s);
-    const TrainState::Key key{feats, lens, latency, group_offsets, loss_dev, n, n_groups, max_group, apply_update ? 1 : 0};
+    // the graph bakes in workspace pointers (cu, X, row_cand): a workspace reallocation by a
+    // scoring call between steps (ws_gen) forces a re-capture
+    const TrainState::Key key{feats, lens, latency, group_offsets, loss_dev, n, n_groups, m->ws_gen, max_group,
+                              apply_update ? 1 : 0};
     if (!t.graph || !(t.key == key)) {
         if (t.graph) { cudaGraphExecDestroy(t.graph); t.graph = nullptr; }
         const int64_t before = m->launches;

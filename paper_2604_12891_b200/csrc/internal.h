@@ -54,11 +54,11 @@ struct TrainState {
     // CUDA graph of one step, replayed while the call signature is unchanged
     struct Key {
         const void *feats, *lens, *lat, *off, *loss;
-        int64_t n, n_groups;
+        int64_t n, n_groups, ws_gen;
         int max_group, apply;
         bool operator==(const Key& o) const {
             return feats == o.feats && lens == o.lens && lat == o.lat && off == o.off && loss == o.loss && n == o.n &&
-                   n_groups == o.n_groups && max_group == o.max_group && apply == o.apply;
+                   n_groups == o.n_groups && ws_gen == o.ws_gen && max_group == o.max_group && apply == o.apply;
         }
     } key{};
     cudaGraphExec_t graph = nullptr;
@@ -92,7 +92,7 @@ struct Workspace {
     __nv_bfloat16* Gb = nullptr;   // [rows][di]    gated scan output
     CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
     CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
-    CUtensorMap tmHf, tmAo;
+    CUtensorMap tmHf, tmAo;                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
     // KB + AC two-column model (fp32 path): the KB column's buffers and the lateral activations
     float* Hk = nullptr;          // [rows][dm]  KB residual stream
     float* E1k = nullptr;         // [rows][e1]  KB encoder hidden 1
@@ -101,7 +101,6 @@ struct Workspace {
     float* pooled_k = nullptr;    // [cap_n][dm]
     float* dh1k = nullptr;        // [cap_n][h1]
     CUtensorMap tmAbS2;                                // in_proj A half-slices for 2-CTA cluster multicast (box {64, 64})
-    CUtensorMap tmAbS;                                 // in_proj A slices for cluster multicast (box {64, 128/n_tiles})                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
     std::vector<void*> allocs;
 };
 
@@ -121,6 +120,8 @@ struct tcl_model {
     float* invA = nullptr;  // [n_layer][di][N]  1 / A
     int* d_err = nullptr;
     tcl::Workspace ws;
+    int64_t ws_gen = 0;     // bumped on every workspace (re)allocation (graph keys)
+    int use_graphs = 1;     // tcl_set_option(TCL_OPT_GRAPHS)
     unsigned long long* topk_tmp = nullptr;
     size_t topk_tmp_cap = 0;
     // multi-GPU

@@ -7,6 +7,14 @@
 
 namespace tcl {
 
+// Opt a kernel in to `smem` bytes of dynamic shared memory on the CURRENT device (cached per
+// device) and, if blocks_per_sm != nullptr, return its occupancy at `threads` threads per CTA.
+cudaError_t prepare_kernel_raw(const void* fn, int smem, int threads, int* blocks_per_sm);
+template <typename K>
+inline cudaError_t prepare_kernel(K* kern, int smem, int threads = 0, int* blocks_per_sm = nullptr) {
+    return prepare_kernel_raw(reinterpret_cast<const void*>(kern), smem, threads, blocks_per_sm);
+}
+
 // Device error bits (sticky, tcl_sync_error).
 enum : int { ERR_LEN = 1, ERR_TASK = 2 };
 
@@ -160,8 +168,12 @@ void launch_conv_bwd(const float* X, int ldx, const float* w, const float* b, in
                      const int32_t* lens, const int32_t* p_rows, int max_rows, float* part, size_t part_cap,
                      float* dw, float* db, cudaStream_t s);
 void launch_scan_bwd(const ScanBwdArgs& a, cudaStream_t s);
+// LambdaRank loss + dL/ds over CSR groups (reading R24).  dscores [n_total] is zeroed first; a
+// group with fewer than 2 or more than max_group members, or outside [0, n_total), contributes 0
+// and sets ERR_TASK in *err.
 cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64_t* off, int64_t n_groups,
-                              int max_group, float sigma, float* dscores, float* gloss, float* loss, cudaStream_t s);
+                              int max_group, int64_t n_total, float sigma, float* dscores, float* gloss, float* loss,
+                              int* err, cudaStream_t s);
 void launch_adam(float* w, const float* g, float* m, float* v, int64_t n, float lr, float b1, float b2, float eps,
                  int* step_dev, float* corr_dev, cudaStream_t s);
 void launch_refresh_w1(const float* W1, int e1, int d_in, int ldp, float* W1p, cudaStream_t s);

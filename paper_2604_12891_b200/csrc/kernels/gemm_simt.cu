@@ -299,14 +299,12 @@ __global__ void __launch_bounds__(256) k_gemm_simt128(GemmArgs a) {
 
 void launch_gemm_simt(const GemmArgs& a, cudaStream_t s) {
     if (a.max_rows <= 0) return;
-    static const int bk = [] { const char* v = getenv("TCL_SIMT_BK"); return (v && atoi(v) == 8) ? 8 : 16; }();
     const bool ln = a.epi == EPI_RESID_LN || a.epi == EPI_LN;
     if (ln && (a.N != 128 || a.wT || (a.K % 16) != 0 || (a.K2 % 16) != 0)) return;   // callers guarantee
     if (a.N >= 128 && !a.wT && (a.K % 16) == 0 && (a.K2 % 16) == 0) {
         dim3 grid2((a.max_rows + BM2 - 1) / BM2, (a.N + BN2 - 1) / BN2);
         if (a.K2 > 0) k_gemm_simt128<16, true><<<grid2, 256, 0, s>>>(a);
-        else if (bk == 16) k_gemm_simt128<16, false><<<grid2, 256, 0, s>>>(a);
-        else k_gemm_simt128<8, false><<<grid2, 256, 0, s>>>(a);
+        else k_gemm_simt128<16, false><<<grid2, 256, 0, s>>>(a);
         return;
     }
     dim3 grid((a.max_rows + BM - 1) / BM, (a.N + BN - 1) / BN);

@@ -17,6 +17,7 @@
 // warps 2..5 = epilogue (warp w drains TMEM lanes 32*(w%4) .. 32*(w%4)+31).
 #include <cuda_bf16.h>
 
+#include "../kernels.h"
 #include "../kernels_tc.h"
 #include "../tc_ptx.cuh"
 
@@ -254,7 +255,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         if (k & 1) {
                             tc::fence_proxy_async();
                             __syncwarp();
-                            if (lane == 0 && !p.diag_nostore) {
+                            if (lane == 0) {
                                 asm volatile(
                                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
                                     ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(n_tile * BN + (c - 1) * 32),
@@ -418,12 +419,8 @@ static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const
                                const TcGemmParams& p, int grid, cudaStream_t s) {
     const int smem = TcSmem<BN, KB, EPI>::kBytes;
     auto kern = k_gemm_tc<BN, KB, EPI, CL>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = prepare_kernel(kern, smem);
+    if (e != cudaSuccess) return e;
     if (CL == 1) {
         kern<<<grid, kThreads, smem, s>>>(a, b, c, p);
     } else {
@@ -451,9 +448,7 @@ static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const 
     if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
     if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
     if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
-    if (p.mcast == 2 && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
-    if (p.mcast && p.n_tiles == 4) return launch_impl<BN, KB, 0, 4>(a, b, c, p, grid, s);
-    if (p.mcast && p.n_tiles == 2) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
+    if (p.mcast && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
     return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);
 }
 

@@ -17,6 +17,7 @@
 // tanh form (h (1 + tanh h), h = v/2): the two SiLUs per E1/E2 element are the epilogue's cost.
 #include <cuda_bf16.h>
 
+#include "../kernels.h"
 #include "../kernels_tc.h"
 #include "../tc_ptx.cuh"
 
@@ -290,12 +291,8 @@ static cudaError_t launch_k(const CUtensorMap& x, const CUtensorMap& w1, const C
                             const CUtensorMap& e2, const EncParams& p, int num_sms, cudaStream_t s) {
     constexpr int smem = Smem<E1N, E2N>::kBytes;
     auto kern = k_enc12<E1N, E2N, DROP>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = prepare_kernel(kern, smem);
+    if (e != cudaSuccess) return e;
     kern<<<num_sms, kThreads, smem, s>>>(x, w1, w2, e2, p);
     return cudaGetLastError();
 }

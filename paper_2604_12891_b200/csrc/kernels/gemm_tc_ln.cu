@@ -16,6 +16,7 @@
 // of the previous version).
 #include <cuda_bf16.h>
 
+#include "../kernels.h"
 #include "../kernels_tc.h"
 #include "../tc_ptx.cuh"
 
@@ -303,12 +304,8 @@ template <int BN, int KB>
 static cudaError_t launch(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& h, const CUtensorMap& o,
                           const TcGemmParams& p, int num_sms, cudaStream_t s) {
     constexpr int smem = Smem<BN, KB>::kBytes;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_gemm_ln<BN, KB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
+    cudaError_t e = prepare_kernel(k_gemm_ln<BN, KB>, smem);
+    if (e != cudaSuccess) return e;
     k_gemm_ln<BN, KB><<<num_sms, kThreads, smem, s>>>(a, b, h, o, p);
     return cudaGetLastError();
 }

@@ -311,13 +311,9 @@ static cudaError_t launch_k(const MixerF32Args& a, int num_sms, cudaStream_t s) 
     constexpr int smem = Smem<DI, R + 2 * N>::kBytes;
     static_assert(smem <= 232448, "mixer_f32 shared memory");
     auto kern = k_mixer_f32<DI, N, R, 4, DISC>;
-    static int bps = 0;
-    if (!bps) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, DI, smem);
-        if (e != cudaSuccess || bps < 1) bps = 1;
-    }
+    int bps = 1;
+    cudaError_t e = prepare_kernel(kern, smem, DI, &bps);
+    if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * bps;
     if (grid > a.n) grid = a.n;
     kern<<<(unsigned)grid, DI, smem, s>>>(a);

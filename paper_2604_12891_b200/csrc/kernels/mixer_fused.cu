@@ -40,7 +40,7 @@ namespace tcl {
 
 constexpr int kTC = 16;  // tokens per chunk (= MMA M)
 
-template <int DI, int NXP, int OCC>
+template <int DI, int NXP>
 struct MixerSmem {
     static constexpr int kWxld = DI + 8;   // bf16 row stride of W_x (+16 B: conflict-free B fragments)
     static constexpr int kDbcld = NXP + 4;
@@ -51,10 +51,10 @@ struct MixerSmem {
     static constexpr int kDbc = kDl + kTC * DI * 4;                // float [16][NXP + 4]
     static constexpr int kUb = kDbc + kTC * kDbcld * 4;            // bf16  [16][DI + 8] (MMA A operand)
     static constexpr int kWx = kUb + kTC * kWxld * 2;              // bf16  [NXP][DI + 8]
-    static constexpr int kBar = OCC == 2 ? kWx + NXP * kWxld * 2 : kUb;  // 2 mbarriers
-    // candidate-start bits of the CTA's rows, 16 per chunk (OCC == 2 only; more chunks than this
-    // fall back to walking cu[] per chunk)
-    static constexpr int kStartWords = OCC == 2 ? 1024 : 0;
+    static constexpr int kBar = kWx + NXP * kWxld * 2;             // 2 mbarriers
+    // candidate-start bits of the CTA's rows, 16 per chunk (more chunks than this fall back to
+    // walking cu[] per chunk)
+    static constexpr int kStartWords = 1024;
     static constexpr int kStarts = kBar + 16;                      // u32 [kStartWords]
     static constexpr int kBytes = kStarts + 4 * kStartWords;
 };
@@ -92,20 +92,6 @@ __device__ __forceinline__ float softplus_fast(float v) {
     return fmaf(y, p, fmaxf(v, 0.0f));
 }
 
-// 2^x for a pair (x <= 0) on the FMA/ALU pipes (Cody-Waite + degree-3 near-minimax, rel. err 1e-4)
-__device__ __forceinline__ float2 exp2_poly_pair(float2 x) {
-    x.x = fmaxf(x.x, -125.0f);
-    x.y = fmaxf(x.y, -125.0f);
-    const float2 t = __fadd2_rn(x, make_float2(12582912.0f, 12582912.0f));
-    const float2 j = __fadd2_rn(t, make_float2(-12582912.0f, -12582912.0f));
-    const float2 f = __fadd2_rn(x, make_float2(-j.x, -j.y));
-    float2 p = __ffma2_rn(f, make_float2(0.05500858f, 0.05500858f), make_float2(0.24221037f, 0.24221037f));
-    p = __ffma2_rn(p, f, make_float2(0.6932829f, 0.6932829f));
-    p = __ffma2_rn(p, f, make_float2(1.0f, 1.0f));
-    return make_float2(__uint_as_float(__float_as_uint(p.x) + (__float_as_uint(t.x) << 23)),
-                       __uint_as_float(__float_as_uint(p.y) + (__float_as_uint(t.y) << 23)));
-}
-
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -114,12 +100,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0, int SU = 1>
-__global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
-    // OCC == 3: lean variant (W_x fragments from L1, no bf16 copy of u, W_dt per chunk) so that
-    // three CTAs fit per SM (<= 85 registers, <= 75 KB shared memory).
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int SU>
+__global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {
     constexpr int NW = DI / 32;
-    using L = MixerSmem<DI, NXP, OCC>;
+    using L = MixerSmem<DI, NXP>;
     extern __shared__ __align__(128) uint8_t msm[];
     __nv_bfloat16* xz_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kXZ);   // [2][16][2 DI]
     float* u_s = reinterpret_cast<float*>(msm + L::kU);                       // [16][DI + 4]
@@ -134,20 +118,16 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     const int g = lane >> 2, tq = lane & 3;
 
     // ---- once per CTA: W_x into padded smem, W_dt fragments into registers, per-channel constants
-    if (OCC == 2) {
-        for (int idx = d; idx < NXP * DI / 8; idx += DI) {
-            const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
-            *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
-                __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
-        }
+    for (int idx = d; idx < NXP * DI / 8; idx += DI) {
+        const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
+        *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
+            __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
     }
     constexpr int NT_DT = DI / 8 / NW;  // dt_proj n-tiles per warp
-    // W_dt fragments / b_dt held in registers for the whole launch (OCC == 2), or re-read from L1
-    // per chunk (OCC == 3)
-    constexpr bool kWdtReg = OCC == 2;
+    // W_dt fragments / b_dt held in registers for the whole launch
     uint32_t wdt[NT_DT][RP / 16][2];
 #pragma unroll
-    for (int j = 0; j < NT_DT && kWdtReg; ++j) {
+    for (int j = 0; j < NT_DT; ++j) {
         const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
 #pragma unroll
         for (int ks = 0; ks < RP / 16; ++ks) {
@@ -157,7 +137,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     }
     float2 bdt[NT_DT];  // dt_proj bias of this thread's output columns
 #pragma unroll
-    for (int j = 0; j < NT_DT && kWdtReg; ++j) bdt[j] = __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
+    for (int j = 0; j < NT_DT; ++j) bdt[j] = __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
     float2 A2[N / 2], iA[N / 2];
 #pragma unroll
     for (int n = 0; n < N / 2; ++n) {
@@ -267,9 +247,9 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
             asm("tanh.approx.f32 %0, %1;" : "=f"(th) : "f"(h));
             const float u = fmaf(h, th, h);
             u_s[tt * L::kUld + d] = u;
-            if (OCC == 2) u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
+            u_b[tt * L::kWxld + d] = __float2bfloat16_rn(u);
         };
-        if (a.diag != 2 && a.diag != 3) {
+        {
             if (tc == kTC) {
 #pragma unroll
                 for (int tt = 0; tt < kTC; ++tt) conv_tok(tt);
@@ -283,40 +263,20 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 2. x_proj on the tensor cores: dbc[16][NXP] = u[16][DI] . W_x^T
-        for (int nt = warp; nt < (a.diag == 2 ? 0 : NXP / 8); nt += NW) {
+        for (int nt = warp; nt < NXP / 8; nt += NW) {
             float acc[4] = {0.f, 0.f, 0.f, 0.f};
-            const __nv_bfloat16* wrow = OCC == 2 ? wx_s + (nt * 8 + g) * L::kWxld : a.Wx_b + (int64_t)(nt * 8 + g) * DI;
-            if (OCC == 2) {
-                // fragments by ldmatrix: A (16 x 16 of u) one x4 per k-step, B (8 rows of W_x) one
-                // x4 per two k-steps
-                const uint32_t a_addr = tc::smem_u32(u_b + (lane & 15) * L::kWxld + 8 * (lane >> 4));
-                const uint32_t b_addr = tc::smem_u32(wx_s + (nt * 8 + (lane & 7)) * L::kWxld + 8 * (lane >> 3));
+            // fragments by ldmatrix: A (16 x 16 of u) one x4 per k-step, B (8 rows of W_x) one x4
+            // per two k-steps
+            const uint32_t a_addr = tc::smem_u32(u_b + (lane & 15) * L::kWxld + 8 * (lane >> 4));
+            const uint32_t b_addr = tc::smem_u32(wx_s + (nt * 8 + (lane & 7)) * L::kWxld + 8 * (lane >> 3));
 #pragma unroll 4
-                for (int k0 = 0; k0 < DI; k0 += 32) {
-                    uint32_t af[4], af2[4], bf[4];
-                    ldsm_x4(af, a_addr + k0 * 2);
-                    ldsm_x4(af2, a_addr + (k0 + 16) * 2);
-                    ldsm_x4(bf, b_addr + k0 * 2);
-                    mma_16816(acc, af, bf[0], bf[1]);
-                    mma_16816(acc, af2, bf[2], bf[3]);
-                }
-            }
-#pragma unroll 4
-            for (int k0 = 0; k0 < (OCC == 2 ? 0 : DI); k0 += 16) {
-                uint32_t af[4];
-                {
-                    const float2 p0 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 2 * tq);
-                    const float2 p1 = *reinterpret_cast<const float2*>(u_s + (g + 8) * L::kUld + k0 + 2 * tq);
-                    const float2 p2 = *reinterpret_cast<const float2*>(u_s + g * L::kUld + k0 + 8 + 2 * tq);
-                    const float2 p3 = *reinterpret_cast<const float2*>(u_s + (g + 8) * L::kUld + k0 + 8 + 2 * tq);
-                    af[0] = pk_bf16(p0.x, p0.y);
-                    af[1] = pk_bf16(p1.x, p1.y);
-                    af[2] = pk_bf16(p2.x, p2.y);
-                    af[3] = pk_bf16(p3.x, p3.y);
-                }
-                const uint32_t b0 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 2 * tq));
-                const uint32_t b1 = __ldg(reinterpret_cast<const unsigned int*>(wrow + k0 + 8 + 2 * tq));
-                mma_16816(acc, af, b0, b1);
+            for (int k0 = 0; k0 < DI; k0 += 32) {
+                uint32_t af[4], af2[4], bf[4];
+                ldsm_x4(af, a_addr + k0 * 2);
+                ldsm_x4(af2, a_addr + (k0 + 16) * 2);
+                ldsm_x4(bf, b_addr + k0 * 2);
+                mma_16816(acc, af, bf[0], bf[1]);
+                mma_16816(acc, af2, bf[2], bf[3]);
             }
             const int c = nt * 8 + 2 * tq;
             *reinterpret_cast<float2*>(dbc_s + g * L::kDbcld + c) = make_float2(acc[0], acc[1]);
@@ -324,7 +284,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
         }
         __syncthreads();
         // ---- 3. dt_proj + softplus: dl[16][DI] = softplus(dt_r[16][RP] . W_dt^T + b_dt)
-        if (a.diag != 2) {
+        {
             uint32_t af[RP / 16][4];
 #pragma unroll
             for (int ks = 0; ks < RP / 16; ++ks) {
@@ -343,17 +303,9 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
             for (int j = 0; j < NT_DT; ++j) {
                 float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int ks = 0; ks < RP / 16; ++ks) {
-                    if (kWdtReg) {
-                        mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
-                    } else {
-                        const __nv_bfloat16* wrow = a.Wdt_b + (int64_t)((warp + j * NW) * 8 + g) * RP;
-                        mma_16816(acc, af[ks], __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 2 * tq)),
-                                  __ldg(reinterpret_cast<const unsigned int*>(wrow + ks * 16 + 8 + 2 * tq)));
-                    }
-                }
+                for (int ks = 0; ks < RP / 16; ++ks) mma_16816(acc, af[ks], wdt[j][ks][0], wdt[j][ks][1]);
                 const int c = (warp + j * NW) * 8 + 2 * tq;
-                const float2 bj = kWdtReg ? bdt[j] : __ldg(reinterpret_cast<const float2*>(a.b_dt + (warp + j * NW) * 8 + 2 * tq));
+                const float2 bj = bdt[j];
                 const float b0v = bj.x, b1v = bj.y;
                 *reinterpret_cast<float2*>(dl_s + g * DI + c) =
                     make_float2(softplus_fast(acc[0] + b0v), softplus_fast(acc[1] + b1v));
@@ -407,7 +359,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
                     for (int h = 0; h < 2; ++h) {
                         const int n = 2 * q + h;
                         const float2 x2 = __fmul2_rn(dl2, A2[n]);
-                        const float2 ab = (n >= N / 2 - OFF) ? exp2_poly_pair(x2) : make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 ab = make_float2(ex2(x2.x), ex2(x2.y));
                         const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
                         const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
                         // Bbar u = (Ab - 1) v with v = B u / A;  s <- Ab (s + v) - v
@@ -426,7 +378,7 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
             bcp += L::kDbcld;
             gout += DI;
         };
-        if (a.diag != 1) {
+        {
             if (tc == kTC && SU > 1) {
 #pragma unroll 1
                 for (int t0 = 0; t0 < kTC; t0 += SU) {
@@ -445,38 +397,25 @@ __global__ void __launch_bounds__(DI, OCC) k_mixer_fused(MixerArgs a) {
     }
 }
 
-template <int DI, int N, int RP, int NXP, int DC, int DISC, int OCC, int OFF = 0, int SU = 1>
+template <int DI, int N, int RP, int NXP, int DC, int DISC, int SU>
 static cudaError_t mixer_launch_k(const MixerArgs& a, int num_sms, cudaStream_t s) {
-    constexpr int smem = MixerSmem<DI, NXP, OCC>::kBytes;
-    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC, OCC, OFF, SU>;
+    constexpr int smem = MixerSmem<DI, NXP>::kBytes;
+    auto kern = k_mixer_fused<DI, N, RP, NXP, DC, DISC, SU>;
     if (a.ldg != DI) return cudaErrorInvalidValue;
-    static int blocks_per_sm = 0;
-    if (!blocks_per_sm) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&blocks_per_sm, kern, DI, smem);
-        if (e != cudaSuccess || blocks_per_sm < 1) blocks_per_sm = 1;
-    }
+    int blocks_per_sm = 0;
+    cudaError_t e = prepare_kernel(kern, smem, DI, &blocks_per_sm);
+    if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * blocks_per_sm;
     if (grid > a.n) grid = a.n;
     kern<<<(unsigned)grid, DI, smem, s>>>(a);
     return cudaGetLastError();
 }
 
+// scan tokens per unrolled step of a full chunk: 2 (measured at `large`: 1 -> 4.14 ms, 2 -> 4.03,
+// 4 -> 4.08-4.12, 16 -> 4.24 with spills)
 template <int DI, int N, int RP, int NXP>
 static cudaError_t mixer_launch(const MixerArgs& a, int num_sms, cudaStream_t s) {
     if (a.d_conv != 4) return cudaErrorInvalidValue;  // validated on the host
-    static const int occ = [] { const char* v = getenv("TCL_MIXER_OCC"); return (v && v[0] == '3') ? 3 : 2; }();
-    static const int off = [] { const char* v = getenv("TCL_MIXER_OFF"); return v ? atoi(v) : 0; }();
-    if (occ == 3)
-        return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1, 3>(a, num_sms, s)
-                           : mixer_launch_k<DI, N, RP, NXP, 4, 0, 3>(a, num_sms, s);
-    if (a.disc == 0 && N == 16 && off == 1) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 1>(a, num_sms, s);
-    if (a.disc == 0 && N == 16 && off == 2) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 2>(a, num_sms, s);
-    // scan tokens per unrolled step of a full chunk (measured at `large`: 1 -> 4.14 ms, 2 -> 4.03,
-    // 4 -> 4.08-4.12, 16 -> 4.24 with spills); TCL_MIXER_SU=1 restores the rolled loop
-    static const int su = [] { const char* v = getenv("TCL_MIXER_SU"); return v ? atoi(v) : 2; }();
-    if (a.disc == 0 && su == 2) return mixer_launch_k<DI, N, RP, NXP, 4, 0, 2, 0, 2>(a, num_sms, s);
     return a.disc == 1 ? mixer_launch_k<DI, N, RP, NXP, 4, 1, 2>(a, num_sms, s)
                        : mixer_launch_k<DI, N, RP, NXP, 4, 0, 2>(a, num_sms, s);
 }

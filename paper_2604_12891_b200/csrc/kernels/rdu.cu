@@ -350,23 +350,16 @@ cudaError_t launch_rdu_select(const float* pool, const int32_t* ops, int64_t n_p
     if ((e = cudaMemsetAsync(n_out, 0, sizeof(int32_t), s)) != cudaSuccess) return e;
     k_minmax_hist<<<std::max(1, std::min(1024, (int)((n_pool + n_lab + 255) / 256))), 256, 0, s>>>(
         pool, n_pool, lab, n_lab, ops, n_ops, mm, hist);
-    static const bool force_coop = [] { const char* v = getenv("TCL_RDU_COOP"); return v && v[0] == '1'; }();
     // the cluster wins while each thread scans <= 4 candidates per pick (measured: 3.0 us/pick at
     // 16,384 vs 6.8 cooperative); beyond that the 148-CTA cooperative grid's wider scan wins
-    if (!force_coop && n_pool <= (int64_t)kMaxCluster * kCThreads * 4) {
+    if (n_pool <= (int64_t)kMaxCluster * kCThreads * 4) {
         // cluster path: C CTAs (as many as useful, <= 8), each holding ceil(n_pool / C) candidates
         // in shared memory: the per-pick scan is spread wide, the exchange stays one cluster barrier
         const int C = (int)std::min<int64_t>(kMaxCluster, std::max<int64_t>(1, (n_pool + kCThreads - 1) / kCThreads));
         const int per = (int)((n_pool + C - 1) / C);
         SelArgs a{pool, ops, n_pool, lab, n_lab, n_ops, budget_total, per, mm, hist, nullptr, out, n_out};
         const int smem = ((per + kCThreads - 1) / kCThreads) * kCThreads * (4 + 4 + 2);
-        static bool attr = false;
-        if (!attr) {
-            if ((e = cudaFuncSetAttribute(k_rdu_cluster, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          kPerCta * (4 + 4 + 2))) != cudaSuccess)
-                return e;
-            attr = true;
-        }
+        if ((e = prepare_kernel(k_rdu_cluster, kPerCta * (4 + 4 + 2))) != cudaSuccess) return e;
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(C);
         cfg.blockDim = dim3(kCThreads);

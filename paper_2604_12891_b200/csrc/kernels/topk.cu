@@ -4,8 +4,13 @@
 //   key = orderable_u32(score) << 32 | (0xFFFFFFFF - global_index)
 // so the k largest keys are exactly the top-k.  Key 0 never encodes a real candidate (the
 // smallest real high word is orderable(-inf) = 0x007FFFFF) and is used as the padding sentinel.
-// Selection is a tournament: each CTA bitonic-sorts a chunk of 8192 keys in shared memory and
-// keeps its best k; rounds repeat until one chunk remains.  Integer-only -> bit-exact.
+// Selection, k <= 1024: each CTA takes up to 8,192 keys, finds its k-th largest key by an
+// MSB-first radix select (8-bit digits, shared-memory histograms, early exit once the boundary
+// digit holds exactly the keys still needed), gathers the keys above it and bitonic-sorts only
+// those k; rounds repeat over the survivors until one CTA's worth remains (k_topk_radix).
+// k > 1024: a tournament in which each CTA bitonic-sorts a chunk of keys in shared memory and
+// keeps its best k, rounds repeating until one chunk remains (k_topk_chunk).  Integer-only ->
+// bit-exact in both paths.
 #include <math.h>
 
 #include "../kernels.h"
@@ -170,13 +175,9 @@ size_t topk_tmp_keys(int64_t n, int k) {
 template <int C>
 static void launch_chunk(bool from_scores, unsigned blocks, const float* scores, const u64* src, int64_t cur,
                          int64_t index_base, int k, u64* dst, cudaStream_t s) {
-    static bool done = false;
     const int smem = C * (int)sizeof(u64);
-    if (!done) {
-        cudaFuncSetAttribute(k_topk_chunk<true, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(k_topk_chunk<false, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        done = true;
-    }
+    prepare_kernel(k_topk_chunk<true, C>, smem);
+    prepare_kernel(k_topk_chunk<false, C>, smem);
     if (from_scores)
         k_topk_chunk<true, C><<<blocks, 1024, smem, s>>>(scores, nullptr, cur, index_base, k, dst);
     else

@@ -130,7 +130,7 @@ cudaError_t launch_topk_eval(const float* scores, const float* lat, const int64_
     int P = 1;
     while (P < max_task_len) P <<= 1;
     const size_t smem = (size_t)P * sizeof(unsigned long long);
-    cudaError_t e = cudaFuncSetAttribute(k_task_topk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = prepare_kernel(k_task_topk, (int)smem);
     if (e != cudaSuccess) return e;
     const int grid = (int)std::min<int64_t>(n_tasks, (int64_t)num_sms * 4);
     k_task_topk<<<grid, kThreads, smem, s>>>(scores, lat, off, w, n_tasks, max_task_len, ks, cols, err);

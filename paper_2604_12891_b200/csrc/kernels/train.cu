@@ -410,13 +410,25 @@ __device__ float block_sum(float v, float* red) {
 }
 
 __global__ void __launch_bounds__(1024) k_lambdarank(const float* __restrict__ scores, const float* __restrict__ lat,
-                                                     const int64_t* __restrict__ off, int64_t n_groups, float sigma,
-                                                     float* __restrict__ dscores, float* __restrict__ gloss) {
+                                                     const int64_t* __restrict__ off, int64_t n_groups, int max_group,
+                                                     int64_t n_total, float sigma, float* __restrict__ dscores,
+                                                     float* __restrict__ gloss, int* __restrict__ err) {
     extern __shared__ unsigned long long keys[];   // [P]
     __shared__ float red[32];
     const int64_t g = blockIdx.x;
     const int64_t o = off[g];
-    const int n = (int)(off[g + 1] - o);
+    const int64_t n64 = off[g + 1] - o;
+    // shared memory is sized for max_group on the host: a group outside [2, max_group] or outside
+    // [0, n_total) is skipped (loss term 0, its candidates keep the zero gradient set by the
+    // launcher) and raises ERR_TASK (tcl_sync_error -> TCL_ESHAPE)
+    if (n64 < 2 || n64 > max_group || o < 0 || o + n64 > n_total) {
+        if (threadIdx.x == 0) {
+            gloss[g] = 0.0f;
+            atomicOr(err, ERR_TASK);
+        }
+        return;
+    }
+    const int n = (int)n64;
     int P = 1;
     while (P < n) P <<= 1;
     float* ys = reinterpret_cast<float*>(keys + P);    // [n] relevance
@@ -613,18 +625,19 @@ void launch_scan_bwd(const ScanBwdArgs& a, cudaStream_t s) {
 }
 
 cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64_t* off, int64_t n_groups,
-                              int max_group, float sigma, float* dscores, float* gloss, float* loss, cudaStream_t s) {
+                              int max_group, int64_t n_total, float sigma, float* dscores, float* gloss, float* loss,
+                              int* err, cudaStream_t s) {
     int P = 1;
     while (P < max_group) P <<= 1;
     const size_t smem = (size_t)P * 8 + (size_t)P * 4 * 4;
-    static bool attr = false;   // set once for the largest group (4096); never inside a graph capture
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(trn::k_lambdarank, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             4096 * (8 + 16));
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
-    trn::k_lambdarank<<<(unsigned)n_groups, 1024, smem, s>>>(scores, lat, off, n_groups, sigma, dscores, gloss);
+    // opted in once per device for the largest group (4096): the first (direct) step does it, so a
+    // graph capture never needs to
+    cudaError_t e = prepare_kernel(trn::k_lambdarank, 4096 * (8 + 16));
+    if (e != cudaSuccess) return e;
+    // candidates outside every group get dL/ds = 0 (not stale values)
+    if ((e = cudaMemsetAsync(dscores, 0, sizeof(float) * (size_t)n_total, s)) != cudaSuccess) return e;
+    trn::k_lambdarank<<<(unsigned)n_groups, 1024, smem, s>>>(scores, lat, off, n_groups, max_group, n_total, sigma,
+                                                             dscores, gloss, err);
     trn::k_loss_mean<<<1, 1024, 0, s>>>(gloss, n_groups, loss);
     return cudaGetLastError();
 }

@@ -20,11 +20,8 @@ struct MixerArgs {
     const int32_t* cu; const int32_t* lens;
     int64_t n;
     int DI, N, R, RP, d_conv, disc, max_len;
-    int diag;  // profiling diagnostics only: 1 = skip the scan phase, 2 = skip conv/x_proj/dt_proj, 3 = skip conv
 };
 
 cudaError_t launch_mixer_fused(const MixerArgs& a, int num_sms, cudaStream_t s);
-// Warp-specialised variant (producer warps: TMA + conv + x/dt_proj; scan warps: the recurrence).
-cudaError_t launch_mixer_ws(const MixerArgs& a, int num_sms, cudaStream_t s);
 
 }  // namespace tcl

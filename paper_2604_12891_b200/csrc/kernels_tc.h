@@ -22,12 +22,11 @@ struct TcGemmParams {
     __nv_bfloat16* out; int ldo; // bf16 output (EPI_BF16) / LayerNorm output (EPI_RESID_LN)
     // TC_EPI_RESID_LN: H = (residual ? H : 0) + acc (+ bias); out = bf16(LN(H) * g + b)
     float* H; int ldh; int residual;
-    int skip_h_store;
-    int diag_nostore;            // profiling only: skip the output stores
+    int skip_h_store;            // RESID_LN (gemm_tc_ln): do not write H back (last layer: only LN_f(H) is consumed)
     int silu_from;               // EPI_BF16 without bias: columns >= silu_from (> 0) leave as SiLU(acc)
                                  // (in_proj: the mixer's gate SiLU(z) formed in this HBM-bound epilogue)
-    int mcast;                   // EPI_BF16, n_tiles in {2, 4}: the n_tiles CTAs of a cluster share each
-                                 // A tile via TMA multicast (A map box {64, 128 / n_tiles})            // RESID_LN (gemm_tc_ln): do not write H back (last layer: only LN_f(H) is consumed)
+    int mcast;                   // EPI_BF16, n_tiles in {2, 4}: pairs of CTAs (N tiles 2j, 2j+1) share each
+                                 // A tile via TMA multicast (A map box {64, 64}: each CTA fetches half)
     const float* ln_g; const float* ln_b; float eps;
     DropoutCtx drop; int site; const int32_t* row_cand; const int32_t* cu;
 };

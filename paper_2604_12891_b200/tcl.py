@@ -48,7 +48,8 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
            "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
            "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step",
-           "tcl_train_read"]
+           "tcl_train_read", "tcl_set_option"]
+TCL_OPT_GRAPHS = 1
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc", "lateral"]
 
@@ -101,12 +102,14 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_debug_read.argtypes = [vp, ctypes.c_char_p, vp, i64, i64]
     L.tcl_rdu_select.argtypes = [vp, vp, vp, i64, vp, i64, i32, i32, vp, vp, vp]
     L.tcl_topk_score.argtypes = [vp, vp, vp, vp, vp, i64, i32, vp, i32, vp, vp]
+    L.tcl_set_option.argtypes = [vp, i32, i64]
     L.tcl_profile_name.restype = ctypes.c_char_p
     L.tcl_profile_name.argtypes = [ctypes.c_int]
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
                "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select",
-               "tcl_topk_score", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step", "tcl_train_read"):
+               "tcl_topk_score", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step", "tcl_train_read",
+               "tcl_set_option"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -120,10 +123,38 @@ def _check(code: int):
 def _ptr(t) -> int:
     """Device/host address of a torch tensor or numpy array (no copy, must be contiguous)."""
     if isinstance(t, np.ndarray):
-        assert t.flags["C_CONTIGUOUS"]
+        if not t.flags["C_CONTIGUOUS"]:
+            raise TclError(-1, "array must be C-contiguous")
         return t.ctypes.data
-    assert t.is_contiguous()
+    if not t.is_contiguous():
+        raise TclError(-1, "tensor must be contiguous")
     return t.data_ptr()
+
+
+_NP = {"f32": np.float32, "f64": np.float64, "i32": np.int32, "i64": np.int64}
+
+
+def _arg(t, kind: str, count: int, name: str, device: bool = True) -> int:
+    """Validated pointer of argument `name`: dtype `kind`, >= `count` elements, contiguous, on a
+    CUDA device (device=True: a torch CUDA tensor) or in host memory (device=False: a numpy array
+    or a CPU tensor).  Raises TclError(TCL_EINVAL) instead of passing a bad pointer to the C ABI."""
+    if t is None:
+        raise TclError(-1, f"{name} is None")
+    if isinstance(t, np.ndarray):
+        if device:
+            raise TclError(-1, f"{name}: a CUDA tensor is required, got a numpy array")
+        dt, size = t.dtype, t.size
+        ok = dt == np.dtype(_NP[kind])
+    else:
+        if bool(t.is_cuda) != device:
+            raise TclError(-1, f"{name}: expected a {'CUDA' if device else 'host'} tensor")
+        dt, size = t.dtype, t.numel()
+        ok = str(dt) == "torch." + {"f32": "float32", "f64": "float64", "i32": "int32", "i64": "int64"}[kind]
+    if not ok:
+        raise TclError(-1, f"{name}: dtype {dt} where {np.dtype(_NP[kind])} is required")
+    if size < count:
+        raise TclError(-1, f"{name}: {size} elements where {count} are required")
+    return _ptr(t)
 
 
 def _stream(stream) -> Optional[int]:
@@ -198,38 +229,56 @@ class Model:
     def handle(self):
         return self._h
 
+    def set_option(self, option: int, value: int):
+        _check(load().tcl_set_option(self._h, option, value))
+
+    def use_graphs(self, on: bool = True):
+        """CUDA-graph replay of repeated calls (TCL_OPT_GRAPHS, default on)."""
+        self.set_option(TCL_OPT_GRAPHS, 1 if on else 0)
+
     def reserve(self, n_max: int, mc_passes_max: int = 0):
         _check(load().tcl_reserve(self._h, n_max, mc_passes_max))
 
     # -- device-buffer calls (torch CUDA tensors) --------------------------------------------
-    def tcl_score(self, feats, lens, scores, stream=None):
+    def _feats(self, feats, lens, device=True):
         n = lens.shape[0]
-        _check(load().tcl_score(self._h, _ptr(feats), _ptr(lens), n, _ptr(scores), _stream(stream)))
+        row = self.dims.max_len * self.dims.d_in
+        return n, _arg(feats, "f32", n * row, "feats", device), _arg(lens, "i32", n, "lens", device)
+
+    def tcl_score(self, feats, lens, scores, stream=None):
+        n, pf, pl = self._feats(feats, lens)
+        _check(load().tcl_score(self._h, pf, pl, n, _arg(scores, "f32", n, "scores"), _stream(stream)))
 
     def tcl_score_mc(self, feats, lens, n_passes: int, seed: int, index_base: int, mean, var, stream=None):
-        n = lens.shape[0]
-        _check(load().tcl_score_mc(self._h, _ptr(feats), _ptr(lens), n, n_passes, seed, index_base,
-                                   _ptr(mean), _ptr(var), _stream(stream)))
+        n, pf, pl = self._feats(feats, lens)
+        _check(load().tcl_score_mc(self._h, pf, pl, n, n_passes, seed, index_base,
+                                   _arg(mean, "f32", n, "mean"), _arg(var, "f32", n, "var"), _stream(stream)))
 
     def tcl_topk(self, scores, k: int, index_base: int, idx, top, n: Optional[int] = None, stream=None):
         n = scores.shape[0] if n is None else n
-        _check(load().tcl_topk(self._h, _ptr(scores), n, k, index_base, _ptr(idx), _ptr(top), _stream(stream)))
+        _check(load().tcl_topk(self._h, _arg(scores, "f32", n, "scores"), n, k, index_base,
+                               _arg(idx, "i64", k, "idx"), _arg(top, "f32", k, "top"), _stream(stream)))
 
     def tcl_comm_init(self, uid: bytes, nranks: int, rank: int):
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(uid)
         _check(load().tcl_comm_init(self._h, buf, nranks, rank))
 
     def tcl_topk_global(self, scores, index_base: int, k: int, idx, top, stream=None):
-        _check(load().tcl_topk_global(self._h, _ptr(scores), scores.shape[0], index_base, k, _ptr(idx),
-                                      _ptr(top), _stream(stream)))
+        n = scores.shape[0]
+        _check(load().tcl_topk_global(self._h, _arg(scores, "f32", n, "scores"), n, index_base, k,
+                                      _arg(idx, "i64", k, "idx"), _arg(top, "f32", k, "top"), _stream(stream)))
 
     def tcl_topk_score(self, scores, latency, task_offsets, task_weights, max_task_len: int, ks, result,
                        stream=None):
         """Eq. 12 Top-k score over CSR tasks (device tensors); result [3*len(ks)] fp64 = score|num|den."""
         kk = np.ascontiguousarray(ks, dtype=np.int32)
-        _check(load().tcl_topk_score(self._h, _ptr(scores), _ptr(latency), _ptr(task_offsets),
-                                     _ptr(task_weights), task_offsets.shape[0] - 1, max_task_len,
-                                     kk.ctypes.data, kk.size, _ptr(result), _stream(stream)))
+        nt = task_offsets.shape[0] - 1
+        n = scores.shape[0]
+        _check(load().tcl_topk_score(self._h, _arg(scores, "f32", n, "scores"), _arg(latency, "f32", n, "latency"),
+                                     _arg(task_offsets, "i64", nt + 1, "task_offsets"),
+                                     _arg(task_weights, "f32", nt, "task_weights"), nt, max_task_len,
+                                     kk.ctypes.data, kk.size, _arg(result, "f64", 3 * kk.size, "result"),
+                                     _stream(stream)))
 
     # -- training (fp32 models) ------------------------------------------------------------------
     def tcl_train_init(self, n_max: int, lr: float = 7e-4, beta1: float = 0.9, beta2: float = 0.999,
@@ -239,9 +288,11 @@ class Model:
     def tcl_train_step(self, feats, lens, latency, group_offsets, max_group: int, apply_update: bool = True,
                        loss=None, stream=None):
         """One LambdaRank + Adam step on device tensors; loss (fp32 [1] device tensor) optional."""
-        _check(load().tcl_train_step(self._h, _ptr(feats), _ptr(lens), lens.shape[0], _ptr(latency),
-                                     _ptr(group_offsets), group_offsets.shape[0] - 1, max_group,
-                                     1 if apply_update else 0, _ptr(loss) if loss is not None else None,
+        n, pf, pl = self._feats(feats, lens)
+        ng = group_offsets.shape[0] - 1
+        _check(load().tcl_train_step(self._h, pf, pl, n, _arg(latency, "f32", n, "latency"),
+                                     _arg(group_offsets, "i64", ng + 1, "group_offsets"), ng, max_group,
+                                     1 if apply_update else 0, _arg(loss, "f32", 1, "loss") if loss is not None else None,
                                      _stream(stream)))
 
     def tcl_train_read(self, what: str, count: int) -> np.ndarray:
@@ -253,10 +304,12 @@ class Model:
     def tcl_rdu_select(self, pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int,
                        selected, n_selected, stream=None):
         """RDU acquisition round (Alg. 1 lines 16-31): device tensors in, picks in `selected`."""
-        _check(load().tcl_rdu_select(self._h, _ptr(pool_scores), _ptr(pool_ops), pool_scores.shape[0],
-                                     _ptr(labeled_scores) if labeled_scores.shape[0] else None,
-                                     labeled_scores.shape[0], n_ops, budget_total, _ptr(selected),
-                                     _ptr(n_selected), _stream(stream)))
+        n, nl = pool_scores.shape[0], labeled_scores.shape[0]
+        _check(load().tcl_rdu_select(self._h, _arg(pool_scores, "f32", n, "pool_scores"),
+                                     _arg(pool_ops, "i32", n, "pool_ops"),
+                                     n, _arg(labeled_scores, "f32", nl, "labeled_scores") if nl else None,
+                                     nl, n_ops, budget_total, _arg(selected, "i64", budget_total, "selected"),
+                                     _arg(n_selected, "i32", 1, "n_selected"), _stream(stream)))
 
     def tcl_sync_error(self, stream=None):
         _check(load().tcl_sync_error(self._h, _stream(stream)))
@@ -284,10 +337,11 @@ class Model:
     def tcl_score_host(self, feats: np.ndarray, lens: np.ndarray, k: int = 0, index_base: int = 0,
                        scores: np.ndarray = None, idx: np.ndarray = None, top: np.ndarray = None,
                        stream=None) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
-        n = lens.shape[0]
+        n, pf, pl = self._feats(feats, lens, device=False)
         scores = np.empty(n, np.float32) if scores is None else scores
         idx = np.empty(max(k, 1), np.int64) if idx is None else idx
         top = np.empty(max(k, 1), np.float32) if top is None else top
-        _check(load().tcl_score_host(self._h, _ptr(feats), _ptr(lens), n, index_base, _ptr(scores), k,
-                                     _ptr(idx), _ptr(top), _stream(stream)))
+        _check(load().tcl_score_host(self._h, pf, pl, n, index_base, _arg(scores, "f32", n, "scores", False), k,
+                                     _arg(idx, "i64", k, "idx", False), _arg(top, "f32", k, "top", False),
+                                     _stream(stream)))
         return scores, idx[:k], top[:k]

@@ -213,7 +213,9 @@ def _topk_gpu(torch, m, s, k, index_base=0):
 
 @pytest.mark.parametrize("n,k", [(1, 1), (100, 16), (8192, 64), (8193, 64), (65536, 64),
                                  (300000, 1024), (50, 64), (20000, 4096),
-                                 (8192, 256), (100000, 256), (100000, 257), (1000000, 64)])
+                                 (8192, 256), (100000, 256), (100000, 257), (1000000, 64),
+                                 # the radix-select / bitonic-tournament boundary (k <= 1024 radix)
+                                 (100000, 1024), (100000, 1025), (700, 1000), (300, 257)])
 def test_topk_bitexact_vs_stable_sort(torch_cuda, n, k):
     from paper_2604_12891_b200 import Model
     d, w, _, _ = _setup("tiny", n=2)

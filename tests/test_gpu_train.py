@@ -136,18 +136,29 @@ f, l = inputs.make_features(d, 32, 7, workload="tuning")
 lat = np.exp(np.random.default_rng(3).normal(-6, 0.7, 32)).astype(np.float32)
 off = np.arange(0, 33, 8, dtype=np.int64)
 m = Model(w, d)
+m.use_graphs(sys.argv[3] == "1")
 m.tcl_train_init(32, lr=1e-3)
 ft, lt, latt, offt = (torch.from_numpy(a).cuda() for a in (f, l, lat, off))
 loss = torch.zeros(1, device="cuda")
 for _ in range(3):
     m.tcl_train_step(ft, lt, latt, offt, 8, True, loss)
-np.save(sys.argv[2], m.tcl_train_read("weights", w.size))
+# Alg. 1 loop: score a pool much larger than the training batch (the workspace grows and is
+# reallocated), then train again -- a replayed step graph must not use the freed buffers
+fp, lp = inputs.make_features(d, 20000, 8, workload="tuning")
+sp = torch.empty(20000, device="cuda")
+m.tcl_score(torch.from_numpy(fp).cuda(), torch.from_numpy(lp).cuda(), sp)
+for _ in range(2):
+    m.tcl_train_step(ft, lt, latt, offt, 8, True, loss)
+m.tcl_sync_error()
+np.save(sys.argv[2], np.concatenate([m.tcl_train_read("weights", w.size), sp.cpu().numpy()]))
 '''
 
 
 def test_graph_replay_equals_direct_launches(torch_cuda, tmp_path):
-    """The captured step graph (default) and direct launches (TCL_TRAIN_GRAPH=0) give bit-identical
-    weights after 3 Adam steps (the step counter and bias corrections live on the device)."""
+    '''The captured step graph (default) and direct launches (TCL_OPT_GRAPHS = 0) give bit-identical
+    weights after 3 Adam steps, a pool scoring that reallocates the workspace, and 2 more steps
+    (the step counter and bias corrections live on the device; the graph is re-captured when the
+    workspace it baked in is reallocated).'''
     import os
     import subprocess
     import sys
@@ -156,8 +167,29 @@ def test_graph_replay_equals_direct_launches(torch_cuda, tmp_path):
     script.write_text(_STEPS_SCRIPT)
     out = {}
     for mode in ("1", "0"):
-        env = dict(os.environ, TCL_TRAIN_GRAPH=mode)
         path = tmp_path / f"w{mode}.npy"
-        subprocess.run([sys.executable, str(script), root, str(path)], check=True, env=env, timeout=300)
+        subprocess.run([sys.executable, str(script), root, str(path), mode], check=True, timeout=300)
         out[mode] = np.load(path)
+    assert np.isfinite(out["0"]).all()
     assert np.array_equal(out["1"], out["0"])
+
+
+def test_bad_groups_flagged(torch_cuda):
+    '''A group larger than max_group (or with < 2 members) is skipped and flagged (TCL_ESHAPE);
+    candidates outside every group get a zero score gradient.'''
+    from paper_2604_12891_b200 import Model, TclError
+    c = inputs.config("tiny")
+    d = c["dims"]
+    w = inputs.make_weights(d, c["seed"])
+    f, l = inputs.make_features(d, 32, 7, workload="tuning")
+    lat = np.exp(np.random.default_rng(3).normal(-6, 0.7, 32)).astype(np.float32)
+    m = Model(w, d)
+    m.tcl_train_init(32)
+    off = np.array([0, 8, 24, 30], dtype=np.int64)      # group 1 has 16 > max_group = 8; 30..31 uncovered
+    ft, lt, latt, offt = _dev(torch_cuda, f, l, lat, off)
+    m.tcl_train_step(ft, lt, latt, offt, 8, False)
+    with pytest.raises(TclError) as e:
+        m.tcl_sync_error()
+    assert e.value.code == -2
+    ds = m.tcl_train_read("dscores", 32)
+    assert np.all(ds[8:24] == 0) and np.all(ds[30:] == 0) and np.any(ds[:8] != 0)
