@@ -72,6 +72,8 @@ def lib() -> ctypes.CDLL:
         L.tclo_score.argtypes = [P(_Dims), fp, fp, ip, ctypes.c_int64, dp, ctypes.c_int]
         L.tclo_score_mc.argtypes = [P(_Dims), fp, fp, ip, ctypes.c_int64, ctypes.c_int32,
                                     ctypes.c_uint64, ctypes.c_int64, dp, dp, ctypes.c_int]
+        L.tclo_score_pass.argtypes = [P(_Dims), fp, fp, ip, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64,
+                                      ctypes.c_int64, dp, ctypes.c_int]
         L.tclo_topk_f64.argtypes = [dp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, dp]
         L.tclo_topk_f32.argtypes = [fp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, lp, fp]
         L.tclo_adapters_count.restype = ctypes.c_int64
@@ -222,6 +224,21 @@ def score_mc(d, w, feats, lens, n_passes: int, seed: int, index_base: int = 0,
     return mean, var
 
 
+def score_pass(d, w, feats, lens, pass_index: int, seed: int, index_base: int = 0,
+               nthreads: Optional[int] = None) -> np.ndarray:
+    """Scores of ONE MC-dropout pass (the masks tclo_score_mc uses for that pass)."""
+    feats = _f32(feats)
+    lens = np.ascontiguousarray(lens, dtype=np.int32)
+    n = lens.shape[0]
+    out = np.zeros(n, dtype=np.float64)
+    rc = lib().tclo_score_pass(ctypes.byref(_cdims(d)), _p(_f32(w), ctypes.c_float), _p(feats, ctypes.c_float),
+                               _p(lens, ctypes.c_int32), n, pass_index, seed, index_base,
+                               _p(out, ctypes.c_double), nthreads or default_threads())
+    if rc != 0:
+        raise ValueError("tclo_score_pass failed")
+    return out
+
+
 def topk(scores: np.ndarray, k: int, index_base: int = 0) -> Tuple[np.ndarray, np.ndarray]:
     """(idx int64 [k], score [k]) under (score desc, index asc), NaN -> -inf, clamp + fill."""
     idx = np.zeros(k, dtype=np.int64)
@@ -250,6 +267,90 @@ def rdu_select(pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: 
                               _p(ls, ctypes.c_float), len(labeled_scores), n_ops, budget_total,
                               _p(out, ctypes.c_int64))
     return out[:k]
+
+
+def _rdu_prepare_f64(pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int):
+    """Alg. 1 lines 16-19 in fp64: f^ (min-max over finite pool u labeled predictions, 0.5 when
+    flat), eligibility (finite, op in range) and the per-op budgets B_t count(op) / n_pool."""
+    pool = np.asarray(pool_scores, dtype=np.float64)
+    ops = np.asarray(pool_ops, dtype=np.int64)
+    lab = np.asarray(labeled_scores, dtype=np.float64)
+    fin = np.concatenate([pool[np.isfinite(pool)], lab[np.isfinite(lab)]])
+    lo, hi = (fin.min(), fin.max()) if fin.size else (0.0, 0.0)
+    norm = (lambda v: np.full_like(v, 0.5)) if not hi > lo else (lambda v: (v - lo) / (hi - lo))
+    fh = norm(pool)
+    labh = list(norm(lab[np.isfinite(lab)]))
+    ok_op = (ops >= 0) & (ops < n_ops)
+    alive = np.isfinite(pool) & ok_op
+    count = np.bincount(ops[ok_op], minlength=n_ops).astype(np.float64)
+    budget = budget_total * count / pool.size
+    return fh, ops, labh, alive, budget
+
+
+def _rdu_total_f64(fh, labh):
+    """Eq. 1 (d_s: nearest labeled f^, 1 when none), Eqs. 2-3 (u_s: population variance of the
+    labeled set plus the candidate, TWO-PASS: mean first, then the squared deviations) and line 24
+    (t_s = f^ d_s + u_s), all in fp64, for every candidate f^ in `fh`."""
+    L = np.asarray(labh, dtype=np.float64)
+    if L.size == 0:
+        return fh * 1.0 + 0.0
+    ds = np.abs(fh[:, None] - L[None, :]).min(1)
+    mu = (fh + L.sum()) / (L.size + 1)
+    us = ((fh - mu) ** 2 + ((L[None, :] - mu[:, None]) ** 2).sum(1)) / (L.size + 1)
+    return fh * ds + us
+
+
+def rdu_select_f64(pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int) -> np.ndarray:
+    """One RDU selection round (Alg. 1 lines 16-31, Eqs. 1-3) written plainly in fp64: every pick
+    recomputes d_s and the two-pass variance over the current labeled set; argmax t_s, ties by
+    higher f^ then lower index (reading R21); a pick joins the labeled set before the next."""
+    fh, ops, labh, alive, budget = _rdu_prepare_f64(pool_scores, pool_ops, labeled_scores, n_ops, budget_total)
+    sel = np.zeros(n_ops)
+    picks = []
+    for _ in range(budget_total):
+        elig = alive.copy()
+        elig[alive] = sel[ops[alive]] < budget[ops[alive]]
+        idx = np.nonzero(elig)[0]
+        if idx.size == 0:
+            break
+        t = _rdu_total_f64(fh[idx], labh)
+        best = idx[np.lexsort((idx, -fh[idx], -t))[0]]
+        picks.append(int(best))
+        alive[best] = False
+        sel[ops[best]] += 1
+        labh.append(fh[best])
+    return np.array(picks, dtype=np.int64)
+
+
+def rdu_follow_f64(pool_scores, pool_ops, labeled_scores, n_ops: int, budget_total: int, picks,
+                   tol: float) -> int:
+    """Replay a pick sequence (e.g. the GPU's) in fp64 (R19-style near-tie rule for RDU): every pick
+    must be eligible and its fp64 t_s within `tol` of the best eligible fp64 t_s given the picks
+    before it; the sequence may only end when nothing is eligible.  Returns the number of picks
+    that are not the fp64 argmax (near ties, each within tol); raises AssertionError otherwise."""
+    fh, ops, labh, alive, budget = _rdu_prepare_f64(pool_scores, pool_ops, labeled_scores, n_ops, budget_total)
+    sel = np.zeros(n_ops)
+    near = 0
+    for step in range(budget_total):
+        elig = alive.copy()
+        elig[alive] = sel[ops[alive]] < budget[ops[alive]]
+        idx = np.nonzero(elig)[0]
+        if step == len(picks):
+            assert idx.size == 0, f"sequence ended after {step} picks with {idx.size} eligible candidates"
+            break
+        if idx.size == 0:
+            raise AssertionError(f"pick {step} made with no eligible candidate")
+        b = int(picks[step])
+        assert elig[b], f"pick {step} ({b}) is not eligible"
+        t = _rdu_total_f64(fh[idx], labh)
+        best = idx[np.lexsort((idx, -fh[idx], -t))[0]]
+        tb = t[np.searchsorted(idx, b)]
+        assert tb >= t.max() - tol, f"pick {step}: t_s {tb:.9g} < best {t.max():.9g} - {tol}"
+        near += int(b != best)
+        alive[b] = False
+        sel[ops[b]] += 1
+        labh.append(fh[b])
+    return near
 
 
 def rdu_scores(fh_pool, fh_lab):

@@ -485,6 +485,7 @@ typedef struct {
     const float* kb_w;   /* non-NULL: KB + AC two-column model; w is the AC column */
     const float* ad_w;
     int ad_rank;
+    int one_pass;        /* >= 0: scores[i] = the score of dropout pass `one_pass` alone */
 } job_t;
 
 static void* worker(void* arg) {
@@ -498,7 +499,10 @@ static void* worker(void* arg) {
             if (j->mean) { j->mean[i] = NAN; j->var[i] = NAN; }
             continue;
         }
-        if (j->mc_passes <= 0) {
+        if (j->one_pass >= 0) {   /* one dropout pass (pins the MC reduction from outside) */
+            mc_ctx mc = {j->one_pass, j->seed, j->index_base + i};
+            j->scores[i] = forward_one(j->d, j->w, xf, T, &mc, NULL, NULL, NULL);
+        } else if (j->mc_passes <= 0) {
             j->scores[i] = j->kb_w ? forward_kbac(j->d, j->kb_w, j->w, j->ad_w, j->ad_rank, xf, T, NULL)
                                    : forward_one(j->d, j->w, xf, T, NULL, NULL, NULL, NULL);
         } else {
@@ -539,7 +543,7 @@ static int run_threads(job_t* proto, int nthreads) {
 int tclo_score(const tclo_dims* d, const float* w, const float* feats, const int32_t* lens,
                int64_t n, double* scores, int nthreads) {
     if (!dims_ok(d) || n < 0) return -1;
-    job_t j = {d, w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, NULL, NULL, 0};
+    job_t j = {d, w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, NULL, NULL, 0, -1};
     return run_threads(&j, nthreads);
 }
 
@@ -547,7 +551,7 @@ int tclo_score(const tclo_dims* d, const float* w, const float* feats, const int
 int tclo_score_kbac(const tclo_dims* d, const float* kb_w, const float* ac_w, const float* ad_w, int a,
                     const float* feats, const int32_t* lens, int64_t n, double* scores, int nthreads) {
     if (!dims_ok(d) || n < 0 || a < 1) return -1;
-    job_t j = {d, ac_w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, kb_w, ad_w, a};
+    job_t j = {d, ac_w, feats, lens, n, 0, 1, 0, 0, 0, scores, NULL, NULL, kb_w, ad_w, a, -1};
     return run_threads(&j, nthreads);
 }
 
@@ -555,7 +559,7 @@ int tclo_score_mc_kbac(const tclo_dims* d, const float* kb_w, const float* ac_w,
                        const float* feats, const int32_t* lens, int64_t n, int32_t n_passes, uint64_t seed,
                        int64_t index_base, double* mean, double* var, int nthreads) {
     if (!dims_ok(d) || n < 0 || n_passes < 1 || a < 1) return -1;
-    job_t j = {d, ac_w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, kb_w, ad_w, a};
+    job_t j = {d, ac_w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, kb_w, ad_w, a, -1};
     return run_threads(&j, nthreads);
 }
 
@@ -565,7 +569,17 @@ int tclo_score_mc(const tclo_dims* d, const float* w, const float* feats, const 
                   int64_t n, int32_t n_passes, uint64_t seed, int64_t index_base, double* mean,
                   double* var, int nthreads) {
     if (!dims_ok(d) || n < 0 || n_passes < 1) return -1;
-    job_t j = {d, w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, NULL, NULL, 0};
+    job_t j = {d, w, feats, lens, n, 0, 1, n_passes, seed, index_base, NULL, mean, var, NULL, NULL, 0, -1};
+    return run_threads(&j, nthreads);
+}
+
+/* The score of ONE MC-dropout pass `pass` (the same masks tclo_score_mc draws for that pass): the
+ * per-pass scores that tclo_score_mc reduces to (mean, population variance).  Used by the pins to
+ * check that reduction against numpy's mean / var of these scores. */
+int tclo_score_pass(const tclo_dims* d, const float* w, const float* feats, const int32_t* lens,
+                    int64_t n, int32_t pass, uint64_t seed, int64_t index_base, double* scores, int nthreads) {
+    if (!dims_ok(d) || n < 0 || pass < 0) return -1;
+    job_t j = {d, w, feats, lens, n, 0, 1, 0, seed, index_base, scores, NULL, NULL, NULL, NULL, 0, pass};
     return run_threads(&j, nthreads);
 }
 

@@ -382,6 +382,65 @@ def test_mc_keep_rate_and_determinism(oracle):
     assert np.all(v > 0)
 
 
+def test_mc_reduction_is_numpy_mean_and_population_var(oracle):
+    """R17: tcl_score_mc's mean / var are np.mean / np.var (ddof 0) of the per-pass scores, each
+    pass scored on its own (tclo_score_pass: the masks of that pass).  A variance divided by
+    passes^2, a sample variance or a dropped pass fails here."""
+    d, w, f, l = _model("tiny", 20)
+    P, seed, base = 5, 1234, 40
+    per = np.stack([oracle.score_pass(d, w, f, l, ps, seed, index_base=base) for ps in range(P)])
+    m, v = oracle.score_mc(d, w, f, l, n_passes=P, seed=seed, index_base=base)
+    np.testing.assert_allclose(m, per.mean(0), rtol=1e-13, atol=1e-15)
+    np.testing.assert_allclose(v, per.var(0), rtol=1e-10, atol=1e-15)
+    assert np.all(per.std(0) > 0) and not np.allclose(per[0], per[1])
+
+
+def _dropout_mask(oracle, seed, p, units, token, site, ps, gidx):
+    """R17 masks written out from the (KAT-pinned) Philox4x32-10 block: counter =
+    (unit >> 2, token << 2 | site, pass, gidx), key = seed; keep iff word[unit & 3] >= floor(p 2^32)."""
+    thr = int(math.floor(p * 2 ** 32))
+    out = np.empty(units)
+    for u0 in range(0, units, 4):
+        wds = oracle.philox4x32_10([u0 >> 2, (token << 2) | site, ps, gidx], [seed & 0xFFFFFFFF, seed >> 32])
+        for k in range(4):
+            if u0 + k < units:
+                out[u0 + k] = 1.0 / (1.0 - p) if wds[k] >= thr else 0.0
+    return out
+
+
+def test_dropout_sites_backbone_off(oracle):
+    """Dropout-site placement (R17: after the SiLU of encoder linears 1, 2 (per token) and decoder
+    linears 1, 2 (token 0)) pinned by an independent numpy forward: with W_out == 0 the model is
+    MLP -> LN_f -> masked mean -> MLP, and each pass of tclo_score_pass must equal it with the masks
+    drawn from the Philox block directly."""
+    d, w, f, l = _model("tiny", 6)
+    d = d.replace(dropout_p=0.3)
+    w = w.copy()
+    for m in inputs.manifest(d):
+        if m["name"].endswith("W_out"):
+            w[m["offset"]:m["offset"] + int(np.prod(m["shape"]))] = 0.0
+    W = {k: v.astype(np.float64) for k, v in inputs.split_weights(d, w).items()}
+    seed, base, p = 0x1234_0000_0007, 9, float(np.float32(0.3))   # dims.dropout_p is fp32
+    e1, e2, h1, h2 = d.enc_dims[0], d.enc_dims[1], d.dec_dims[0], d.dec_dims[1]
+    for ps in range(2):
+        got = oracle.score_pass(d, w, f, l, ps, seed, index_base=base)
+        for i in range(len(l)):
+            T, gi = int(l[i]), base + i
+            x = f[i, :T].astype(np.float64)
+            a1 = _silu(x @ W["enc.W1"].T + W["enc.b1"])
+            a1 *= np.stack([_dropout_mask(oracle, seed, p, e1, t, 0, ps, gi) for t in range(T)])
+            a2 = _silu(a1 @ W["enc.W2"].T + W["enc.b2"])
+            a2 *= np.stack([_dropout_mask(oracle, seed, p, e2, t, 1, ps, gi) for t in range(T)])
+            h = a2 @ W["enc.W3"].T + W["enc.b3"]
+            mu = h.mean(1, keepdims=True)
+            var = ((h - mu) ** 2).mean(1, keepdims=True)
+            pooled = (((h - mu) / np.sqrt(var + d.ln_eps)) * W["lnf_w"] + W["lnf_b"]).mean(0)
+            q1 = _silu(pooled @ W["dec.W1"].T + W["dec.b1"]) * _dropout_mask(oracle, seed, p, h1, 0, 2, ps, gi)
+            q2 = _silu(q1 @ W["dec.W2"].T + W["dec.b2"]) * _dropout_mask(oracle, seed, p, h2, 0, 3, ps, gi)
+            s = q2 @ W["dec.W3"][0] + W["dec.b3"][0]
+            assert got[i] == pytest.approx(s, rel=1e-11, abs=1e-12), (ps, i)
+
+
 # ----------------------------------------------------------------------------- top-k
 def test_topk_against_lexsort(oracle):
     rng = np.random.default_rng(6)

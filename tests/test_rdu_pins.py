@@ -132,3 +132,34 @@ def test_flat_and_nonfinite(oracle):
     pool = np.float32([0.1, np.nan, 0.9, np.inf, -np.inf, 0.5])
     picks = oracle.rdu_select(pool, np.zeros(6, np.int32), np.float32([np.nan, 0.2]), 1, 6)
     assert sorted(picks.tolist()) == [0, 2, 5]
+
+
+@pytest.mark.parametrize("seed,n,m,n_ops,B", [(0, 40, 0, 1, 10), (1, 60, 5, 3, 20), (2, 80, 30, 4, 40),
+                                              (3, 50, 1, 2, 50), (4, 33, 7, 5, 9)])
+def test_f64_oracle_brute_force(oracle, seed, n, m, n_ops, B):
+    """The plain fp64 selection (oracle.rdu_select_f64, two-pass Eq. 3) against the from-scratch
+    pure-Python brute force, on the same well-separated inputs."""
+    rng = np.random.default_rng(seed)
+    pool = (rng.permutation(4096)[:n] / 4096.0).astype(np.float32)
+    lab = (rng.permutation(4096)[:m] / 4096.0 + 1 / 8192).astype(np.float32)
+    ops = rng.integers(0, n_ops, n).astype(np.int32)
+    assert oracle.rdu_select_f64(pool, ops, lab, n_ops, B).tolist() == _brute_force(pool, ops, lab, n_ops, B)
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_fp32_selection_within_near_ties_of_f64(oracle, seed):
+    """The fp32 oracle (the kernel's operation order) follows the fp64 selection up to near ties:
+    every fp32 pick is within 1e-5 of the best fp64 total score given the picks before it."""
+    rng = np.random.default_rng(100 + seed)
+    n, m, n_ops, B = 1500, 40, 6, 150
+    pool = rng.normal(size=n).astype(np.float32)
+    lab = rng.normal(size=m).astype(np.float32)
+    ops = rng.integers(0, n_ops, n).astype(np.int32)
+    picks = oracle.rdu_select(pool, ops, lab, n_ops, B)
+    near = oracle.rdu_follow_f64(pool, ops, lab, n_ops, B, picks, tol=1e-5)
+    assert near <= B // 20
+    # a deliberately wrong sequence (the worst candidate first) is rejected
+    bad = picks.copy()
+    bad[0] = int(np.argmin(np.where(np.isfinite(pool), pool, np.inf)))
+    with pytest.raises(AssertionError):
+        oracle.rdu_follow_f64(pool, ops, lab, n_ops, B, bad, tol=1e-5)
