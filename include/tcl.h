@@ -181,8 +181,8 @@ tcl_status tcl_model_create_kbac(const float* kb_weights_host, const float* ac_w
  * beta1, beta2, eps (paper: Adam, lr 7e-4) and the LambdaRank scale sigma_rank (1).
  * tcl_train_step runs one step on a batch already on the device: feats/lens as tcl_score,
  * latency_dev [n] the measured latencies (> 0), group_offsets_dev [n_groups+1] int64 CSR groups
- * (one tuning task each; 2 <= members <= max_group <= 4096; a group outside that range, or outside
- * [0, n), contributes nothing and makes tcl_sync_error return TCL_ESHAPE; candidates outside every
+ * (one tuning task each; 1 <= members <= max_group, 2 <= max_group <= 4096; a single-member group
+ * has no pairs and contributes 0; a group outside that range, or outside [0, n), contributes nothing and makes tcl_sync_error return TCL_ESHAPE; candidates outside every
  * group get a zero score gradient), the loss
  *   L = mean_g sum_{y_i > y_j} |G_i - G_j| |1/D_i - 1/D_j| log2(1 + e^{-sigma (s_i - s_j)}),
  *   y = min latency of the group / latency, G = (2^y - 1) / maxDCG, D = log2(1 + predicted rank)

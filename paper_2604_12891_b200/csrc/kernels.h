@@ -169,7 +169,7 @@ void launch_conv_bwd(const float* X, int ldx, const float* w, const float* b, in
                      float* dw, float* db, cudaStream_t s);
 void launch_scan_bwd(const ScanBwdArgs& a, cudaStream_t s);
 // LambdaRank loss + dL/ds over CSR groups (reading R24).  dscores [n_total] is zeroed first; a
-// group with fewer than 2 or more than max_group members, or outside [0, n_total), contributes 0
+// group with no member or more than max_group members, or outside [0, n_total), contributes 0
 // and sets ERR_TASK in *err.
 cudaError_t launch_lambdarank(const float* scores, const float* lat, const int64_t* off, int64_t n_groups,
                               int max_group, int64_t n_total, float sigma, float* dscores, float* gloss, float* loss,

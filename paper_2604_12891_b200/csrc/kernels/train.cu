@@ -418,10 +418,10 @@ __global__ void __launch_bounds__(1024) k_lambdarank(const float* __restrict__ s
     const int64_t g = blockIdx.x;
     const int64_t o = off[g];
     const int64_t n64 = off[g + 1] - o;
-    // shared memory is sized for max_group on the host: a group outside [2, max_group] or outside
+    // shared memory is sized for max_group on the host: a group outside [1, max_group] or outside
     // [0, n_total) is skipped (loss term 0, its candidates keep the zero gradient set by the
     // launcher) and raises ERR_TASK (tcl_sync_error -> TCL_ESHAPE)
-    if (n64 < 2 || n64 > max_group || o < 0 || o + n64 > n_total) {
+    if (n64 < 1 || n64 > max_group || o < 0 || o + n64 > n_total) {
         if (threadIdx.x == 0) {
             gloss[g] = 0.0f;
             atomicOr(err, ERR_TASK);
