@@ -136,8 +136,12 @@ def stage_model(d, P: int, n: int):
         "conv": dict(bytes=P * di * act + P * di * 4),
         "x_proj": dict(flops=2 * P * di * (R + 2 * N), bytes=P * di * 4 + P * (R + 2 * N) * 4),
         "dt_proj": dict(flops=2 * P * R * di, bytes=P * R * 4 + P * di * 4),
-        # scan: u, delta, z in; g out (fp32) + B, C per token; N exps per (t, d)
-        "scan": dict(bytes=P * di * (3 * 4 + act) + P * 2 * N * 4, exps=P * di * N),
+        # scan: u, delta, z in; g out (fp32) + B, C per token; N exps per (t, d).  bf16 path (split
+        # mixer): the packet (u, Delta fp16, B, C fp32, SiLU(z) bf16) in, g (bf16) out
+        "scan": (dict(bytes=P * (6 * di + 8 * N) + P * di * 2, exps=P * di * N) if bf16 else
+                 dict(bytes=P * di * (3 * 4 + act) + P * 2 * N * 4, exps=P * di * N)),
+        # bf16 mixer prep: x (bf16) in; u, Delta (fp16), B, C (fp32) out; x_proj + dt_proj flops
+        "mixprep": dict(bytes=P * di * 2 + P * (4 * di + 8 * N), flops=2 * P * di * (R + 2 * N) + 2 * P * R * di),
         "out_proj": dict(flops=2 * P * di * dm, bytes=out_bytes),
         "head": dict(bytes=head_bytes),
         "mixer": dict(bytes=P * 2 * di * act + P * di * act, exps=P * di * N),
@@ -309,7 +313,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         wk = work.get(kind, {})
         calls = per_step_launches[kind]                  # launches of this stage per step
         units = (mc or 1) * (d.n_layer if kind in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj",
-                                                     "scan", "out_proj", "mixer") else 1)
+                                                     "scan", "out_proj", "mixer", "mixprep") else 1)
         scale = units / calls                            # fraction of a step's work per launch
         if "bytes" in wk:
             entry["gbs"] = wk["bytes"] * scale / (entry["ms_per_launch"] * 1e-3) / 1e9
@@ -326,7 +330,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     wk = work[dom]
     calls = per_step_launches[dom]
     units = (mc or 1) * (d.n_layer if dom in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan",
-                                                "out_proj", "mixer") else 1)
+                                                "out_proj", "mixer", "mixprep") else 1)
     traffic = None  # DRAM bytes per launch of this kernel from one ncu --set full capture (profiles/)
     tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
     if os.path.exists(tp):

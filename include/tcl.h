@@ -256,7 +256,8 @@ int64_t tcl_launch_count(const tcl_model* model);
 typedef enum {
     TCL_PROF_PACK = 0, TCL_PROF_ENCODER, TCL_PROF_LAYERNORM, TCL_PROF_IN_PROJ, TCL_PROF_CONV,
     TCL_PROF_X_PROJ, TCL_PROF_DT_PROJ, TCL_PROF_SCAN, TCL_PROF_OUT_PROJ, TCL_PROF_HEAD,
-    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_LATERAL, TCL_PROF_NKINDS
+    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_LATERAL, TCL_PROF_MIXPREP,
+    TCL_PROF_NKINDS
 } tcl_prof_kind;
 tcl_status tcl_profile_enable(tcl_model* model, int enable);
 tcl_status tcl_profile_read(tcl_model* model, double* ms_out, int64_t* launches_out, int reset);
@@ -264,8 +265,9 @@ const char* tcl_profile_name(int kind);
 
 /* Debugging aid (per-stage parity tests): copy the current contents of a workspace buffer, as
  * fp32, to host memory.  name: "H" (residual stream [P][d_model]), "A" (LayerNorm output
- * [P][d_model]), "XZ" (in_proj output [P][2 d_inner]), "G" (gated scan output [P][d_inner]),
- * "U" (conv output, fp32 path only), "DELTA" (fp32 path only).  Rows are the packed tokens of the
+ * [P][d_model]), "XZ" (in_proj output [P][2 d_inner]; bf16 path: [x | SiLU(z)]), "G" (gated
+ * scan output [P][d_inner]), "U" (conv + SiLU output [P][d_inner]), "DELTA" ([P][d_inner]), "BC"
+ * (bf16 path: x_proj's B and C [P][2 d_state]).  Rows are the packed tokens of the
  * last chunk scored; buffers hold the values of the LAST kernel that wrote them (bf16 path with
  * d_model >= 128: the last layer writes LN_f(H) into "A" and does not write "H").  Synchronises. */
 tcl_status tcl_debug_read(tcl_model* model, const char* name, float* host_out, int64_t rows, int64_t cols);

@@ -4,6 +4,7 @@
 // arena, the per-chunk launch sequence of the forward pass, MC-dropout passes
 // (CS6), top-k (a11), the host->device pipelined end-to-end call, and sticky error reporting.
 // Every arithmetic step of the path runs in the kernels under kernels/; this file only launches.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -251,6 +252,8 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         TAKE(XZb, rows * xzw);
         TAKE(Ab, rows * dm);
         TAKE(Gb, rows * di);
+        w.pk_ld = mixer_packet_bytes(di, d.d_state);
+        TAKE(Pk, rows * w.pk_ld);
         const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
         __nv_bfloat16* E1b = w.XZb;
         __nv_bfloat16* E2b = w.XZb + rows * e1;
@@ -263,6 +266,9 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         if (e1 >= 64) ok = ok && make_tmap_bf16(&w.tmE1o, E1b, e1, rows, (uint64_t)e1 * 2, 64, 32);
         if (e2 >= 64) ok = ok && make_tmap_bf16(&w.tmE2o, E2b, e2, rows, (uint64_t)e2 * 2, 64, 32);
         ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
+        // split mixer: in_proj writes x as [rows][di] (the XZb storage) and SiLU(z) into the packet
+        ok = ok && make_tmap_bf16(&w.tmXo, w.XZb, di, rows, (uint64_t)di * 2, 64, 32) &&
+             make_tmap_bf16(&w.tmGZo, w.Pk + mixer_packet_gz_offset(di, d.d_state), di, rows, (uint64_t)w.pk_ld, 64, 32);
         ok = ok && make_tmap_f32(&w.tmHf, w.H, dm, rows, (uint64_t)dm * 4, 32, 32);
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
         const int nt_in = 2 * di / m->bn_in;
@@ -597,9 +603,10 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            // the fused mixer's gate SiLU(z) is applied here (HBM-bound epilogue, idle SFU) instead of
-            // in the SFU-bound scan
+            // SiLU(z) (the scan's gate) is formed in this HBM-bound epilogue (idle SFU) and written
+            // straight into the mixer packet; x goes to its own [rows][di] buffer for k_mixprep
             p.silu_from = di;
+            p.split_col = di;
             // A tiles shared by TMA multicast inside clusters of 2 CTAs (N tiles 2j, 2j+1 of the same
             // row tile; each CTA fetches 64 of the 128 rows): the read side is bound by the L2->SM
             // traffic of the 4x re-read A tile (measured 0.60 ms with the stores disabled), and
@@ -607,24 +614,33 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             // cluster-coupled stalls).
             p.mcast = (p.n_tiles == 2 || p.n_tiles == 4) ? 1 : 0;
             const CUtensorMap& amap = p.mcast ? w.tmAbS2 : w.tmAb;
-            if ((e = launch_gemm_tc(amap, m->tmWin[l], w.tmXZo, p, m->bn_in, kb_of(dm), m->num_sms, s)) != cudaSuccess)
+            if ((e = launch_gemm_tc(amap, m->tmWin[l], w.tmXo, p, m->bn_in, kb_of(dm), m->num_sms, s, &w.tmGZo)) !=
+                cudaSuccess)
                 return cuda_error(e, "in_proj");
             ++nl;
             if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;
         }
-        {
-            ProfScope ps(m, TCL_PROF_MIXER, s);
-            MixerArgs a{};
-            a.XZ = w.XZb; a.ldxz = 2 * di; a.G = w.Gb; a.ldg = di;
-            a.A2 = m->A2 + (size_t)l * di * N; a.invA = m->invA + (size_t)l * di * N; a.Dv = q.Dv;
+        {   // conv + SiLU, x_proj, dt_proj + softplus -> packet (mixer_split.cu)
+            ProfScope ps(m, TCL_PROF_MIXPREP, s);
+            MixPrepArgs a{};
+            a.X = w.XZb; a.Pk = w.Pk; a.pk_ld = w.pk_ld;
             a.w_conv = q.w_conv; a.b_conv = q.b_conv; a.b_dt = q.b_dt;
             a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
-            a.cu = w.cu; a.lens = lens; a.n = n;
-            a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.d_conv = d.d_conv; a.disc = d.disc; a.max_len = L;
-            e = launch_mixer_fused(a, m->num_sms, s);
-            if (e != cudaSuccess) return cuda_error(e, "mixer");
+            a.cu = w.cu; a.row_cand = w.row_cand; a.n = n; a.DI = di; a.N = N; a.R = R; a.RP = m->rp;
+            a.d_conv = d.d_conv; a.max_len = L;
+            if ((e = launch_mixprep(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "mixprep");
             ++nl;
-            if (debug_sync("mixer", s) != TCL_OK) return TCL_ECUDA;
+            if (debug_sync("mixprep", s) != TCL_OK) return TCL_ECUDA;
+        }
+        {   // the selective scan + D skip + gate (SFU-bound)
+            ProfScope ps(m, TCL_PROF_SCAN, s);
+            ScanBf16Args a{};
+            a.Pk = w.Pk; a.G = w.Gb;
+            a.A2 = m->A2 + (size_t)l * di * N; a.invA = m->invA + (size_t)l * di * N; a.Dv = q.Dv;
+            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.disc = d.disc;
+            if ((e = launch_scan_bf16(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "scan");
+            ++nl;
+            if (debug_sync("scan", s) != TCL_OK) return TCL_ECUDA;
         }
         {
             ProfScope ps(m, TCL_PROF_OUT_PROJ, s);
@@ -1032,6 +1048,33 @@ tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t ro
     const Workspace& w = m->ws;
     if (rows > w.rows) return set_error(TCL_EINVAL, "rows exceed the workspace");
     const std::string nm(name);
+    if (m->use_tc && (nm == "XZ" || nm == "U" || nm == "DELTA" || nm == "BC")) {
+        // bf16 path: x in XZb as [P][di] (bf16); u, Delta (fp16), B, C (fp32), SiLU(z) (bf16) in
+        // the mixer packet rows
+        const int di = m->dims.expand * m->dims.d_model, N = m->dims.d_state;
+        const int want = nm == "XZ" ? 2 * di : (nm == "BC" ? 2 * N : di);
+        if (cols != want) return set_error(TCL_EINVAL, "cols does not match the buffer");
+        std::vector<uint8_t> pk((size_t)rows * w.pk_ld);
+        CUDA_TRY(cudaMemcpy(pk.data(), w.Pk, pk.size(), cudaMemcpyDeviceToHost));
+        std::vector<uint16_t> xb((size_t)rows * di);
+        if (nm == "XZ") CUDA_TRY(cudaMemcpy(xb.data(), w.XZb, xb.size() * 2, cudaMemcpyDeviceToHost));
+        auto bf = [](uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; };
+        auto hf = [](uint16_t h) { __half_raw r; r.x = h; return __half2float(__half(r)); };
+        for (int64_t r = 0; r < rows; ++r) {
+            const uint8_t* row = pk.data() + (size_t)r * w.pk_ld;
+            for (int c = 0; c < want; ++c) {
+                float v;
+                uint16_t h;
+                if (nm == "XZ" && c < di) v = bf(xb[(size_t)r * di + c]);
+                else if (nm == "XZ") { memcpy(&h, row + 4 * di + 8 * N + 2 * (c - di), 2); v = bf(h); }
+                else if (nm == "U") { memcpy(&h, row + 2 * c, 2); v = hf(h); }
+                else if (nm == "DELTA") { memcpy(&h, row + 2 * di + 2 * c, 2); v = hf(h); }
+                else memcpy(&v, row + 4 * di + 4 * c, 4);
+                out[(size_t)r * want + c] = v;
+            }
+        }
+        return TCL_OK;
+    }
     const void* src = nullptr;
     bool bf = false;
     if (nm == "H") src = w.H;
@@ -1083,7 +1126,7 @@ tcl_status tcl_profile_read(tcl_model* m, double* ms_out, int64_t* launches_out,
 const char* tcl_profile_name(int kind) {
     static const char* names[TCL_PROF_NKINDS] = {"pack", "encoder", "layernorm", "in_proj", "conv",
                                                  "x_proj", "dt_proj", "scan", "out_proj", "head",
-                                                 "topk", "mixer", "allgather", "mc", "lateral"};
+                                                 "topk", "mixer", "allgather", "mc", "lateral", "mixprep"};
     return (kind >= 0 && kind < TCL_PROF_NKINDS) ? names[kind] : "";
 }
 

@@ -69,6 +69,7 @@ template <int BN, int KB, int EPI, int CL = 1>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
                                                          const __grid_constant__ CUtensorMap tmC,
+                                                         const __grid_constant__ CUtensorMap tmC2,
                                                          const TcGemmParams p) {
     using S = TcSmem<BN, KB, EPI>;
     constexpr int kStages = S::kStages;
@@ -256,9 +257,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                             tc::fence_proxy_async();
                             __syncwarp();
                             if (lane == 0) {
+                                const int col = n_tile * BN + (c - 1) * 32;
+                                const bool second = p.split_col > 0 && col >= p.split_col;
                                 asm volatile(
                                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                                    ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(n_tile * BN + (c - 1) * 32),
+                                    ::"l"(reinterpret_cast<uint64_t>(second ? &tmC2 : &tmC)),
+                                    "r"(second ? col - p.split_col : col),
                                     "r"(m * kBM + quarter * 32), "r"(tc::smem_u32(stg))
                                     : "memory");
                                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -416,13 +420,13 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 
 template <int BN, int KB, int EPI, int CL = 1>
 static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                               const TcGemmParams& p, int grid, cudaStream_t s) {
+                               const CUtensorMap& c2, const TcGemmParams& p, int grid, cudaStream_t s) {
     const int smem = TcSmem<BN, KB, EPI>::kBytes;
     auto kern = k_gemm_tc<BN, KB, EPI, CL>;
     cudaError_t e = prepare_kernel(kern, smem);
     if (e != cudaSuccess) return e;
     if (CL == 1) {
-        kern<<<grid, kThreads, smem, s>>>(a, b, c, p);
+        kern<<<grid, kThreads, smem, s>>>(a, b, c, c2, p);
     } else {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -436,7 +440,7 @@ static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const
         at[0].val.clusterDim.z = 1;
         cfg.attrs = at;
         cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, p);
+        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, c2, p);
         if (e != cudaSuccess) return e;
     }
     return cudaGetLastError();
@@ -444,20 +448,22 @@ static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const
 
 template <int BN, int KB>
 static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                              const TcGemmParams& p, int grid, cudaStream_t s) {
-    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
-    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
-    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
-    if (p.mcast && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, p, grid, s);
-    return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);
+                              const CUtensorMap& c2, const TcGemmParams& p, int grid, cudaStream_t s) {
+    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, c2, p, grid, s);
+    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, c2, p, grid, s);
+    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, c2, p, grid, s);
+    if (p.mcast && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, c2, p, grid, s);
+    return launch_impl<BN, KB, 0>(a, b, c, c2, p, grid, s);
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s) {
+                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s, const CUtensorMap* c2) {
+    if (p.split_col > 0 && (!c2 || !TcSmem<128, 1, 0>::kTmaStore || bn < 128)) return cudaErrorInvalidValue;
+    const CUtensorMap& cc2 = c2 ? *c2 : c;
     // grid: one persistent CTA per SM, a multiple of the number of N tiles
     const int grid = (num_sms / p.n_tiles) * p.n_tiles;
     if (p.epi == TC_EPI_BF16 && p.act_silu == 0 && p.bias) return cudaErrorInvalidValue;  // unsupported combo
-#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, c, p, grid, s);
+#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, c, cc2, p, grid, s);
     TCL_TC_CASE(256, 1) TCL_TC_CASE(256, 2) TCL_TC_CASE(256, 3) TCL_TC_CASE(256, 4)
     TCL_TC_CASE(128, 1) TCL_TC_CASE(128, 2) TCL_TC_CASE(128, 3) TCL_TC_CASE(128, 4)
     TCL_TC_CASE(64, 1) TCL_TC_CASE(64, 2) TCL_TC_CASE(64, 3) TCL_TC_CASE(64, 4)

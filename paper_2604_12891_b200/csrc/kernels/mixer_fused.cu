@@ -35,6 +35,7 @@
 #include "../kernels.h"
 #include "../kernels_mixer.h"
 #include "../tc_ptx.cuh"
+#include "mixer_common.cuh"
 
 namespace tcl {
 
@@ -58,47 +59,6 @@ struct MixerSmem {
     static constexpr int kStarts = kBar + 16;                      // u32 [kStartWords]
     static constexpr int kBytes = kStarts + 4 * kStartWords;
 };
-
-__device__ __forceinline__ uint32_t pk_bf16(float a, float b) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t addr) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(addr));
-}
-
-__device__ __forceinline__ void mma_16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
-}
-
-// softplus(v) = max(v, 0) + log(1 + y), y = e^{-|v|} in (0, 1]: one MUFU.EX2 for y, log1p(y) as
-// y * P4(y) on the FMA pipe (Chebyshev fit of log1p(y)/y on [0, 1], relative error 1.2e-4 in fp32
-// Horner form: an exponent error of 1.2e-4 |Delta A| in exp(Delta A), far below the bf16
-// rounding of the path).  The dt_proj phase issues 32 softplus per thread at once and was
-// MUFU-throttled with the former ex2 + lg2 pair.
-__device__ __forceinline__ float softplus_fast(float v) {
-    const float y = ex2(-fabsf(v) * kLog2e);
-    float p = fmaf(0.041064512f, y, -0.15602843f);
-    p = fmaf(p, y, 0.30467236f);
-    p = fmaf(p, y, -0.49636829f);
-    p = fmaf(p, y, 0.99988794f);
-    return fmaf(y, p, fmaxf(v, 0.0f));
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            tc::smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(tc::smem_u32(bar))
-        : "memory");
-}
 
 template <int DI, int N, int RP, int NXP, int DC, int DISC, int SU>
 __global__ void __launch_bounds__(DI, 2) k_mixer_fused(MixerArgs a) {

@@ -1,0 +1,500 @@
+// mixer_split.cu -- the Mamba mixer of the bf16 path as two kernels:
+//
+//   k_mixprep  u   = SiLU(b_conv + causal depthwise conv_{d_conv}(x))          (R4)
+//              [dt_r | B | C] = u W_x^T                                         (R7)
+//              Delta = softplus(dt_r W_dt^T + b_dt)
+//   k_scan     s_t = exp(Delta A) s_{t-1} + (exp(Delta A) - 1)/A * B_t u_t      (Eqs. 4-5 + ZOH; R5)
+//              y_t = C_t . s_t + D u_t ;  g_t = y_t * SiLU(z_t)                 (R6)
+//
+// Why two kernels: the recurrence is bound by the SFU (N MUFU.EX2 per (t, d)) and its own
+// FMA-pipe mix; the conv / x_proj / dt_proj / softplus work, when it shares the SM with the scan
+// (the one-kernel mixer, mixer_fused.cu), costs the scan ~30% of its issue slots (round 1
+// phase split: 2.73 ms scan alone vs 3.86 ms fused at `large`).  Here that work runs in an
+// HBM-bound kernel of its own, and the scan kernel does nothing but the recurrence.
+//
+// The two kernels meet in a per-token "mixer packet" (one row per packed token, written by three
+// producers, read by the scan as ONE contiguous bulk copy per 16-token chunk):
+//     [ u fp16 x DI | Delta fp16 x DI | B, C fp32 x 2N | SiLU(z) bf16 x DI ]      (6 DI + 8 N bytes)
+// u and Delta are stored in fp16 (10-bit mantissa: 8x finer than bf16; both are bounded: u is a
+// SiLU of a 4-tap conv, Delta a softplus), B and C in fp32; SiLU(z) comes from the in_proj
+// epilogue (bf16, the GEMM output precision of this path).
+//
+// Work decomposition (both kernels): persistent CTAs of DI threads, thread d owns channel d; each
+// CTA owns the packed rows of a contiguous candidate range (balanced by rows) and walks them in
+// 16-row chunks that may span candidates (conv window / SSM state reset at candidate starts, from
+// a start-bit array built once per CTA in shared memory).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+
+#include <algorithm>
+
+#include "../kernels.h"
+#include "../kernels_mixer.h"
+#include "../tc_ptx.cuh"
+#include "mixer_common.cuh"
+
+namespace tcl {
+namespace mx {
+
+constexpr int kTC = 16;          // tokens per chunk (= mma.sync M)
+constexpr int kStartWords = 1024; // start bits for up to 2,048 chunks per CTA (else walk cu[])
+
+// Candidate-start bits of rows [r0, r_end) in shared memory (16 bits per chunk).
+__device__ __forceinline__ bool build_start_bits(uint32_t* st_w, const int32_t* cu, const RowRange& rr, int nthr) {
+    const int64_t n_chunks = (rr.r_end - rr.r0 + kTC - 1) / kTC;
+    if ((n_chunks + 2) / 2 > kStartWords) return false;
+    const int nw = (int)(n_chunks + 2) / 2;
+    for (int w = threadIdx.x; w < nw; w += nthr) st_w[w] = 0u;
+    __syncthreads();
+    for (int64_t i = rr.c0 + threadIdx.x; i < rr.c1; i += nthr) {
+        const int64_t off = cu[i] - rr.r0;
+        atomicOr(&st_w[off >> 5], 1u << (off & 31));
+    }
+    __syncthreads();
+    return true;
+}
+
+// Start bits of the chunk at rows [r, r + tc): from shared memory, or by walking cu[] (k_next).
+__device__ __forceinline__ uint32_t chunk_starts(bool bits, const uint32_t* st_w, int chunk, const int32_t* cu,
+                                                 int64_t& k_next, int64_t c1, int64_t r, int tc) {
+    if (bits) return (st_w[chunk >> 1] >> ((chunk & 1) * 16)) & 0xFFFFu;
+    uint32_t starts = 0;
+    while (k_next < c1 && cu[k_next] < r + tc) {
+        starts |= 1u << (int)(cu[k_next] - r);
+        ++k_next;
+    }
+    return starts;
+}
+
+// ============================================================================ k_mixprep
+// Warp-per-chunk: every warp of the grid takes 16-row chunks of the packed rows (grid-stride over
+// the global chunk index, so no chunk depends on another and no CTA-wide barrier is needed); lane
+// l owns the CPL = DI / 32 consecutive channels [CPL l, CPL l + CPL).  Per chunk:
+//   0. the chunk's 16 rows of x plus the d_conv - 1 rows before it (the conv halo) were copied
+//      into the warp's shared-memory tile by cp.async while the previous chunk was finishing;
+//   1. conv + SiLU (taps that fall before the token's candidate start are dropped by select,
+//      never by multiplication); u goes to the packet as fp16 and replaces x in the tile as bf16
+//      (the x_proj A operand; each lane overwrites only the channels it has just read);
+//   2. x_proj: mma.sync m16n8k16 over K = DI (W_x staged once per CTA in shared memory), fp32
+//      accumulators in registers; B and C go to the packet from the fragments; the dt_r columns
+//      become the dt_proj A fragments in registers (the m16n8 C layout of n-tiles 2k, 2k+1 IS the
+//      m16k16 A layout); the tile is free now and the NEXT chunk's x is requested into it;
+//   3. dt_proj (K = RP) + bias + softplus -> Delta (fp16) to the packet from the fragments.
+// Every row's result is independent of the chunking (fixed tap and k order): batch-invariant.
+template <int DI, int N, int RP, int NXP, int DC>
+struct PrepSmem {
+    static constexpr int kWarps = 16;
+    static constexpr int kHalo = DC - 1;
+    static constexpr int kRows = kTC + kHalo;       // tile rows: halo, then the chunk
+    static constexpr int kWxld = DI + 8;            // bf16 row stride of W_x / the tile (+16 B: conflict-free ldmatrix)
+    static constexpr int kWx = 0;                                  // bf16 [NXP][DI + 8]
+    static constexpr int kWdt = kWx + NXP * kWxld * 2;             // bf16 [DI][RP]
+    static constexpr int kBdt = kWdt + DI * RP * 2;                // f32  [DI]
+    static constexpr int kTile = (kBdt + DI * 4 + 127) / 128 * 128;   // per warp: bf16 [kRows][DI + 8]
+    static constexpr int kBytes = kTile + kWarps * kRows * kWxld * 2;
+    static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per block");
+};
+
+template <int CPL> struct LaneVec;
+template <> struct LaneVec<8> { using T = uint4; };
+template <> struct LaneVec<4> { using T = uint2; };
+template <> struct LaneVec<2> { using T = uint32_t; };
+
+template <int BYTES>
+__device__ __forceinline__ void cp_async(void* dst, const void* src) {
+    if constexpr (BYTES == 16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(dst)), "l"(src) : "memory");
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], %2;" ::"r"(tc::smem_u32(dst)), "l"(src), "n"(BYTES)
+                     : "memory");
+}
+
+template <int DI, int N, int RP, int NXP, int DC>
+__global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
+    using L = PrepSmem<DI, N, RP, NXP, DC>;
+    constexpr int CPL = DI / 32;                     // channels per lane
+    constexpr int H = L::kHalo;
+    using V = typename LaneVec<CPL>::T;
+    constexpr int NT_X = NXP / 8;                    // x_proj n-tiles
+    constexpr int KS_DT = RP / 16;                   // dt_proj k-steps
+    extern __shared__ __align__(128) uint8_t msm[];
+    __nv_bfloat16* wx_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kWx);
+    __nv_bfloat16* wdt_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kWdt);
+    float* bdt_s = reinterpret_cast<float*>(msm + L::kBdt);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, tq = lane & 3;
+    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(msm + L::kTile) + warp * L::kRows * L::kWxld;
+
+    // ---- once per CTA: W_x, W_dt, b_dt into shared memory; this lane's conv taps in registers
+    for (int idx = threadIdx.x; idx < NXP * DI / 8; idx += blockDim.x) {
+        const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
+        *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
+            __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
+    }
+    for (int idx = threadIdx.x; idx < DI * RP / 8; idx += blockDim.x)
+        *reinterpret_cast<uint4*>(wdt_s + idx * 8) = __ldg(reinterpret_cast<const uint4*>(a.Wdt_b) + idx);
+    for (int idx = threadIdx.x; idx < DI; idx += blockDim.x) bdt_s[idx] = __ldg(a.b_dt + idx);
+    // conv taps / bias of this lane's channel pairs, pre-halved: SiLU(v) = h (1 + tanh h), h = v / 2
+    constexpr int CP = CPL / 2;
+    float2 wc[CP][DC], bc[CP];
+#pragma unroll
+    for (int c = 0; c < CP; ++c) {
+        const int ch = CPL * lane + 2 * c;
+        bc[c] = make_float2(0.5f * __ldg(a.b_conv + ch), 0.5f * __ldg(a.b_conv + ch + 1));
+#pragma unroll
+        for (int k = 0; k < DC; ++k)
+            wc[c][k] = make_float2(0.5f * __ldg(a.w_conv + ch * DC + k), 0.5f * __ldg(a.w_conv + (ch + 1) * DC + k));
+    }
+    __syncthreads();
+
+    const int64_t P = a.cu[a.n];
+    const int64_t n_chunks = (P + kTC - 1) / kTC;
+    const int64_t wstep = (int64_t)gridDim.x * L::kWarps;
+    const __nv_bfloat16* __restrict__ X = a.X;
+    uint8_t* __restrict__ pk = a.Pk;
+    // x rows [r0 - H, r0 + 16) of chunk ck -> the tile (rows outside [0, P) are not copied: the
+    // halo ones are masked by the candidate positions, the tail ones produce no output)
+    auto fetch = [&](int64_t ck) {
+        if (ck >= n_chunks) return;
+        const int64_t rb = ck * kTC - H;
+#pragma unroll
+        for (int t = 0; t < L::kRows; ++t) {
+            const int64_t r = rb + t;
+            if (r >= 0 && r < P) cp_async<CPL * 2>(tile + t * L::kWxld + CPL * lane, X + r * DI + CPL * lane);
+        }
+        asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    // token position inside its candidate for rows ck * 16 + lane (lanes 0..15): two dependent
+    // global loads, issued one chunk ahead like the x rows
+    auto positions = [&](int64_t ck) -> int {
+        const int64_t r = ck * kTC + lane;
+        return (ck < n_chunks && lane < kTC && r < P) ? (int)(r - __ldg(a.cu + __ldg(a.row_cand + r))) : 0;
+    };
+    int64_t ck = (int64_t)blockIdx.x * L::kWarps + warp;
+    fetch(ck);
+    int tpos_next = positions(ck);
+    for (; ck < n_chunks; ck += wstep) {
+        const int64_t r0 = ck * kTC;
+        const int tc = (int)(P - r0 < kTC ? P - r0 : kTC);
+        const int tpos = tpos_next;
+        asm volatile("cp.async.wait_group 0;" ::: "memory");
+        __syncwarp();
+        // ---- 1. conv + SiLU.  win[j] = x at row t - 1 - j (channel pairs, packed fp32x2 math)
+        float2 win[H][CP];
+#pragma unroll
+        for (int j = 0; j < H; ++j) {
+            const V v = *reinterpret_cast<const V*>(tile + (H - 1 - j) * L::kWxld + CPL * lane);
+            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+            for (int c = 0; c < CP; ++c) win[j][c] = __bfloat1622float2(e[c]);
+        }
+#pragma unroll
+        for (int t = 0; t < kTC; ++t) {
+            const int tp = __shfl_sync(0xffffffffu, tpos, t);   // warp-uniform: the branches below do not diverge
+            __nv_bfloat16* trow = tile + (H + t) * L::kWxld + CPL * lane;
+            const V v = *reinterpret_cast<const V*>(trow);
+            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
+            float2 x[CP], h[CP];
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+                x[c] = __bfloat1622float2(e[c]);
+                h[c] = __ffma2_rn(wc[c][DC - 1], x[c], bc[c]);
+            }
+            if (tp >= H) {   // every tap inside the candidate (all but its first d_conv - 1 tokens)
+#pragma unroll
+                for (int j = 0; j < H; ++j)
+#pragma unroll
+                    for (int c = 0; c < CP; ++c) h[c] = __ffma2_rn(wc[c][DC - 2 - j], win[j][c], h[c]);
+            } else {         // taps before the candidate start are dropped
+#pragma unroll
+                for (int j = 0; j < H; ++j)
+                    if (tp > j)
+#pragma unroll
+                        for (int c = 0; c < CP; ++c) h[c] = __ffma2_rn(wc[c][DC - 2 - j], win[j][c], h[c]);
+            }
+#pragma unroll
+            for (int j = H - 1; j > 0; --j)
+#pragma unroll
+                for (int c = 0; c < CP; ++c) win[j][c] = win[j - 1][c];
+            V uh, ub;
+            __half2* uh2 = reinterpret_cast<__half2*>(&uh);
+            __nv_bfloat162* ub2 = reinterpret_cast<__nv_bfloat162*>(&ub);
+#pragma unroll
+            for (int c = 0; c < CP; ++c) {
+                win[0][c] = x[c];
+                float2 th;
+                asm("tanh.approx.f32 %0, %1;" : "=f"(th.x) : "f"(h[c].x));
+                asm("tanh.approx.f32 %0, %1;" : "=f"(th.y) : "f"(h[c].y));
+                const float2 u = __ffma2_rn(h[c], th, h[c]);
+                uh2[c] = __float22half2_rn(u);
+                ub2[c] = __float22bfloat162_rn(u);
+            }
+            *reinterpret_cast<V*>(trow) = ub;   // x of this row is no longer needed (read above)
+            if (t < tc) *reinterpret_cast<V*>(pk + (r0 + t) * (int64_t)a.pk_ld + 2 * CPL * lane) = uh;
+        }
+        __syncwarp();
+        // ---- 2. x_proj: acc[nt] = u[16][DI] . W_x[nt*8 .. +8][DI]^T
+        float acc[NT_X][4];
+#pragma unroll
+        for (int nt = 0; nt < NT_X; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
+        {
+            const uint32_t a_addr = tc::smem_u32(tile + (H + (lane & 15)) * L::kWxld + 8 * (lane >> 4));
+            const uint32_t b_addr = tc::smem_u32(wx_s + (lane & 7) * L::kWxld + 8 * (lane >> 3));
+#pragma unroll 2
+            for (int k0 = 0; k0 < DI; k0 += 32) {
+                uint32_t af[4], af2[4];
+                ldsm_x4(af, a_addr + k0 * 2);
+                ldsm_x4(af2, a_addr + (k0 + 16) * 2);
+#pragma unroll
+                for (int nt = 0; nt < NT_X; ++nt) {
+                    uint32_t bf[4];
+                    ldsm_x4(bf, b_addr + (nt * 8 * L::kWxld + k0) * 2);
+                    mma_16816(acc[nt], af, bf[0], bf[1]);
+                    mma_16816(acc[nt], af2, bf[2], bf[3]);
+                }
+            }
+        }
+        __syncwarp();               // every ldmatrix of the tile is done: request the next chunk's x
+        fetch(ck + wstep);
+        tpos_next = positions(ck + wstep);
+        // B, C columns [R, R + 2N) to the packet; dt_r columns [0, R) -> dt_proj A fragments
+        const bool row_lo = g < tc, row_hi = g + 8 < tc;
+        uint8_t* prow_lo = pk + (r0 + g) * (int64_t)a.pk_ld;
+        uint8_t* prow_hi = pk + (r0 + g + 8) * (int64_t)a.pk_ld;
+#pragma unroll
+        for (int nt = 0; nt < NT_X; ++nt) {
+            const int c = nt * 8 + 2 * tq;
+            if (c >= a.R && c < a.R + 2 * N) {
+                if (row_lo) *reinterpret_cast<float2*>(prow_lo + 4 * DI + 4 * (c - a.R)) = make_float2(acc[nt][0], acc[nt][1]);
+                if (row_hi) *reinterpret_cast<float2*>(prow_hi + 4 * DI + 4 * (c - a.R)) = make_float2(acc[nt][2], acc[nt][3]);
+            }
+        }
+        uint32_t adt[KS_DT][4];
+#pragma unroll
+        for (int ks = 0; ks < KS_DT; ++ks) {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int nt = 2 * ks + h < NT_X ? 2 * ks + h : 0;
+                const bool ok = 2 * ks + h < NT_X && (2 * ks + h) * 8 + 2 * tq < a.R;   // R % 4 == 0 (validated)
+                adt[ks][2 * h] = ok ? pk_bf16(acc[nt][0], acc[nt][1]) : 0u;
+                adt[ks][2 * h + 1] = ok ? pk_bf16(acc[nt][2], acc[nt][3]) : 0u;
+            }
+        }
+        // ---- 3. dt_proj + bias + softplus -> Delta (fp16) to the packet
+#pragma unroll 4
+        for (int j = 0; j < DI / 8; ++j) {
+            float c4[4] = {0.f, 0.f, 0.f, 0.f};
+            const __nv_bfloat16* wrow = wdt_s + (j * 8 + g) * RP + 2 * tq;
+#pragma unroll
+            for (int ks = 0; ks < KS_DT; ++ks)
+                mma_16816(c4, adt[ks], *reinterpret_cast<const uint32_t*>(wrow + ks * 16),
+                          *reinterpret_cast<const uint32_t*>(wrow + ks * 16 + 8));
+            const int c = j * 8 + 2 * tq;
+            const float2 b2 = *reinterpret_cast<const float2*>(bdt_s + c);
+            const float2 lo = softplus_fast2(__fadd2_rn(make_float2(c4[0], c4[1]), b2));
+            const float2 hi = softplus_fast2(__fadd2_rn(make_float2(c4[2], c4[3]), b2));
+            if (row_lo) *reinterpret_cast<__half2*>(prow_lo + 2 * DI + 2 * c) = __float22half2_rn(lo);
+            if (row_hi) *reinterpret_cast<__half2*>(prow_hi + 2 * DI + 2 * c) = __float22half2_rn(hi);
+        }
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+}
+
+// ============================================================================ k_scan
+template <int DI, int N, int STAGES>
+struct ScanSmem {
+    static constexpr int kRow = 6 * DI + 8 * N;                    // packet row bytes
+    static constexpr int kPk = 0;                                  // [STAGES][16][kRow]
+    static constexpr int kBar = kPk + STAGES * kTC * kRow;         // STAGES mbarriers
+    static constexpr int kStarts = kBar + 8 * STAGES + 8;
+    static constexpr int kBytes = kStarts + 4 * kStartWords;
+};
+
+template <int DI, int N, int DISC, int STAGES, int MINB>
+__global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
+    using L = ScanSmem<DI, N, STAGES>;
+    constexpr int kRow = L::kRow;
+    extern __shared__ __align__(128) uint8_t msm[];
+    uint8_t* pk_s = msm + L::kPk;
+    uint64_t* bar = reinterpret_cast<uint64_t*>(msm + L::kBar);
+    uint32_t* st_w = reinterpret_cast<uint32_t*>(msm + L::kStarts);
+    const int d = threadIdx.x;
+
+    float2 A2[N / 2], iA[N / 2];
+#pragma unroll
+    for (int n = 0; n < N / 2; ++n) {
+        A2[n] = __ldg(reinterpret_cast<const float2*>(a.A2 + d * N) + n);
+        if (DISC == 0) iA[n] = __ldg(reinterpret_cast<const float2*>(a.invA + d * N) + n);
+    }
+    const float Dv = __ldg(a.Dv + d);
+    if (d == 0) {
+        for (int b = 0; b < STAGES; ++b) tc::mbar_init(&bar[b], 1);
+        tc::fence_mbar_init();
+    }
+    __syncthreads();
+    const RowRange rr = cta_rows(a.cu, a.n);
+    const bool bits = build_start_bits(st_w, a.cu, rr, DI);
+    int64_t k_next = rr.c0;
+    auto issue = [&](int64_t r, int b) {
+        if (d == 0 && r < rr.r_end) {
+            const uint32_t bytes = (uint32_t)(rr.r_end - r < kTC ? rr.r_end - r : kTC) * kRow;
+            tc::mbar_arrive_expect_tx(&bar[b], bytes);
+            bulk_g2s(pk_s + b * kTC * kRow, a.Pk + r * (int64_t)kRow, bytes, &bar[b]);
+        }
+    };
+#pragma unroll
+    for (int b = 0; b < STAGES; ++b) issue(rr.r0 + (int64_t)b * kTC, b);
+    uint32_t parity = 0;
+    float2 s[N / 2];
+#pragma unroll
+    for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+    int buf = 0, chunk = 0;
+    for (int64_t r0 = rr.r0; r0 < rr.r_end; r0 += kTC, ++chunk) {
+        const int tc = (int)(rr.r_end - r0 < kTC ? rr.r_end - r0 : kTC);
+        const uint32_t starts = chunk_starts(bits, st_w, chunk, a.cu, k_next, rr.c1, r0, tc);
+        tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
+        parity ^= 1u << buf;
+        const uint8_t* row = pk_s + buf * kTC * kRow;
+        __nv_bfloat16* gout = a.G + r0 * DI + d;
+        // one token: the row pointer advances by a compile-time stride, so in the unrolled
+        // full-chunk loop every shared-memory access is base + immediate
+        auto scan_tok = [&](int tt) {
+            if ((starts >> tt) & 1u) {
+#pragma unroll
+                for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+            }
+            const float u = __half2float(reinterpret_cast<const __half*>(row)[d]);
+            const float dl = __half2float(reinterpret_cast<const __half*>(row + 2 * DI)[d]);
+            const float4* B4 = reinterpret_cast<const float4*>(row + 4 * DI);
+            const float4* C4 = reinterpret_cast<const float4*>(row + 4 * DI + 4 * N);
+            const float gz = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row + 4 * DI + 8 * N)[d]);
+            const float2 dl2 = make_float2(dl, dl);
+            const float2 u2 = make_float2(u, u);
+            float2 y2 = make_float2(0.f, 0.f), y2b = make_float2(0.f, 0.f);
+            if (DISC == 1) {   // Euler-B: Bbar = Delta B
+                const float2 du2 = __fmul2_rn(dl2, u2);
+#pragma unroll
+                for (int q = 0; q < N / 4; ++q) {
+                    const float4 b4 = B4[q], c4 = C4[q];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = 2 * q + h;
+                        const float2 x2 = __fmul2_rn(dl2, A2[n]);
+                        const float2 ab = make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
+                        const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+                        s[n] = __ffma2_rn(ab, s[n], __fmul2_rn(bb, du2));
+                        if (h) y2b = __ffma2_rn(cc, s[n], y2b); else y2 = __ffma2_rn(cc, s[n], y2);
+                    }
+                }
+            } else {           // ZOH: Bbar u = (Abar - 1) v, v = B u / A;  s <- Abar (s + v) - v
+#pragma unroll
+                for (int q = 0; q < N / 4; ++q) {
+                    const float4 b4 = B4[q], c4 = C4[q];
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int n = 2 * q + h;
+                        const float2 x2 = __fmul2_rn(dl2, A2[n]);
+                        const float2 ab = make_float2(ex2(x2.x), ex2(x2.y));
+                        const float2 bb = h ? make_float2(b4.z, b4.w) : make_float2(b4.x, b4.y);
+                        const float2 cc = h ? make_float2(c4.z, c4.w) : make_float2(c4.x, c4.y);
+                        const float2 v = __fmul2_rn(__fmul2_rn(bb, u2), iA[n]);
+                        const float2 t = __fadd2_rn(s[n], v);
+                        s[n] = __ffma2_rn(ab, t, make_float2(-v.x, -v.y));
+                        if (h) y2b = __ffma2_rn(cc, s[n], y2b); else y2 = __ffma2_rn(cc, s[n], y2);
+                    }
+                }
+            }
+            const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
+            gout[0] = __float2bfloat16_rn(y * gz);
+            row += kRow;
+            gout += DI;
+        };
+        if (tc == kTC) {
+#pragma unroll 1
+            for (int t0 = 0; t0 < kTC; t0 += 2) {
+                scan_tok(t0);
+                scan_tok(t0 + 1);
+            }
+        } else {
+#pragma unroll 1
+            for (int tt = 0; tt < tc; ++tt) scan_tok(tt);
+        }
+        __syncthreads();   // every thread is done with this buffer: refill it STAGES chunks ahead
+        issue(r0 + (int64_t)STAGES * kTC, buf);
+        if (++buf == STAGES) buf = 0;
+    }
+}
+
+// ============================================================================ launchers
+template <int DI, int N, int RP, int NXP>
+static cudaError_t prep_launch(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
+    using L = PrepSmem<DI, N, RP, NXP, 4>;
+    constexpr int smem = L::kBytes;
+    auto kern = k_mixprep<DI, N, RP, NXP, 4>;
+    cudaError_t e = prepare_kernel(kern, smem);
+    if (e != cudaSuccess) return e;
+    // one CTA of 16 warps per SM; never more CTAs than 16-row chunks need (the chunk count is
+    // bounded by the row capacity of the batch, n * max_len, so the grid does not depend on P)
+    const int64_t chunks_max = (a.n * (int64_t)a.max_len + kTC - 1) / kTC;
+    int64_t grid = std::min<int64_t>(num_sms, (chunks_max + L::kWarps - 1) / L::kWarps);
+    kern<<<(unsigned)std::max<int64_t>(grid, 1), 32 * L::kWarps, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int DI, int N, int DISC>
+static cudaError_t scan_launch(const ScanBf16Args& a, int num_sms, cudaStream_t s) {
+    // 3 CTAs of DI threads per SM at DI = 256 (24 warps: the scan is latency-sensitive), each with
+    // a 2-chunk packet ring; smaller DI packs more CTAs
+    constexpr int MINB = DI == 256 ? 3 : (DI == 128 ? 6 : 8);
+    constexpr int STAGES = 2;
+    constexpr int smem = ScanSmem<DI, N, STAGES>::kBytes;
+    auto kern = k_scan<DI, N, DISC, STAGES, MINB>;
+    int bps = 1;
+    cudaError_t e = prepare_kernel(kern, smem, DI, &bps);
+    if (e != cudaSuccess) return e;
+    int64_t grid = (int64_t)num_sms * bps;
+    if (grid > a.n) grid = a.n;
+    kern<<<(unsigned)grid, DI, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+template <int DI, int N>
+static cudaError_t prep_rp(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
+    const int nxp = ((a.R + 2 * N) + 7) / 8 * 8;
+    if (a.RP == 16) {
+        if (nxp <= 24) return prep_launch<DI, N, 16, 24>(a, num_sms, s);
+        if (nxp <= 48) return prep_launch<DI, N, 16, 48>(a, num_sms, s);
+    } else if (a.RP == 32) {
+        if (nxp <= 64) return prep_launch<DI, N, 32, 64>(a, num_sms, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace mx
+
+int mixer_packet_bytes(int di, int N) { return 6 * di + 8 * N; }
+
+cudaError_t launch_mixprep(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
+    using namespace mx;
+    if (a.n == 0) return cudaSuccess;
+    if (a.d_conv != 4 || a.pk_ld != mixer_packet_bytes(a.DI, a.N)) return cudaErrorInvalidValue;
+    if (a.DI == 256) return a.N == 16 ? prep_rp<256, 16>(a, num_sms, s) : prep_rp<256, 8>(a, num_sms, s);
+    if (a.DI == 128) return a.N == 16 ? prep_rp<128, 16>(a, num_sms, s) : prep_rp<128, 8>(a, num_sms, s);
+    if (a.DI == 64) return a.N == 16 ? prep_rp<64, 16>(a, num_sms, s) : prep_rp<64, 8>(a, num_sms, s);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_scan_bf16(const ScanBf16Args& a, int num_sms, cudaStream_t s) {
+    using namespace mx;
+    if (a.n == 0) return cudaSuccess;
+#define TCL_SCAN_CASE(DI_, N_)                                                                     \
+    if (a.DI == DI_ && a.N == N_)                                                                  \
+        return a.disc == 1 ? scan_launch<DI_, N_, 1>(a, num_sms, s) : scan_launch<DI_, N_, 0>(a, num_sms, s);
+    TCL_SCAN_CASE(256, 16) TCL_SCAN_CASE(256, 8) TCL_SCAN_CASE(128, 16) TCL_SCAN_CASE(128, 8)
+    TCL_SCAN_CASE(64, 16) TCL_SCAN_CASE(64, 8)
+#undef TCL_SCAN_CASE
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace tcl

@@ -51,7 +51,7 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_train_read", "tcl_set_option"]
 TCL_OPT_GRAPHS = 1
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
-              "head", "topk", "mixer", "allgather", "mc", "lateral"]
+              "head", "topk", "mixer", "allgather", "mc", "lateral", "mixprep"]
 
 _lib: Optional[ctypes.CDLL] = None
 

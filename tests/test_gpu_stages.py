@@ -50,7 +50,7 @@ def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
     d, w, f, l, m, scores = _run(torch_cuda, name, prec)
     P = int(l.sum())
     di, dm = d.d_inner, d.d_model
-    stages = {k: [] for k in ("a", "x", "z", "g", "h")}
+    stages = {k: [] for k in ("a", "x", "z", "u", "delta", "B", "C", "g", "h")}
     ref_scores = []
     for i in range(len(l)):
         sc, st = oracle.forward_one(d, w, f[i], int(l[i]))
@@ -82,6 +82,15 @@ def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
         rep["z"] = _close(XZ[:, di:], zr / (1.0 + np.exp(-zr)), rtol, "in_proj SiLU(z)")
     else:
         rep["z"] = _close(XZ[:, di:], ref["z"], rtol, "in_proj z")
+    # the mixer's intermediates: conv + SiLU output u, Delta = softplus(dt_proj), x_proj's B and C
+    if prec == 1:   # (the fp32 path's fused mixer keeps them on chip)
+        U = m.debug_read("U", P, di)
+        DL = m.debug_read("DELTA", P, di)
+        rep["u"] = _close(U, ref["u"], rtol, "conv + SiLU u")
+        rep["delta"] = _close(DL, ref["delta"], rtol, "Delta")
+        BC = m.debug_read("BC", P, 2 * d.d_state)
+        rep["B"] = _close(BC[:, :d.d_state], ref["B"], rtol, "B")
+        rep["C"] = _close(BC[:, d.d_state:], ref["C"], rtol, "C")
     rep["g"] = _close(G, ref["g"], rtol, "gated scan output")
     if not lnf_path:
         rep["h"] = _close(H, ref["h"], rtol, "residual after layer 0")
