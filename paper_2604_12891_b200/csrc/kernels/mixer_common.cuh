@@ -1,5 +1,5 @@
-// mixer_common.cuh -- device helpers shared by the bf16-path mixer kernels (mixer_fused.cu,
-// mixer_split.cu): warp-level MMA fragments, the one-MUFU softplus and the bulk-copy wrappers.
+// mixer_common.cuh -- device helpers of the bf16-path mixer kernels (mixer_split.cu): warp-level
+// MMA fragments, the one-MUFU softplus and the bulk-copy wrappers.
 #pragma once
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
