@@ -149,6 +149,16 @@ def stage_model(d, P: int, n: int):
     }
 
 
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -162,6 +172,9 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--precision", choices=["config", "fp32", "bf16"], default="config",
                     help="override the configuration's precision (fp32 path / bf16 projections)")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
+                    help="weak: n candidates per GPU (default); strong: the config's n split over the GPUs "
+                         "(SURVEY §8(e): rank r scores the contiguous shard r, global top-k over all)")
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules; using 3", file=sys.stderr)
@@ -220,7 +233,8 @@ def run_reference(args, cfg, d, n, k, world, rank):
                        "d_state": d.d_state, "mc_passes": passes},
             "cpu_baseline": {"value": value, "unit": "candidates/s", "cores": cores, "kind": "oracle",
                              "sample": f"{sample} candidates of the {args.config} workload per step "
-                                       f"(fp64 C oracle, {cores} threads)"},
+                                       f"(fp64 C oracle, {cores} threads)", "cpu_model": cpu_model(),
+                             "nproc": os.cpu_count()},
             "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
     print(json.dumps(line), flush=True)
@@ -237,8 +251,18 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     peaks = load_peaks()
     w = inputs.make_weights(d, cfg["seed"])
-    feats, lens = inputs.make_features(d, n, cfg["seed"] + 1 + 7919 * rank, workload=FEATURE_WORKLOAD[args.config])
-    index_base = rank * n
+    if args.scaling == "strong":
+        # one global batch of n candidates, rank r takes its contiguous shard (global index = start + i)
+        from paper_2604_12891_b200.tcl import shard_range
+        fg, lg = inputs.make_features(d, n, cfg["seed"] + 1, workload=FEATURE_WORKLOAD[args.config])
+        index_base, n_loc = shard_range(n, world, rank)
+        feats, lens = np.ascontiguousarray(fg[index_base:index_base + n_loc]), lg[index_base:index_base + n_loc].copy()
+        n_total = n
+        n = n_loc
+    else:
+        feats, lens = inputs.make_features(d, n, cfg["seed"] + 1 + 7919 * rank, workload=FEATURE_WORKLOAD[args.config])
+        index_base = rank * n
+        n_total = n * world
     P = int(lens.sum())
     m = Model(w, d, device=local_rank)
     m.reserve(n)
@@ -271,9 +295,9 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         step()
     m.tcl_sync_error(stream=stream)
 
-    # ---------------- timed region (device time, CUDA events on the launching stream)
-    m.profile_enable(True)
-    m.profile_read(reset=True)
+    # ---------------- timed region (device time, CUDA events on the launching stream).  Repeated
+    # calls replay CUDA graphs (TCL_OPT_GRAPHS, captured during the warm-up); every step recomputes
+    # the whole path from the device-resident inputs.
     clocks = ClockSampler(local_rank)
     if world > 1:
         dist.barrier()
@@ -291,15 +315,23 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    # ---------------- per-kernel device times: the same steps again with every launch bracketed by
+    # CUDA events on the launching stream (direct launches; the headline number above is unprofiled)
+    m.profile_enable(True)
+    m.profile_read(reset=True)
+    for _ in range(args.steps):
+        step()
+    torch.cuda.synchronize()
     prof = m.profile_read(reset=True)
     m.profile_enable(False)
-    ms = ev0.elapsed_time(ev1)
+    ms_prof = sum(v[0] for v in prof.values())
     if world > 1:
         t = torch.tensor([ms], device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = n * world / (ms_step * 1e-3)
+    value = n_total / (ms_step * 1e-3)
 
     # ---------------- roofline of the dominant kernel (live CUDA-event stage times)
     work = stage_model(d, P, n)
@@ -307,7 +339,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     kernels = {}
     for kind, (tot_ms, cnt) in prof.items():
         per = tot_ms / cnt
-        kernels[kind] = {"ms_per_launch": per, "launches": cnt, "share": tot_ms / ms}
+        kernels[kind] = {"ms_per_launch": per, "launches": cnt, "share": tot_ms / ms_prof}
     per_step_launches = {kind: cnt / args.steps for kind, (_, cnt) in prof.items()}
     for kind, entry in kernels.items():
         wk = work.get(kind, {})
@@ -387,7 +419,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
             t = torch.tensor([ems], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": n * world / (ems / args.steps * 1e-3), "unit": "candidates/s",
+        e2e = {"value": n_total / (ems / args.steps * 1e-3), "unit": "candidates/s",
                "h2d_bytes_per_step": int(feats.nbytes + lens.nbytes),
                "d2h_bytes_per_step": int(n * 4 + k * 12),
                "ms_per_step": ems / args.steps}
@@ -408,20 +440,30 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         else:
             O.score(d, w, feats[:sample], lens[:sample], nthreads=cores)
         dt = time.perf_counter() - t0
+        # one thread on a sixteenth of the sample (the per-core rate)
+        s1 = max(1, sample // 16)
+        t1 = time.perf_counter()
+        if mc:
+            O.score_mc(d, w, feats[:s1], lens[:s1], mc, 1234, 0, nthreads=1)
+        else:
+            O.score(d, w, feats[:s1], lens[:s1], nthreads=1)
+        dt1 = time.perf_counter() - t1
         cpu = {"value": sample / dt, "unit": "candidates/s", "cores": cores, "kind": "oracle",
                "sample": f"first {sample} of the {n} candidates of this workload "
-                         f"(fp64 C oracle, gcc -O2, {cores} threads, {dt:.1f} s)"}
+                         f"(fp64 C oracle, gcc -O2, {cores} threads, {dt:.1f} s)",
+               "cpu_model": cpu_model(), "nproc": os.cpu_count(),
+               "one_thread": {"value": s1 / dt1, "unit": "candidates/s", "sample": f"first {s1} candidates, 1 thread, {dt1:.1f} s"}}
 
     if rank == 0:
         dtype = "bf16+f32" if d.precision == inputs.PREC_BF16_PROJ else "f32"
         line = {
             "metric": METRIC, "value": value, "unit": "candidates/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": dtype, "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT[args.config], "config": args.config,
                        "precision": "bf16 projections" if d.precision == inputs.PREC_BF16_PROJ else "fp32",
-                       "n_per_gpu": n, "global_n": n * world, "packed_tokens_per_gpu": P,
+                       "n_per_gpu": n, "global_n": n_total, "packed_tokens_per_gpu": P,
                        "max_len": d.max_len, "d_model": d.d_model, "n_layer": d.n_layer,
                        "d_state": d.d_state, "topk": k, "mc_passes": mc,
                        "parallelism": f"dp{world} (candidate shards, all-gather top-k)",
@@ -432,6 +474,8 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
             "gpu_launches": launches,
             "clocks": clk,
             "kernels": kernels,
+            "kernel_times": "per-launch CUDA events on the launching stream, in a re-run of the timed steps "
+                            "with direct launches (the timed steps replay CUDA graphs)",
             "peaks": {"hbm_gbs": peaks["hbm"], "bf16_tflops": peaks["bf16"], "ex2_per_s": mb["ex2"],
                       "ffma_per_s": mb["ffma"], "ffma2_lanes_per_s": mb.get("ffma2"),
                       "tanh_per_s": mb.get("tanh"), "scanmix_ex2_per_s": mb.get("scanmix"), "source": peaks["source"], "issue_source": mb["source"]},

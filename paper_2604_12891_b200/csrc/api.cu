@@ -286,6 +286,7 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
 static tcl_status ensure_topk_tmp(tcl_model* m, int64_t n, int k) {
     size_t need = (size_t)k + topk_tmp_keys(std::max<int64_t>(n, 1), k) + (size_t)k;
     if (need <= m->topk_tmp_cap) return TCL_OK;
+    ++m->ws_gen;
     if (m->topk_tmp) cudaFree(m->topk_tmp);
     m->topk_tmp = nullptr;
     m->topk_tmp_cap = 0;
@@ -525,10 +526,13 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     run_head(m, lens, n, scores, drop, mc_mean, s);
 }
 
+static bool debug_sync_on() {   // TCL_DEBUG_SYNC=1: synchronise and check after every launch (debugging)
+    static const bool on = [] { const char* e = getenv("TCL_DEBUG_SYNC"); return e && e[0] == '1'; }();
+    return on;
+}
+
 static tcl_status debug_sync(const char* where, cudaStream_t s) {
-    static int on = -1;
-    if (on < 0) { const char* e = getenv("TCL_DEBUG_SYNC"); on = (e && e[0] == '1') ? 1 : 0; }
-    if (!on) return TCL_OK;
+    if (!debug_sync_on()) return TCL_OK;
     cudaError_t e = cudaStreamSynchronize(s);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, where);
@@ -675,6 +679,65 @@ static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* l
     const cudaError_t e = cudaGetLastError();   // launch-configuration errors of the fp32 kernels
     if (e != cudaSuccess) return cuda_error(e, m->kb ? "forward_chunk_kbac" : "forward_chunk");
     return debug_sync(m->kb ? "forward_chunk_kbac" : "forward_chunk", s);
+}
+
+// ------------------------------------------------------------------------------ CUDA graphs
+// A repeated call (same kind, pointers, sizes, seeds, scratch generation) is replayed from a
+// CUDA graph: the first occurrence launches directly, the second is captured (on a private stream,
+// thread-local capture mode) and launched on the caller's stream, later ones only replay.  The
+// launch sequence of a call depends on nothing but its key, so a replay is bit-identical to the
+// direct launches (tested).  Per-stage profiling and TCL_DEBUG_SYNC always launch directly.
+static bool debug_sync_on();
+constexpr size_t kMaxGraphs = 8, kMaxSeen = 16;
+
+template <class F>
+static tcl_status run_graphed(tcl_model* m, const GraphKey& key, cudaStream_t s, F&& enqueue) {
+    if (!m->use_graphs || m->prof_on || debug_sync_on()) return enqueue(s);
+    for (GraphEntry& g : m->graphs) {
+        if (g.key == key) {
+            g.stamp = ++m->graph_clock;
+            CUDA_TRY(cudaGraphLaunch(g.exec, s));
+            m->launches += g.launches;
+            return TCL_OK;
+        }
+    }
+    auto it = std::find(m->seen.begin(), m->seen.end(), key);
+    if (it == m->seen.end()) {   // first occurrence: direct launches
+        if (m->seen.size() >= kMaxSeen) m->seen.erase(m->seen.begin());
+        m->seen.push_back(key);
+        return enqueue(s);
+    }
+    m->seen.erase(it);
+    if (!m->cap_stream) CUDA_TRY(cudaStreamCreateWithFlags(&m->cap_stream, cudaStreamNonBlocking));
+    const int64_t before = m->launches;
+    CUDA_TRY(cudaStreamBeginCapture(m->cap_stream, cudaStreamCaptureModeThreadLocal));
+    const tcl_status st = enqueue(m->cap_stream);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(m->cap_stream, &graph);
+    const int64_t nl = m->launches - before;
+    m->launches = before;
+    if (st != TCL_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ce != cudaSuccess) return cuda_error(ce, "graph capture");
+    GraphEntry g;
+    g.key = key;
+    g.launches = nl;
+    const cudaError_t ie = cudaGraphInstantiate(&g.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) return cuda_error(ie, "graph instantiate");
+    if (m->graphs.size() >= kMaxGraphs) {   // evict the least recently used
+        auto lru = std::min_element(m->graphs.begin(), m->graphs.end(),
+                                    [](const GraphEntry& a, const GraphEntry& b) { return a.stamp < b.stamp; });
+        cudaGraphExecDestroy(lru->exec);
+        m->graphs.erase(lru);
+    }
+    g.stamp = ++m->graph_clock;
+    m->graphs.push_back(g);
+    CUDA_TRY(cudaGraphLaunch(g.exec, s));
+    m->launches += nl;
+    return TCL_OK;
 }
 
 static int64_t chunk_cap(const tcl_model* m) {
@@ -857,6 +920,8 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     cudaDeviceSynchronize();
     free_workspace(m);
     comm_destroy(m);
+    for (GraphEntry& g : m->graphs) cudaGraphExecDestroy(g.exec);
+    if (m->cap_stream) cudaStreamDestroy(m->cap_stream);
     for (void* q : {(void*)m->w_dev, (void*)m->W1p, (void*)m->A2, (void*)m->invA, (void*)m->d_err,
                     (void*)m->topk_tmp, (void*)m->keys_send, (void*)m->keys_recv,
                     (void*)m->stage_feats, (void*)m->stage_lens, (void*)m->stage_scores,
@@ -892,15 +957,23 @@ tcl_status tcl_score(tcl_model* m, const float* feats, const int32_t* lens, int6
     const int64_t cap = chunk_cap(m);
     tcl_status st = ensure_workspace(m, std::min(n, cap));
     if (st != TCL_OK) return st;
-    DropoutCtx nodrop{};
-    const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
-    for (int64_t off = 0; off < n; off += cap) {
-        const int64_t nc = std::min(cap, n - off);
-        st = forward_any(m, feats + off * stride, lens + off, nc, scores + off, nodrop, nullptr, s);
-        if (st != TCL_OK) return st;
-    }
-    CUDA_TRY(cudaGetLastError());
-    return TCL_OK;
+    GraphKey key;
+    key.kind = 0;
+    key.p[0] = feats; key.p[1] = lens; key.p[2] = scores;
+    key.v[0] = n;
+    key.gen = m->ws_gen;
+    st = run_graphed(m, key, s, [&](cudaStream_t cs) -> tcl_status {
+        DropoutCtx nodrop{};
+        const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
+        for (int64_t off = 0; off < n; off += cap) {
+            const int64_t nc = std::min(cap, n - off);
+            tcl_status st2 = forward_any(m, feats + off * stride, lens + off, nc, scores + off, nodrop, nullptr, cs);
+            if (st2 != TCL_OK) return st2;
+        }
+        CUDA_TRY(cudaGetLastError());
+        return TCL_OK;
+    });
+    return st;
 }
 
 tcl_status tcl_score_mc(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
@@ -915,27 +988,34 @@ tcl_status tcl_score_mc(tcl_model* m, const float* feats, const int32_t* lens, i
     const int64_t cap = chunk_cap(m);
     tcl_status st = ensure_workspace(m, std::min(n, cap));
     if (st != TCL_OK) return st;
-    const double p = m->dims.dropout_p;
-    DropoutCtx drop{};
-    drop.seed = seed;
-    drop.thr = (uint32_t)std::floor(p * 4294967296.0);
-    drop.scale = (float)(1.0 / (1.0 - p));
-    drop.enabled = 1;
-    const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
-    for (int64_t off = 0; off < n; off += cap) {
-        const int64_t nc = std::min(cap, n - off);
-        drop.index_base = index_base + off;
-        for (int ps = 0; ps < n_passes; ++ps) {
-            drop.pass = ps;
-            st = forward_any(m, feats + off * stride, lens + off, nc, nullptr, drop, mean + off, s);
-            if (st != TCL_OK) return st;
+    GraphKey key;
+    key.kind = 1;
+    key.p[0] = feats; key.p[1] = lens; key.p[2] = mean; key.p[3] = var;
+    key.v[0] = n; key.v[1] = n_passes; key.v[2] = (int64_t)seed; key.v[3] = index_base;
+    key.gen = m->ws_gen;
+    return run_graphed(m, key, s, [&](cudaStream_t cs) -> tcl_status {
+        const double p = m->dims.dropout_p;
+        DropoutCtx drop{};
+        drop.seed = seed;
+        drop.thr = (uint32_t)std::floor(p * 4294967296.0);
+        drop.scale = (float)(1.0 / (1.0 - p));
+        drop.enabled = 1;
+        const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
+        for (int64_t off = 0; off < n; off += cap) {
+            const int64_t nc = std::min(cap, n - off);
+            drop.index_base = index_base + off;
+            for (int ps = 0; ps < n_passes; ++ps) {
+                drop.pass = ps;
+                tcl_status st2 = forward_any(m, feats + off * stride, lens + off, nc, nullptr, drop, mean + off, cs);
+                if (st2 != TCL_OK) return st2;
+            }
+            ProfScope ps(m, TCL_PROF_MC, cs);
+            launch_mc_finalize(m->ws.m2, nc, n_passes, var + off, cs);
+            ++m->launches;
         }
-        ProfScope ps(m, TCL_PROF_MC, s);
-        launch_mc_finalize(m->ws.m2, nc, n_passes, var + off, s);
-        ++m->launches;
-    }
-    CUDA_TRY(cudaGetLastError());
-    return TCL_OK;
+        CUDA_TRY(cudaGetLastError());
+        return TCL_OK;
+    });
 }
 
 tcl_status tcl_topk(tcl_model* m, const float* scores, int64_t n, int32_t k, int64_t index_base,
@@ -947,13 +1027,20 @@ tcl_status tcl_topk(tcl_model* m, const float* scores, int64_t n, int32_t k, int
     cudaStream_t s = (cudaStream_t)stream;
     tcl_status st = ensure_topk_tmp(m, n, k);
     if (st != TCL_OK) return st;
-    unsigned long long* keys = m->topk_tmp;                 // k keys
-    unsigned long long* tmp = m->topk_tmp + k;
-    ProfScope ps(m, TCL_PROF_TOPK, s);
-    m->launches += launch_topk_keys(scores, n, k, index_base, keys, tmp, s);   // sorted best k, 0-padded
-    m->launches += launch_topk_decode(keys, k, idx, top, s);
-    CUDA_TRY(cudaGetLastError());
-    return TCL_OK;
+    GraphKey key;
+    key.kind = 2;
+    key.p[0] = scores; key.p[1] = idx; key.p[2] = top;
+    key.v[0] = n; key.v[1] = k; key.v[2] = index_base;
+    key.gen = m->ws_gen;
+    return run_graphed(m, key, s, [&](cudaStream_t cs) -> tcl_status {
+        unsigned long long* keys = m->topk_tmp;                 // k keys
+        unsigned long long* tmp = m->topk_tmp + k;
+        ProfScope ps(m, TCL_PROF_TOPK, cs);
+        m->launches += launch_topk_keys(scores, n, k, index_base, keys, tmp, cs);   // sorted best k, 0-padded
+        m->launches += launch_topk_decode(keys, k, idx, top, cs);
+        CUDA_TRY(cudaGetLastError());
+        return TCL_OK;
+    });
 }
 
 tcl_status tcl_topk_score(tcl_model* m, const float* scores, const float* lat, const int64_t* off, const float* w,

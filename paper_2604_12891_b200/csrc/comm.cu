@@ -74,6 +74,7 @@ tcl_status tcl_topk_global(tcl_model* m, const float* scores, int64_t n_local, i
         if (m->topk_tmp) cudaFree(m->topk_tmp);
         m->topk_tmp = nullptr;
         m->topk_tmp_cap = 0;
+        ++m->ws_gen;   // graphs that baked in the old scratch are stale
         e = cudaMalloc((void**)&m->topk_tmp, need * sizeof(unsigned long long));
         if (e != cudaSuccess) return set_error(TCL_ENOMEM, "cudaMalloc(topk_tmp)");
         m->topk_tmp_cap = need;

@@ -68,6 +68,27 @@ struct TrainState {
     std::vector<void*> allocs;
 };
 
+// CUDA-graph cache of repeated calls (TCL_OPT_GRAPHS): a call is identified by its kind, every
+// pointer and size it was given and the generation of the model's scratch buffers it bakes in.
+struct GraphKey {
+    int kind = -1;                 // 0 tcl_score, 1 tcl_score_mc, 2 tcl_topk
+    const void* p[6] = {};
+    int64_t v[6] = {};
+    int64_t gen = 0;
+    bool operator==(const GraphKey& o) const {
+        if (kind != o.kind || gen != o.gen) return false;
+        for (int i = 0; i < 6; ++i)
+            if (p[i] != o.p[i] || v[i] != o.v[i]) return false;
+        return true;
+    }
+};
+struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec = nullptr;
+    int64_t launches = 0;          // kernels per replay
+    uint64_t stamp = 0;            // LRU
+};
+
 struct Workspace {
     int64_t cap_n = 0, rows = 0;
     int32_t* cu = nullptr;        // [cap_n + 1]
@@ -123,8 +144,12 @@ struct tcl_model {
     float* invA = nullptr;  // [n_layer][di][N]  1 / A
     int* d_err = nullptr;
     tcl::Workspace ws;
-    int64_t ws_gen = 0;     // bumped on every workspace (re)allocation (graph keys)
+    int64_t ws_gen = 0;     // bumped on every (re)allocation of model-owned scratch (graph keys)
     int use_graphs = 1;     // tcl_set_option(TCL_OPT_GRAPHS)
+    std::vector<tcl::GraphEntry> graphs;     // captured calls (LRU, <= kMaxGraphs)
+    std::vector<tcl::GraphKey> seen;         // calls seen once (captured on their second occurrence)
+    uint64_t graph_clock = 0;
+    cudaStream_t cap_stream = nullptr;       // capture stream (the graphs are launched on the caller's)
     unsigned long long* topk_tmp = nullptr;
     size_t topk_tmp_cap = 0;
     // multi-GPU

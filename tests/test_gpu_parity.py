@@ -427,3 +427,45 @@ def test_bf16_long_config_small_batch(torch_cuda, oracle):
     m = Model(w, d)
     got = _gpu_score(torch_cuda, m, f, l)
     _check_scores(got, oracle.score(d, w, f, l), d.precision)
+
+
+# ------------------------------------------------------------------------------------ CUDA graphs
+@pytest.mark.parametrize("name,prec", [("tiny", inputs.PREC_FP32), ("tiny", inputs.PREC_BF16_PROJ),
+                                       ("paper", inputs.PREC_FP32), ("large", inputs.PREC_BF16_PROJ)])
+def test_graph_replay_bitexact(torch_cuda, name, prec):
+    """TCL_OPT_GRAPHS: the 1st call launches directly, the 2nd is captured and launched, later ones
+    replay -- every one bit-identical to a model that always launches directly (score, MC, top-k),
+    including after the workspace grew (the graphs that baked in the old buffers are dropped)."""
+    from paper_2604_12891_b200 import Model
+    torch = torch_cuda
+    d, w, f, l = _setup(name, n=300, dims_over=dict(precision=prec))
+    g = Model(w, d)
+    ref = Model(w, d)
+    ref.use_graphs(False)
+    ft, lt = torch.from_numpy(f).cuda(), torch.from_numpy(l).cuda()
+    want = _gpu_score(torch, ref, f, l)
+    s = torch.empty(300, device="cuda")
+    n0 = g.launch_count()
+    for it in range(4):
+        s.fill_(float("nan"))
+        g.tcl_score(ft, lt, s)
+        g.tcl_sync_error()
+        assert np.array_equal(s.cpu().numpy(), want), it
+    per_call = (g.launch_count() - n0) / 4
+    assert per_call == (ref.launch_count()), (per_call, ref.launch_count())
+    wm, wv = _mc_gpu(torch, ref, f, l, 3, 9, index_base=11)
+    for it in range(3):
+        mm, vv = _mc_gpu(torch, g, f, l, 3, 9, index_base=11)
+        assert np.array_equal(mm, wm) and np.array_equal(vv, wv), it
+    wi, wt = _topk_gpu(torch, ref, want, 16, index_base=5)
+    for it in range(3):
+        gi, gt = _topk_gpu(torch, g, want, 16, index_base=5)
+        assert np.array_equal(gi, wi) and np.array_equal(gt, wt), it
+    # a larger batch reallocates the workspace: the old graphs must not be replayed
+    _, _, f2, l2 = _setup(name, n=900, dims_over=dict(precision=prec), seed_off=4)
+    want2 = _gpu_score(torch, ref, f2, l2)
+    for it in range(3):
+        assert np.array_equal(_gpu_score(torch, g, f2, l2), want2), it
+    s.fill_(float("nan"))
+    g.tcl_score(ft, lt, s)
+    assert np.array_equal(s.cpu().numpy(), want)
