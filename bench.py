@@ -172,6 +172,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=0)
     ap.add_argument("--precision", choices=["config", "fp32", "bf16"], default="config",
                     help="override the configuration's precision (fp32 path / bf16 projections)")
+    ap.add_argument("--scan", choices=["auto", "sequential", "chunked"], default="auto",
+                    help="fp32-path recurrence (TCL_OPT_SCAN): by dims, sequential, or chunked across L")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="weak",
                     help="weak: n candidates per GPU (default); strong: the config's n split over the GPUs "
                          "(SURVEY §8(e): rank r scores the contiguous shard r, global top-k over all)")
@@ -265,6 +267,8 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         n_total = n * world
     P = int(lens.sum())
     m = Model(w, d, device=local_rank)
+    if args.scan != "auto":
+        m.scan_mode(args.scan)
     m.reserve(n)
     if world > 1:
         obj = [tcl_comm_unique_id() if rank == 0 else None]

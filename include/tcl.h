@@ -239,8 +239,16 @@ tcl_status tcl_rdu_select(tcl_model* model, const float* pool_scores_dev, const 
  *     tcl_train_step) from a CUDA graph captured on its second occurrence; 0 launches every
  *     kernel directly.  Results are bit-identical either way (tested); graphs only remove the
  *     host launch cost and the inter-kernel gaps of the small, launch-bound configurations.
+ *   TCL_OPT_SCAN (default 0 = auto): how the fp32 path runs the mixer's recurrence.  1 = sequential
+ *     (one thread per (candidate-range, channel) walking the tokens: work-efficient);
+ *     2 = chunked (one CTA per candidate, warp-shuffle chunked scan ACROSS L with the associative
+ *     operator (a1, b1) o (a2, b2) = (a1 a2, a2 b1 + b2), lanes = tokens; for max_len <= 32 and
+ *     d_inner <= 128).  The choice is per model, never per n, so scores stay batch-invariant;
+ *     auto = sequential (measured faster at every BASELINE configuration: the chunked scan does
+ *     ~4-8x the instructions for 32x the parallelism).  The two modes round differently (both
+ *     within the fp32 parity bound).
  * Returns TCL_EINVAL for an unknown option or value. */
-typedef enum { TCL_OPT_GRAPHS = 1 } tcl_option;
+typedef enum { TCL_OPT_GRAPHS = 1, TCL_OPT_SCAN = 2 } tcl_option;
 tcl_status tcl_set_option(tcl_model* model, int32_t option, int64_t value);
 
 /* Synchronise `stream`, then return (and clear) the sticky device error of the model. */

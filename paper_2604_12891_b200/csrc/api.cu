@@ -383,14 +383,18 @@ struct F32Run {
         }
         gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
         if (mixer_f32_supported(di, N, R, d.d_conv)) {
-            // conv + x_proj + dt_proj + scan in one kernel (mixer_f32.cu)
+            // conv + x_proj + dt_proj + scan in one kernel (mixer_f32.cu): the sequential scan, or the
+            // warp-shuffle chunked scan across L (TCL_OPT_SCAN; chosen per model, never per n)
             ProfScope ps(m, TCL_PROF_MIXER, s);
             MixerF32Args a{};
             a.XZ = w.XZ; a.ldxz = 2 * di; a.G = w.G; a.ldg = di;
             a.A2 = col->A2 + (size_t)l * di * N; a.invA = col->invA + (size_t)l * di * N; a.Dv = q.Dv;
             a.w_conv = q.w_conv; a.b_conv = q.b_conv; a.W_x = q.W_x; a.W_dt = q.W_dt; a.b_dt = q.b_dt;
-            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.R = R; a.disc = d.disc;
-            launch_mixer_f32(a, m->num_sms, s);   // errors surface through cudaGetLastError in forward_any
+            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.R = R; a.disc = d.disc; a.max_len = d.max_len;
+            // auto = sequential: measured, the chunked scan's shuffle steps cost more than the
+            // parallelism they buy at every BASELINE configuration
+            if (m->scan_mode == 2) launch_mixer_lpar(a, s);
+            else launch_mixer_f32(a, m->num_sms, s);   // errors surface through cudaGetLastError in forward_any
             ++m->launches;
         } else {
         {
@@ -1123,6 +1127,16 @@ tcl_status tcl_set_option(tcl_model* m, int32_t option, int64_t value) {
     if (option == TCL_OPT_GRAPHS) {
         if (value != 0 && value != 1) return set_error(TCL_EINVAL, "TCL_OPT_GRAPHS takes 0 or 1");
         m->use_graphs = (int)value;
+        return TCL_OK;
+    }
+    if (option == TCL_OPT_SCAN) {
+        if (value < 0 || value > 2) return set_error(TCL_EINVAL, "TCL_OPT_SCAN takes 0 (auto), 1 or 2");
+        const tcl_dims& d = m->dims;
+        const int di = d.expand * d.d_model;
+        if (value == 2 && !mixer_lpar_supported(di, d.d_state, d.dt_rank, d.d_conv, d.max_len))
+            return set_error(TCL_ESHAPE, "chunked scan: needs max_len <= 32, d_inner 64 or 128, d_conv 4");
+        m->scan_mode = (int)value;
+        for (tcl_model* q = m->kb; q; q = q->kb) q->scan_mode = (int)value;
         return TCL_OK;
     }
     return set_error(TCL_EINVAL, "unknown option");

@@ -146,6 +146,7 @@ struct tcl_model {
     tcl::Workspace ws;
     int64_t ws_gen = 0;     // bumped on every (re)allocation of model-owned scratch (graph keys)
     int use_graphs = 1;     // tcl_set_option(TCL_OPT_GRAPHS)
+    int scan_mode = 0;      // tcl_set_option(TCL_OPT_SCAN): 0 auto, 1 sequential, 2 chunked across L
     std::vector<tcl::GraphEntry> graphs;     // captured calls (LRU, <= kMaxGraphs)
     std::vector<tcl::GraphKey> seen;         // calls seen once (captured on their second occurrence)
     uint64_t graph_clock = 0;

@@ -100,9 +100,13 @@ struct MixerF32Args {
     const int32_t* cu;           // [n + 1] packed row offsets (device)
     int64_t n;
     int DI, N, R, disc;
+    int max_len;                 // L (the L-parallel variant needs L <= 32)
 };
 bool mixer_f32_supported(int di, int N, int R, int d_conv);
 cudaError_t launch_mixer_f32(const MixerF32Args& a, int num_sms, cudaStream_t s);
+// L-parallel variant (one CTA per candidate, warp-shuffle chunked scan across L) for short sequences
+bool mixer_lpar_supported(int di, int N, int R, int d_conv, int max_len);
+cudaError_t launch_mixer_lpar(const MixerF32Args& a, cudaStream_t s);
 
 // ---- head: LN_f + masked mean pool (warp per candidate) -> pooled [n][dm] -----------------------
 void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const float* lnf_b, float eps,

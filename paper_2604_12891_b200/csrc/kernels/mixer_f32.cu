@@ -325,7 +325,176 @@ static cudaError_t launch_disc(const MixerF32Args& a, int num_sms, cudaStream_t 
     return a.disc == 1 ? launch_k<DI, N, R, 1>(a, num_sms, s) : launch_k<DI, N, R, 0>(a, num_sms, s);
 }
 
+// ============================================================================ L-parallel mixer
+// The same mixer for the fp32 configurations with short sequences (max_len <= 32 at d_inner <= 128:
+// tiny, tuning round, RDU, the paper model), parallel ALONG L: one CTA per candidate, and the scan
+// as a warp-shuffle chunked scan across the sequence (north star: "warp-shuffle chunked scan across
+// L").  The recurrence s_t = a_t s_{t-1} + b_t per (channel, state) -- a_t = e^{Delta_t A},
+// b_t = (e^{Delta_t A} - 1)/A B_t u_t (ZOH) or Delta_t B_t u_t (Euler-B) -- is an associative scan
+// under (a1, b1) o (a2, b2) = (a1 a2, a2 b1 + b2): lane t of a warp holds token t of a 32-token
+// chunk of ONE candidate, log2(W) Hillis-Steele steps (__shfl_up within W-lane segments, W = the
+// next power of two >= T, so short candidates share a warp between 32 / W channels) give every
+// lane its inclusive prefix (A_t, S_t), which with a zero initial state IS the state after token
+// t.  (Longer sequences would chain 32-token chunks through s_t = A_t s_carry + S_t; this variant
+// serves max_len <= 32, where one chunk holds the whole candidate.)  The chunk is aligned to the
+// candidate's first token and W depends on T only, so a token's arithmetic depends only on its own
+// candidate: scores stay batch-invariant (bit-exact).  The
+// other phases are parallel over (token, channel) pairs: conv + SiLU, x_proj and dt_proj + softplus
+// with the same operation order as the sequential fp32 mixer.  The work is ~4x the sequential
+// scan's (N shuffle-scan steps per state), traded for 32x more parallelism where n * d_inner
+// threads cannot fill the GPU.
+template <int DI, int N, int R, int LMAX>
+struct LparSmem {
+    static constexpr int NX = R + 2 * N;
+    static constexpr int kXZ = 0;                                  // f32 [LMAX][2 DI]
+    static constexpr int kU = kXZ + LMAX * 2 * DI * 4;             // f32 [LMAX][DI + 1]
+    static constexpr int kDl = kU + LMAX * (DI + 1) * 4;           // f32 [LMAX][DI + 1]
+    static constexpr int kDbc = kDl + LMAX * (DI + 1) * 4;         // f32 [LMAX][NX + 1]
+    static constexpr int kWx = kDbc + LMAX * (NX + 1) * 4;         // f32 [NX][DI + 1]
+    static constexpr int kBytes = kWx + NX * (DI + 1) * 4;
+};
+
+template <int DI, int N, int R, int DC, int DISC, int LMAX>
+__global__ void __launch_bounds__(256, 3) k_mixer_lpar(MixerF32Args a) {
+    using L = LparSmem<DI, N, R, LMAX>;
+    constexpr int NX = R + 2 * N;
+    constexpr int NT = 256;
+    constexpr int NWARP = NT / 32;
+    extern __shared__ __align__(16) uint8_t lsm[];
+    auto xz_s = reinterpret_cast<float (*)[2 * DI]>(lsm + L::kXZ);
+    auto u_s = reinterpret_cast<float (*)[DI + 1]>(lsm + L::kU);
+    auto dl_s = reinterpret_cast<float (*)[DI + 1]>(lsm + L::kDl);
+    auto dbc_s = reinterpret_cast<float (*)[NX + 1]>(lsm + L::kDbc);
+    auto wx_s = reinterpret_cast<float (*)[DI + 1]>(lsm + L::kWx);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int64_t i = blockIdx.x;
+    const int64_t r0 = a.cu[i];
+    const int T = (int)(a.cu[i + 1] - r0);
+    if (T <= 0) return;   // invalid length: no rows (the head writes NaN)
+    // ---- load [x | z] rows of the candidate and W_x (float4, coalesced)
+    for (int idx = tid; idx < T * 2 * DI / 4; idx += NT) {
+        const int t = idx / (2 * DI / 4), c4 = idx - t * (2 * DI / 4);
+        *reinterpret_cast<float4*>(&xz_s[t][4 * c4]) =
+            __ldg(reinterpret_cast<const float4*>(a.XZ + (r0 + t) * (int64_t)a.ldxz) + c4);
+    }
+    for (int idx = tid; idx < NX * DI; idx += NT) wx_s[idx / DI][idx % DI] = __ldg(a.W_x + idx);
+    __syncthreads();
+    // ---- 1. causal conv + SiLU (taps before the candidate start are absent)
+    for (int idx = tid; idx < T * DI; idx += NT) {
+        const int t = idx / DI, c = idx - t * DI;
+        float acc = fmaf(__ldg(a.w_conv + c * DC + DC - 1), xz_s[t][c], __ldg(a.b_conv + c));
+#pragma unroll
+        for (int k = 0; k < DC - 1; ++k) {
+            const float xv = t - 1 - k >= 0 ? xz_s[t - 1 - k][c] : 0.0f;
+            acc = fmaf(__ldg(a.w_conv + c * DC + DC - 2 - k), xv, acc);
+        }
+        u_s[t][c] = silu(acc);
+    }
+    __syncthreads();
+    // ---- 2. x_proj: dbc[t][j] = sum_c u[t][c] W_x[j][c] (one FFMA chain over c in order)
+    for (int idx = tid; idx < T * NX; idx += NT) {
+        const int t = idx / NX, j = idx - t * NX;
+        float acc = 0.0f;
+#pragma unroll 8
+        for (int c = 0; c < DI; ++c) acc = fmaf(u_s[t][c], wx_s[j][c], acc);
+        dbc_s[t][j] = acc;
+    }
+    __syncthreads();
+    // ---- 3. dt_proj + softplus
+    for (int idx = tid; idx < T * DI; idx += NT) {
+        const int t = idx / DI, c = idx - t * DI;
+        float acc = __ldg(a.b_dt + c);
+#pragma unroll
+        for (int q = 0; q < R; ++q) acc = fmaf(dbc_s[t][q], __ldg(a.W_dt + c * R + q), acc);
+        dl_s[t][c] = softplus_f32(acc);
+    }
+    __syncthreads();
+    // ---- 4. warp-shuffle chunked scan across L.  The candidate's T <= 32 tokens form ONE chunk of
+    // W = next power of two >= T lanes (a fixed function of T: batch-invariant); a warp scans
+    // 32 / W channels at once (segments of W lanes, log2 W Hillis-Steele steps), lane t = token t.
+    {
+        int W = 1;
+        while (W < T) W <<= 1;
+        const int cpw = 32 / W;                    // channels per warp pass
+        const int sub = lane / W, t = lane - sub * W;
+        for (int c0 = warp * cpw; c0 < DI; c0 += NWARP * cpw) {
+            const int c = c0 + sub;
+            const bool live = t < T && c < DI;
+            const int cc = c < DI ? c : DI - 1;
+            const int tt = t < T ? t : T - 1;
+            const float u = u_s[tt][cc];
+            const float dl = dl_s[tt][cc];
+            float y = 0.0f;
+#pragma unroll
+            for (int n0 = 0; n0 < N; n0 += 4) {
+                float av[4], bv[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int n = n0 + q;
+                    const float x2 = dl * __ldg(a.A2 + cc * N + n);
+                    const float Ab = ex2(x2);
+                    const float Bn = dbc_s[tt][R + n];
+                    float b;
+                    if (DISC == 1) {
+                        b = (dl * u) * Bn;
+                    } else {
+                        const float v = (Bn * u) * __ldg(a.invA + cc * N + n);
+                        b = expm1_acc2(make_float2(x2, x2), make_float2(Ab, Ab)).x * v;
+                    }
+                    av[q] = live ? Ab : 1.0f;   // padding lanes: identity element (1, 0)
+                    bv[q] = live ? b : 0.0f;
+                }
+                // inclusive scan within the W-lane segment: (A, S) <- (A_prev A, A S_prev + S); with a
+                // zero initial state S_t is the state after token t
+                for (int off = 1; off < W; off <<= 1) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const float ap = __shfl_up_sync(0xffffffffu, av[q], off, W);
+                        const float bp = __shfl_up_sync(0xffffffffu, bv[q], off, W);
+                        if (t >= off) {
+                            bv[q] = fmaf(av[q], bp, bv[q]);
+                            av[q] = av[q] * ap;
+                        }
+                    }
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q) y = fmaf(dbc_s[tt][R + N + n0 + q], bv[q], y);
+            }
+            if (live) {
+                y = fmaf(__ldg(a.Dv + c), u, y);
+                a.G[(r0 + t) * (int64_t)a.ldg + c] = y * silu(xz_s[t][DI + c]);
+            }
+        }
+    }
+}
+
+template <int DI, int N, int R, int DISC>
+static cudaError_t launch_lpar(const MixerF32Args& a, cudaStream_t s) {
+    constexpr int LMAX = 32;
+    if (a.max_len > LMAX) return cudaErrorInvalidValue;
+    constexpr int smem = LparSmem<DI, N, R, LMAX>::kBytes;
+    auto kern = k_mixer_lpar<DI, N, R, 4, DISC, LMAX>;
+    cudaError_t e = prepare_kernel(kern, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<(unsigned)a.n, 256, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
 }  // namespace f32m
+
+bool mixer_lpar_supported(int di, int N, int R, int d_conv, int max_len) {
+    return d_conv == 4 && max_len <= 32 && ((di == 64 && R == 4) || (di == 128 && R == 8)) && (N == 8 || N == 16);
+}
+
+cudaError_t launch_mixer_lpar(const MixerF32Args& a, cudaStream_t s) {
+    if (a.n == 0) return cudaSuccess;
+#define TCL_LPAR(DI_, N_, R_)                                                                        \
+    if (a.DI == DI_ && a.N == N_ && a.R == R_)                                                       \
+        return a.disc == 1 ? f32m::launch_lpar<DI_, N_, R_, 1>(a, s) : f32m::launch_lpar<DI_, N_, R_, 0>(a, s);
+    TCL_LPAR(64, 16, 4) TCL_LPAR(64, 8, 4) TCL_LPAR(128, 16, 8) TCL_LPAR(128, 8, 8)
+#undef TCL_LPAR
+    return cudaErrorInvalidValue;
+}
 
 bool mixer_f32_supported(int di, int N, int R, int d_conv) {
     if (d_conv != 4) return false;

@@ -49,7 +49,8 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
            "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step",
            "tcl_train_read", "tcl_set_option"]
-TCL_OPT_GRAPHS = 1
+TCL_OPT_GRAPHS, TCL_OPT_SCAN = 1, 2
+SCAN_MODES = {"auto": 0, "sequential": 1, "chunked": 2}
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
               "head", "topk", "mixer", "allgather", "mc", "lateral", "mixprep"]
 
@@ -235,6 +236,10 @@ class Model:
     def use_graphs(self, on: bool = True):
         """CUDA-graph replay of repeated calls (TCL_OPT_GRAPHS, default on)."""
         self.set_option(TCL_OPT_GRAPHS, 1 if on else 0)
+
+    def scan_mode(self, mode: str):
+        """fp32 path recurrence: "auto" (by dims), "sequential", or "chunked" (warp-shuffle across L)."""
+        self.set_option(TCL_OPT_SCAN, SCAN_MODES[mode])
 
     def reserve(self, n_max: int, mc_passes_max: int = 0):
         _check(load().tcl_reserve(self._h, n_max, mc_passes_max))

@@ -469,3 +469,32 @@ def test_graph_replay_bitexact(torch_cuda, name, prec):
     s.fill_(float("nan"))
     g.tcl_score(ft, lt, s)
     assert np.array_equal(s.cpu().numpy(), want)
+
+
+# ------------------------------------------------------------------------------------ chunked scan
+@pytest.mark.parametrize("name,disc", [("tiny", 0), ("tiny", 1), ("paper", 0), ("tuning", 0), ("rdu", 1)])
+def test_chunked_scan_parity_and_invariance(torch_cuda, oracle, name, disc):
+    """TCL_OPT_SCAN = chunked: the fp32 mixer with the warp-shuffle chunked scan across L (one CTA
+    per candidate, lanes = tokens, associative (a, b) operator) within the fp32 bound of the oracle,
+    within 2e-6 of the sequential scan, and bit-exact under permutation / batch size / sharding."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup(name, n=700, dims_over=dict(disc=disc))
+    l = l.copy()
+    l[:5] = 1
+    l[5:10] = d.max_len
+    m = Model(w, d)
+    m.scan_mode("chunked")
+    got = _gpu_score(torch_cuda, m, f, l)
+    ref = oracle.score(d, w, f, l)
+    err = _check_scores(got, ref, d.precision)
+    seq = Model(w, d)
+    seq.scan_mode("sequential")
+    s_seq = _gpu_score(torch_cuda, seq, f, l)
+    assert np.abs(got - s_seq).max() <= 2e-6 * max(1.0, np.abs(s_seq).max())
+    perm = np.random.default_rng(5).permutation(len(l))
+    assert np.array_equal(_gpu_score(torch_cuda, m, f[perm], l[perm]), got[perm])
+    assert np.array_equal(_gpu_score(torch_cuda, m, f[123:124], l[123:124]), got[123:124])
+    m2 = Model(w, d)
+    m2.scan_mode("chunked")
+    assert np.array_equal(_gpu_score(torch_cuda, m2, f[300:650], l[300:650]), got[300:650])
+    print(f"{name} disc={disc} chunked: max|err|={err:.3e} vs sequential {np.abs(got - s_seq).max():.2e}")
