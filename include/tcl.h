@@ -148,6 +148,26 @@ tcl_status tcl_topk_global(tcl_model* model, const float* local_scores_dev, int6
                            int64_t index_base, int32_t k, int64_t* idx_dev, float* topscore_dev,
                            void* stream);
 
+/* The two device halves of tcl_topk_global, for callers that run the exchange themselves (another
+ * transport, or tests with several processes or virtual shards on one GPU):
+ *   tcl_topk_local_keys: this shard's best k as packed keys (tcl_topk_key), sorted descending,
+ *     0-padded when k > n_local -> keys_dev [k] (uint64, device).  n_local == 0 gives k zeros.
+ *   tcl_topk_merge_keys: the best k of `count` gathered keys (any order, 0 = padding) decoded to
+ *     (idx, score) [k]; slots beyond the real keys get idx -1, score -inf.
+ * tcl_topk_global is exactly local_keys -> ncclAllGather -> merge_keys. */
+tcl_status tcl_topk_local_keys(tcl_model* model, const float* local_scores_dev, int64_t n_local, int64_t index_base,
+                               int32_t k, uint64_t* keys_dev, void* stream);
+tcl_status tcl_topk_merge_keys(tcl_model* model, const uint64_t* keys_dev, int64_t count, int32_t k, int64_t* idx_dev,
+                               float* topscore_dev, void* stream);
+
+/* Host-side pieces of the multi-GPU protocol; no device needed.
+ *   tcl_shard_range: rank's contiguous shard of n_global candidates: start = rank * ceil(n / nranks),
+ *     count = min(n, start + ceil(n / nranks)) - start (clamped to 0); global index = start + i.
+ *   tcl_topk_key: the packed (score desc, index asc) key the device kernels compute:
+ *     orderable_u32(score) << 32 | (0xFFFFFFFF - global_index), NaN = -inf, -0 = +0. */
+tcl_status tcl_shard_range(int64_t n_global, int32_t nranks, int32_t rank, int64_t* start, int64_t* count);
+uint64_t tcl_topk_key(float score, int64_t global_index);
+
 /* End-to-end host variant (the call a user without device buffers makes): copies feats/lens
  * host->device (pipelined in sub-chunks with the scoring on a second stream), scores, selects the
  * top-k (k > 0) and copies the results device->host.  Candidate i gets index index_base + i.  If

@@ -14,18 +14,13 @@
 #include <math.h>
 
 #include "../kernels.h"
+#include "../topk_key.h"
 
 namespace tcl {
 
 typedef unsigned long long u64;
 
-__device__ __forceinline__ u64 make_key(float f, uint32_t gidx) {
-    if (isnan(f)) f = -INFINITY;
-    if (f == 0.0f) f = 0.0f;  // -0 == +0 in the score order
-    uint32_t b = __float_as_uint(f);
-    uint32_t ord = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-    return ((u64)ord << 32) | (u64)(0xFFFFFFFFu - gidx);
-}
+__device__ __forceinline__ u64 make_key(float f, uint32_t gidx) { return topk_key(f, gidx); }
 
 template <bool FROM_SCORES, int C>
 __global__ void __launch_bounds__(1024) k_topk_chunk(const float* __restrict__ scores,

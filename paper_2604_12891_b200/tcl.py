@@ -48,7 +48,8 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
            "tcl_score_host", "tcl_sync_error", "tcl_launch_count", "tcl_last_error", "tcl_build_info",
            "tcl_profile_enable", "tcl_profile_read", "tcl_profile_name", "tcl_debug_read", "tcl_rdu_select",
            "tcl_topk_score", "tcl_adapters_count", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step",
-           "tcl_train_read", "tcl_set_option"]
+           "tcl_train_read", "tcl_set_option", "tcl_topk_local_keys", "tcl_topk_merge_keys", "tcl_shard_range",
+           "tcl_topk_key"]
 TCL_OPT_GRAPHS, TCL_OPT_SCAN = 1, 2
 SCAN_MODES = {"auto": 0, "sequential": 1, "chunked": 2}
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
@@ -104,13 +105,18 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
     L.tcl_rdu_select.argtypes = [vp, vp, vp, i64, vp, i64, i32, i32, vp, vp, vp]
     L.tcl_topk_score.argtypes = [vp, vp, vp, vp, vp, i64, i32, vp, i32, vp, vp]
     L.tcl_set_option.argtypes = [vp, i32, i64]
+    L.tcl_topk_local_keys.argtypes = [vp, vp, i64, i64, i32, vp, vp]
+    L.tcl_topk_merge_keys.argtypes = [vp, vp, i64, i32, vp, vp, vp]
+    L.tcl_shard_range.argtypes = [i64, i32, i32, P(i64), P(i64)]
+    L.tcl_topk_key.restype = u64
+    L.tcl_topk_key.argtypes = [ctypes.c_float, i64]
     L.tcl_profile_name.restype = ctypes.c_char_p
     L.tcl_profile_name.argtypes = [ctypes.c_int]
     for fn in ("tcl_model_create", "tcl_model_destroy", "tcl_reserve", "tcl_score", "tcl_score_mc",
                "tcl_topk", "tcl_comm_unique_id", "tcl_comm_init", "tcl_topk_global",
                "tcl_score_host", "tcl_sync_error", "tcl_profile_enable", "tcl_profile_read", "tcl_debug_read", "tcl_rdu_select",
                "tcl_topk_score", "tcl_model_create_kbac", "tcl_train_init", "tcl_train_step", "tcl_train_read",
-               "tcl_set_option"):
+               "tcl_set_option", "tcl_topk_local_keys", "tcl_topk_merge_keys", "tcl_shard_range"):
         getattr(L, fn).restype = ctypes.c_int
     _lib = L
     return L
@@ -168,11 +174,16 @@ def _stream(stream) -> Optional[int]:
 
 
 def shard_range(n_global: int, world: int, rank: int) -> Tuple[int, int]:
-    """Contiguous candidate shard of `rank`: [start, start + count), with
-    start = rank * ceil(n / world); the global index of local candidate i is start + i."""
-    per = -(-n_global // world) if world > 0 else 0
-    start = min(n_global, rank * per)
-    return start, max(0, min(n_global, start + per) - start)
+    """Contiguous candidate shard of `rank` (libtcl's tcl_shard_range): [start,
+    start + count), start = rank * ceil(n / world); global index of local candidate i = start + i."""
+    st, cnt = ctypes.c_int64(), ctypes.c_int64()
+    _check(load().tcl_shard_range(n_global, world, rank, ctypes.byref(st), ctypes.byref(cnt)))
+    return st.value, cnt.value
+
+
+def topk_key(score: float, global_index: int) -> int:
+    """The packed (score desc, index asc) key of the device top-k (libtcl's tcl_topk_key)."""
+    return int(load().tcl_topk_key(score, global_index))
 
 
 def tcl_weights_count(dims) -> int:
@@ -272,6 +283,18 @@ class Model:
         n = scores.shape[0]
         _check(load().tcl_topk_global(self._h, _arg(scores, "f32", n, "scores"), n, index_base, k,
                                       _arg(idx, "i64", k, "idx"), _arg(top, "f32", k, "top"), _stream(stream)))
+
+    def tcl_topk_local_keys(self, scores, index_base: int, k: int, keys, stream=None):
+        """This shard's best k as packed uint64 keys (device int64 tensor [k]), sorted descending."""
+        n = scores.shape[0]
+        _check(load().tcl_topk_local_keys(self._h, _arg(scores, "f32", n, "scores") if n else None, n, index_base, k,
+                                          _arg(keys, "i64", k, "keys"), _stream(stream)))
+
+    def tcl_topk_merge_keys(self, keys, k: int, idx, top, stream=None):
+        """Best k of gathered packed keys (device int64 tensor) -> (idx, score) [k]."""
+        cnt = keys.shape[0]
+        _check(load().tcl_topk_merge_keys(self._h, _arg(keys, "i64", cnt, "keys"), cnt, k, _arg(idx, "i64", k, "idx"),
+                                          _arg(top, "f32", k, "top"), _stream(stream)))
 
     def tcl_topk_score(self, scores, latency, task_offsets, task_weights, max_task_len: int, ks, result,
                        stream=None):
