@@ -191,6 +191,53 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
     return TCL_OK;
 }
 
+// ------------------------------------------------------------------------------ fp32 path: 3xTF32
+// The fp32 path's row GEMMs (encoder linears, in_proj, out_proj) run on the tensor cores as 3xTF32
+// (gemm_tf32.cu); a GEMM whose weight slice does not fit the kernel stays on the SIMT kernel (a
+// per-model choice by dims, never by n: scores stay batch-invariant).  W_hi / W_lo are split on the
+// device from the fp32 weights (at creation and after every Adam update).
+static int tf32_pick_bn(int n, int k, bool full_row) {
+    if (full_row) return tf32_gemm_supported(n, k) ? n : 0;
+    for (int bn : {256, 128, 64, 32})
+        if (bn <= n && n % bn == 0 && tf32_gemm_supported(bn, k)) return bn;
+    return 0;
+}
+
+static void refresh_tf32(tcl_model* m, cudaStream_t s) {
+    for (Tf32W& t : m->tfw)
+        if (t.bn) launch_tf32_split(t.w, (int64_t)t.n * t.k, t.hi, t.lo, s);
+}
+
+static tcl_status setup_tf32(tcl_model* m) {
+    const tcl_dims& d = m->dims;
+    const int dm = d.d_model, di = d.expand * d.d_model, e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+    const bool fuse_ln = dm == 128 && d.n_layer > 0;   // as forward_chunk
+    struct G { const float* w; int n, k; bool full; };
+    std::vector<G> gs = {{m->W1p, e1, kXld, false}, {m->wp.enc_W2, e2, e1, false}, {m->wp.enc_W3, dm, e2, fuse_ln}};
+    for (int l = 0; l < d.n_layer; ++l) {
+        gs.push_back({m->wp.layers[l].W_in, 2 * di, dm, false});
+        gs.push_back({m->wp.layers[l].W_out, dm, di, fuse_ln && l + 1 < d.n_layer});
+    }
+    size_t total = 0;
+    for (const G& g : gs) total += 2 * (size_t)g.n * g.k;
+    tcl_status st = dev_alloc(&m->tf_split, total);
+    if (st != TCL_OK) return st;
+    float* p = m->tf_split;
+    for (const G& g : gs) {
+        Tf32W t;
+        t.w = g.w; t.n = g.n; t.k = g.k; t.hi = p; t.lo = p + (size_t)g.n * g.k;
+        p += 2 * (size_t)g.n * g.k;
+        t.bn = tf32_pick_bn(g.n, g.k, g.full);
+        if (t.bn && !(make_tmap_f32(&t.tm_hi, t.hi, g.k, g.n, (uint64_t)g.k * 4, 32, t.bn) &&
+                      make_tmap_f32(&t.tm_lo, t.lo, g.k, g.n, (uint64_t)g.k * 4, 32, t.bn)))
+            return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (tf32 weights)");
+        m->tfw.push_back(t);
+    }
+    refresh_tf32(m, 0);
+    const cudaError_t e = cudaDeviceSynchronize();
+    return e == cudaSuccess ? TCL_OK : cuda_error(e, "setup_tf32");
+}
+
 // ------------------------------------------------------------------------------ workspace
 
 static void free_workspace(tcl_model* m) {
@@ -245,6 +292,15 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
             free_workspace(m);
             return set_error(TCL_ECUDA, "cudaMemset(Lat)");
         }
+    }
+    if (!m->use_tc) {   // 3xTF32 A operands of the fp32 path (box {32, 128})
+        const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
+        const bool ok = make_tmap_f32(&w.tmX32, w.X, kXld, rows, kXld * 4, 32, 128) &&
+                        make_tmap_f32(&w.tmE1f, w.U, e1, rows, (uint64_t)e1 * 4, 32, 128) &&
+                        make_tmap_f32(&w.tmE2f, w.Delta, e2, rows, (uint64_t)e2 * 4, 32, 128) &&
+                        make_tmap_f32(&w.tmA32, w.A, dm, rows, (uint64_t)dm * 4, 32, 128) &&
+                        make_tmap_f32(&w.tmG32, w.G, di, rows, (uint64_t)di * 4, 32, 128);
+        if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (fp32 workspace)"); }
     }
     if (m->use_tc) {
         const int64_t xzw = std::max<int64_t>(2 * di, (int64_t)d.enc_dims[0] + d.enc_dims[1]);
@@ -307,6 +363,22 @@ static void run_head(tcl_model* m, const int32_t* lens, int64_t n, float* scores
     const int dm = d.d_model, h1 = d.dec_dims[0], h2 = d.dec_dims[1];
     int64_t& nl = m->launches;
     ProfScope ps(m, TCL_PROF_HEAD, s);
+    {   // the fused head: pool + decoder + score / Welford in one launch (bit-identical to the below)
+        HeadArgs a{};
+        a.H = w.H; a.ldh = dm;
+        a.F = lnf_in_ab ? w.Ab : nullptr; a.ldf = dm;
+        a.lnf_w = m->wp.lnf_w; a.lnf_b = m->wp.lnf_b; a.eps = d.ln_eps;
+        a.cu = w.cu; a.lens = lens; a.max_len = d.max_len; a.n = n;
+        a.dm = dm; a.h1 = h1; a.h2 = h2;
+        a.W1 = m->wp.dec_W1; a.b1 = m->wp.dec_b1; a.W2 = m->wp.dec_W2; a.b2 = m->wp.dec_b2;
+        a.W3 = m->wp.dec_W3; a.b3 = m->wp.dec_b3;
+        a.drop = drop;
+        a.scores = scores; a.mc_mean = mc_mean; a.m2 = w.m2; a.pooled = w.pooled;
+        if (launch_head_fused(a, s)) {
+            ++nl;
+            return;
+        }
+    }
     if (lnf_in_ab)  // bf16 path: the last GEMM epilogue already wrote LN_f(H) (bf16) into Ab
         launch_pool_bf16(w.Ab, dm, dm, w.cu, lens, d.max_len, n, w.pooled, s);
     else
@@ -345,6 +417,22 @@ struct F32Run {
     bool fuse_ln = false;
     const float* ln_g = nullptr;   // set by the caller of gemm(..., EPI_RESID_LN / EPI_LN, ...)
     const float* ln_b = nullptr;
+    bool tf32 = false;             // one-column model: row GEMMs on the 3xTF32 tensor-core kernel
+
+    // 3xTF32 row GEMM (gemm_tf32.cu).  epi 0: Y = acc; 1: Y = SiLU(acc + b) [+ dropout, site];
+    // 3: Y (the residual stream, ldy = N) = [Y +] acc + b, then LN -> ws.A when lng != nullptr.
+    void gemm_tf(const CUtensorMap& amap, const Tf32W& tw, const float* b, float* Y, int ldy, int epi, int site,
+                 int kind, bool residual = false, const float* lng = nullptr, const float* lnb = nullptr) const {
+        ProfScope ps(m, kind, s);
+        Tf32GemmParams p{};
+        p.n_tiles = tw.n / tw.bn; p.p_rows = P; p.epi = epi; p.bias = b;
+        p.Y = Y; p.ldy = ldy; p.H = Y; p.ldh = ldy; p.residual = residual ? 1 : 0;
+        p.out = lng ? m->ws.A : nullptr; p.ldo = tw.n; p.ln_g = lng; p.ln_b = lnb; p.eps = m->dims.ln_eps;
+        p.drop = drop; p.site = site; p.row_cand = m->ws.row_cand; p.cu = m->ws.cu;
+        if (epi != 1) p.drop.enabled = 0;
+        launch_gemm_tf32(amap, tw.tm_hi, tw.tm_lo, p, tw.bn, tw.k, m->num_sms, s);
+        ++m->launches;
+    }
 
     // Y = epi(X W^T [+ X2 W2^T] + b) over the packed rows (or over the n candidates: cands = true)
     void gemm(const float* X, int ldx, const float* W, int ldw, const float* b, float* Y, int ldy, int K,
@@ -381,7 +469,10 @@ struct F32Run {
             launch_layernorm(H, dm, dm, q.ln_w, q.ln_b, d.ln_eps, w.A, nullptr, dm, max_rows, P, s,
                              /*gemm_epilogue_order=*/true); ++m->launches;
         }
-        gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
+        const Tf32W* tw_in = (tf32 && !site) ? &m->tfw[3 + 2 * l] : nullptr;
+        const Tf32W* tw_out = (tf32 && !site) ? &m->tfw[4 + 2 * l] : nullptr;
+        if (tw_in && tw_in->bn) gemm_tf(w.tmA32, *tw_in, nullptr, w.XZ, 2 * di, 0, -1, TCL_PROF_IN_PROJ);
+        else gemm(w.A, dm, q.W_in, dm, nullptr, w.XZ, 2 * di, dm, 2 * di, EPI_NONE, -1, TCL_PROF_IN_PROJ);
         if (mixer_f32_supported(di, N, R, d.d_conv)) {
             // conv + x_proj + dt_proj + scan in one kernel (mixer_f32.cu): the sequential scan, or the
             // warp-shuffle chunked scan across L (TCL_OPT_SCAN; chosen per model, never per n)
@@ -418,6 +509,10 @@ struct F32Run {
         if (site) {
             gemm(w.G, di, q.W_out, di, nullptr, H, dm, di, dm, EPI_RESID, -1, TCL_PROF_OUT_PROJ, w.Lat, m->ad_ld,
                  site->Ua, m->ad_ld);
+        } else if (tw_out && tw_out->bn) {   // out_proj + residual (+ the next LayerNorm) on 3xTF32
+            const bool ln = fuse_ln && l + 1 < d.n_layer;
+            gemm_tf(w.tmG32, *tw_out, nullptr, H, dm, 3, -1, TCL_PROF_OUT_PROJ, true,
+                    ln ? col->wp.layers[l + 1].ln_w : nullptr, ln ? col->wp.layers[l + 1].ln_b : nullptr);
         } else if (fuse_ln && l + 1 < d.n_layer) {
             F32Run r2 = *this;
             r2.ln_g = col->wp.layers[l + 1].ln_w;
@@ -515,10 +610,16 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     // encoder: SiLU after linears 1 and 2 (R1), dropout sites 0, 1 (R17)
     float* E1 = w.U;      // aliases: encoder hidden states live in the mixer buffers
     float* E2 = w.Delta;
-    r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
-    r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
+    r.tf32 = !m->tfw.empty();
     r.fuse_ln = dm == 128 && d.n_layer > 0;
-    if (r.fuse_ln) {
+    if (r.tf32 && m->tfw[0].bn) r.gemm_tf(w.tmX32, m->tfw[0], m->wp.enc_b1, E1, e1, 1, 0, TCL_PROF_ENCODER);
+    else r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
+    if (r.tf32 && m->tfw[1].bn) r.gemm_tf(w.tmE1f, m->tfw[1], m->wp.enc_b2, E2, e2, 1, 1, TCL_PROF_ENCODER);
+    else r.gemm(E1, e1, m->wp.enc_W2, e1, m->wp.enc_b2, E2, e2, e1, e2, EPI_SILU, 1, TCL_PROF_ENCODER);
+    if (r.tf32 && m->tfw[2].bn) {   // linear 3 (+ LN_0 at d_model 128)
+        r.gemm_tf(w.tmE2f, m->tfw[2], m->wp.enc_b3, w.H, dm, 3, -1, TCL_PROF_ENCODER, false,
+                  r.fuse_ln ? m->wp.layers[0].ln_w : nullptr, r.fuse_ln ? m->wp.layers[0].ln_b : nullptr);
+    } else if (r.fuse_ln) {
         F32Run r0 = r;
         r0.ln_g = m->wp.layers[0].ln_w;
         r0.ln_b = m->wp.layers[0].ln_b;
@@ -835,6 +936,9 @@ tcl_status tcl_model_create(const float* weights_host, size_t n_floats, const tc
     }
     if (d.precision == TCL_PREC_BF16_PROJ) {
         if ((st = setup_tc(m, weights_host)) != TCL_OK) { tcl_model_destroy(m); return st; }
+    } else if ((st = setup_tf32(m)) != TCL_OK) {
+        tcl_model_destroy(m);
+        return st;
     }
     if ((st = dev_alloc(&m->d_err, 1)) != TCL_OK) { tcl_model_destroy(m); return st; }
     CUDA_TRY(cudaMemset(m->d_err, 0, sizeof(int)));
@@ -937,6 +1041,7 @@ tcl_status tcl_model_destroy(tcl_model* m) {
     if (m->rdu_scratch) cudaFree(m->rdu_scratch);
     if (m->eval_cols) cudaFree(m->eval_cols);
     if (m->ad_dev) cudaFree(m->ad_dev);
+    if (m->tf_split) cudaFree(m->tf_split);
     free_train(m);
     if (m->kb) tcl_model_destroy(m->kb);
     for (auto& r : m->prof_recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
@@ -1553,6 +1658,8 @@ static tcl_status train_enqueue(tcl_model* m, const float* feats, const int32_t*
     if (apply_update) {
         launch_adam(m->w_dev, t.g, t.mA, t.vA, t.nW, t.lr, t.b1, t.b2, t.eps, t.step_dev, t.corr_dev, s); nl += 2;
         launch_refresh_w1(m->wp.enc_W1, e1, d.d_in, kXld, m->W1p, s); ++nl;
+        refresh_tf32(m, s);   // the 3xTF32 copies the scoring path reads
+        for (const Tf32W& t : m->tfw) nl += t.bn ? 1 : 0;
         for (int l = 0; l < d.n_layer; ++l) {
             launch_refresh_a(m->wp.layers[l].A_log, di * N, m->A2 + (size_t)l * di * N, m->invA + (size_t)l * di * N, s);
             ++nl;

@@ -89,6 +89,16 @@ struct GraphEntry {
     uint64_t stamp = 0;            // LRU
 };
 
+// One row GEMM of the fp32 path on the 3xTF32 tensor-core kernel (gemm_tf32.cu): W_hi / W_lo
+// copies (split on the device from the fp32 weights) and their tensor maps.
+struct Tf32W {
+    const float* w = nullptr;      // the fp32 weight [n][k] it is split from
+    float* hi = nullptr;
+    float* lo = nullptr;
+    CUtensorMap tm_hi, tm_lo;      // box {32, bn}
+    int bn = 0, n = 0, k = 0;      // bn == 0: this GEMM stays on the SIMT kernel
+};
+
 struct Workspace {
     int64_t cap_n = 0, rows = 0;
     int32_t* cu = nullptr;        // [cap_n + 1]
@@ -125,6 +135,7 @@ struct Workspace {
     float* pooled_k = nullptr;    // [cap_n][dm]
     float* dh1k = nullptr;        // [cap_n][h1]
     CUtensorMap tmAbS2;                                // in_proj A half-slices for 2-CTA cluster multicast (box {64, 64})
+    CUtensorMap tmX32, tmE1f, tmE2f, tmA32, tmG32;     // fp32 path 3xTF32 A operands (box {32, 128})
     std::vector<void*> allocs;
 };
 
@@ -147,6 +158,9 @@ struct tcl_model {
     int64_t ws_gen = 0;     // bumped on every (re)allocation of model-owned scratch (graph keys)
     int use_graphs = 1;     // tcl_set_option(TCL_OPT_GRAPHS)
     int scan_mode = 0;      // tcl_set_option(TCL_OPT_SCAN): 0 auto, 1 sequential, 2 chunked across L
+    // fp32 path: row GEMMs on the 3xTF32 tensor-core kernel: enc1, enc2, enc3, then (in, out) per layer
+    std::vector<tcl::Tf32W> tfw;
+    float* tf_split = nullptr;
     std::vector<tcl::GraphEntry> graphs;     // captured calls (LRU, <= kMaxGraphs)
     std::vector<tcl::GraphKey> seen;         // calls seen once (captured on their second occurrence)
     uint64_t graph_clock = 0;

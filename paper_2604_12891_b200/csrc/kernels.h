@@ -1,5 +1,6 @@
 // kernels.h -- internal launchers of libtcl (not part of the C ABI).
 #pragma once
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -107,6 +108,23 @@ cudaError_t launch_mixer_f32(const MixerF32Args& a, int num_sms, cudaStream_t s)
 // L-parallel variant (one CTA per candidate, warp-shuffle chunked scan across L) for short sequences
 bool mixer_lpar_supported(int di, int N, int R, int d_conv, int max_len);
 cudaError_t launch_mixer_lpar(const MixerF32Args& a, cudaStream_t s);
+
+// ---- fused head (head.cu): pool + decoder + score / Welford in one launch ---------------------
+struct HeadArgs {
+    const float* H; int ldh;              // fp32 path: residual stream (LN_f applied here)
+    const __nv_bfloat16* F; int ldf;      // bf16 path: LN_f(H) rows (nullptr on the fp32 path)
+    const float* lnf_w; const float* lnf_b; float eps;
+    const int32_t* cu; const int32_t* lens; int max_len; int64_t n;
+    int dm, h1, h2;
+    const float *W1, *b1, *W2, *b2, *W3, *b3;
+    float* pooled;                        // [n][dm] scratch of the two-launch form (large n)
+    DropoutCtx drop;                      // sites 2, 3 (MC); drop.pass = the Welford pass
+    float* scores;                        // deterministic mode (NaN for invalid lengths)
+    float* mc_mean; float* m2;            // MC mode (mc_mean != nullptr)
+};
+// false: dims not covered (decoder widths other than [dm/2, dm/4, 1]); the caller falls back.
+// One launch for n < 8192; larger batches return false (the five-launch head is faster there).
+bool launch_head_fused(const HeadArgs& a, cudaStream_t s);
 
 // ---- head: LN_f + masked mean pool (warp per candidate) -> pooled [n][dm] -----------------------
 void launch_pool(const float* H, int ldh, int dm, const float* lnf_w, const float* lnf_b, float eps,

@@ -116,6 +116,231 @@ void launch_pool_bf16(const void* F, int ldf, int dm, const int32_t* cu, const i
     }
 }
 
+// ---------------------------------------------------------------------------- fused head
+// The whole head in ONE kernel (one launch instead of five): a CTA of 256 threads takes 32
+// candidates; (1) each warp pools 4 of them exactly as k_pool / k_pool_bf16 (rows in order
+// t = 0..T-1) into shared memory; (2)-(4) the three decoder linears, each output one sequential
+// FFMA chain over k in order (the weights staged 32 k at a time, transposed, in shared memory),
+// v = acc + b, SiLU (+ inverted dropout, sites 2 / 3, token 0) -- the arithmetic of the SIMT
+// GEMMs it replaces, so the scores are bit-identical to the five-launch head; (5) the score is
+// stored (NaN for an invalid length) or folded into the MC Welford statistics.
+template <int CT, int K, int NO, int NOP, bool ACT>
+__device__ __forceinline__ void head_linear(const float* __restrict__ inT, const float* __restrict__ W,
+                                            const float* __restrict__ bias, float* __restrict__ outT,
+                                            float* ws, const DropoutCtx& drop, int site, int64_t cand0,
+                                            int64_t n) {
+    // inT [K][CT + 4], outT [NO][CT + 4] (transposed: 4 consecutive candidates are one float4).
+    // Thread -> a 4 x 4 register tile: columns 4 jq .. 4 jq + 3, candidates 4 cq .. 4 cq + 3; each
+    // output is one sequential FFMA chain over k (2 LDS.128 per 16 FFMA).
+    constexpr int LD = CT + 4;
+    constexpr int JQ = NOP / 4, CQ = CT / 4;
+    const int jq = threadIdx.x % JQ, cq = threadIdx.x / JQ;
+    const bool act_thr = cq < CQ && 4 * jq < NO;
+    float acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
+    for (int k0 = 0; k0 < K; k0 += 32) {
+        __syncthreads();   // ws reuse (and the producer of inT is done)
+        for (int idx = threadIdx.x; idx < NO * 32; idx += 256) {   // W[jj][k0 + kk] -> ws[kk][jj]
+            const int jj = idx >> 5, kk = idx & 31;
+            ws[kk * NOP + jj] = k0 + kk < K ? __ldg(W + (int64_t)jj * K + k0 + kk) : 0.0f;
+        }
+        __syncthreads();
+        if (act_thr) {
+#pragma unroll 4
+            for (int kk = 0; kk < 32; ++kk) {
+                if (k0 + kk >= K) break;
+                const float4 wv = *reinterpret_cast<const float4*>(ws + kk * NOP + 4 * jq);
+                const float4 xv = *reinterpret_cast<const float4*>(inT + (k0 + kk) * LD + 4 * cq);
+                const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, wsv[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xs[a], wsv[b], acc[a][b]);
+            }
+        }
+    }
+    if (act_thr) {
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+            const int j = 4 * jq + b;
+            if (j >= NO) continue;
+            const float bj = __ldg(bias + j);
+            float v4[4];
+#pragma unroll
+            for (int a = 0; a < 4; ++a) {
+                const int c = 4 * cq + a;
+                float v = acc[a][b] + bj;
+                if (ACT) {
+                    v = silu(v);
+                    if (drop.enabled && cand0 + c < n) v = dropout_keep(drop, j, 0, site, cand0 + c) ? v * drop.scale : 0.0f;
+                }
+                v4[a] = v;
+            }
+            *reinterpret_cast<float4*>(outT + j * LD + 4 * cq) = make_float4(v4[0], v4[1], v4[2], v4[3]);
+        }
+    }
+}
+
+// CT candidates per CTA; POOL: the masked mean is computed here (one launch for the whole head),
+// else read from a.pooled.  A candidate's arithmetic does not depend on CT or POOL.
+template <int PER, bool BF16, int H1, int H2, int CT, bool POOL>
+__global__ void __launch_bounds__(256) k_head(HeadArgs a) {
+    constexpr int kHeadCT = CT;
+    constexpr int dm = 32 * PER;
+    constexpr int H1P = H1 <= 32 ? 32 : (H1 <= 64 ? 64 : (H1 <= 128 ? 128 : 256));
+    constexpr int H2P = H2 <= 32 ? 32 : (H2 <= 64 ? 64 : (H2 <= 128 ? 128 : 256));
+    constexpr int LD = CT + 4;   // transposed activations: [feature][candidate], float4 rows
+    extern __shared__ __align__(16) float hsm[];
+    float* pooledT = hsm;                         // [dm][LD]
+    float* h1T = pooledT + dm * LD;               // [H1][LD]
+    float* h2T = h1T + H1 * LD;                   // [H2][LD]
+    float* ws = h2T + H2 * LD;                    // [32][max(H1P, H2P)]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t c0 = (int64_t)blockIdx.x * kHeadCT;
+    // ---- (1) masked mean (of LN_f(H) rows: computed here on the fp32 path, stored bf16 on the bf16 path)
+    if (!POOL) {
+        for (int idx = threadIdx.x; idx < kHeadCT * dm; idx += 256) {
+            const int cc = idx / dm, col = idx - cc * dm;
+            pooledT[col * LD + cc] = c0 + cc < a.n ? a.pooled[(c0 + cc) * dm + col] : 0.0f;
+        }
+    }
+    for (int cc = warp; POOL && cc < kHeadCT; cc += 8) {
+        const int64_t i = c0 + cc;
+        const int T = i < a.n ? a.lens[i] : 0;
+        const bool ok = T >= 1 && T <= a.max_len;
+        if (!BF16) {
+            float acc[PER];
+#pragma unroll
+            for (int j = 0; j < PER; ++j) acc[j] = 0.0f;
+            if (ok) {
+                const float* h = a.H + (int64_t)a.cu[i] * a.ldh;
+                float gv[PER], bv[PER];
+#pragma unroll
+                for (int j = 0; j < PER; ++j) { gv[j] = __ldg(a.lnf_w + lane + 32 * j); bv[j] = __ldg(a.lnf_b + lane + 32 * j); }
+                for (int t = 0; t < T; ++t) {
+                    float v[PER];
+                    float sm = 0.f;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) { v[j] = h[(int64_t)t * a.ldh + lane + 32 * j]; sm += v[j]; }
+                    const float mean = warp_sum(sm) * (1.0f / dm);
+                    float q = 0.f;
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) { const float e = v[j] - mean; q = fmaf(e, e, q); }
+                    const float rstd = rsqrtf(warp_sum(q) * (1.0f / dm) + a.eps);
+#pragma unroll
+                    for (int j = 0; j < PER; ++j) acc[j] += (v[j] - mean) * rstd * gv[j] + bv[j];
+                }
+                const float invT = 1.0f / (float)T;
+#pragma unroll
+                for (int j = 0; j < PER; ++j) acc[j] *= invT;
+            }
+#pragma unroll
+            for (int j = 0; j < PER; ++j) pooledT[(lane + 32 * j) * LD + cc] = acc[j];
+        } else {
+            constexpr int PB = PER / 2;   // bf16x2 pairs per lane
+            float acc[2 * PB];
+#pragma unroll
+            for (int j = 0; j < 2 * PB; ++j) acc[j] = 0.0f;
+            if (ok) {
+                const __nv_bfloat16* f = a.F + (int64_t)a.cu[i] * a.ldf;
+#pragma unroll 4
+                for (int t = 0; t < T; ++t) {
+#pragma unroll
+                    for (int j = 0; j < PB; ++j) {
+                        const float2 fv = __bfloat1622float2(
+                            *reinterpret_cast<const __nv_bfloat162*>(f + (int64_t)t * a.ldf + 2 * (lane + 32 * j)));
+                        acc[2 * j] += fv.x;
+                        acc[2 * j + 1] += fv.y;
+                    }
+                }
+                const float invT = 1.0f / (float)T;
+#pragma unroll
+                for (int j = 0; j < 2 * PB; ++j) acc[j] *= invT;
+            }
+#pragma unroll
+            for (int j = 0; j < PB; ++j) {
+                pooledT[(2 * (lane + 32 * j)) * LD + cc] = acc[2 * j];
+                pooledT[(2 * (lane + 32 * j) + 1) * LD + cc] = acc[2 * j + 1];
+            }
+        }
+    }
+    // ---- (2)-(4) decoder
+    head_linear<CT, dm, H1, H1P, true>(pooledT, a.W1, a.b1, h1T, ws, a.drop, 2, c0, a.n);
+    head_linear<CT, H1, H2, H2P, true>(h1T, a.W2, a.b2, h2T, ws, a.drop, 3, c0, a.n);
+    __syncthreads();
+    // ---- (3) score, then store / Welford
+    if (threadIdx.x < kHeadCT) {
+        const int cc = threadIdx.x;
+        const int64_t i = c0 + cc;
+        if (i < a.n) {
+            float acc = 0.0f;
+#pragma unroll 8
+            for (int k = 0; k < H2; ++k) acc = fmaf(h2T[k * LD + cc], __ldg(a.W3 + k), acc);
+            const float v = acc + __ldg(a.b3);
+            const int T = a.lens[i];
+            const bool ok = T >= 1 && T <= a.max_len;
+            if (!a.mc_mean) {
+                a.scores[i] = ok ? v : NAN;
+            } else if (!ok) {
+                a.mc_mean[i] = NAN;
+                a.m2[i] = NAN;
+            } else {   // Welford over passes (as k_welford)
+                const int pass = a.drop.pass;
+                const float m_old = pass == 0 ? 0.0f : a.mc_mean[i];
+                const float q_old = pass == 0 ? 0.0f : a.m2[i];
+                const float delta = v - m_old;
+                const float m_new = m_old + delta / (float)(pass + 1);
+                a.mc_mean[i] = m_new;
+                a.m2[i] = q_old + delta * (v - m_new);
+            }
+        }
+    }
+}
+
+template <int PER, bool BF16, int CT, bool POOL>
+static bool head_dims(const HeadArgs& a, cudaStream_t s) {
+    const dim3 grid((unsigned)((a.n + CT - 1) / CT));
+#define TCL_HEAD(H1_, H2_)                                                                                 \
+    if (a.h1 == H1_ && a.h2 == H2_) {                                                                 \
+        constexpr int H1P = H1_ <= 32 ? 32 : (H1_ <= 64 ? 64 : (H1_ <= 128 ? 128 : 256));           \
+        const int smem = 4 * ((CT + 4) * (32 * PER + H1_ + H2_) + 32 * H1P);                         \
+        auto kern = k_head<PER, BF16, H1_, H2_, CT, POOL>;                                            \
+        if (prepare_kernel(kern, smem) != cudaSuccess) return false;                                  \
+        kern<<<grid, 256, smem, s>>>(a);                                                              \
+        return true;                                                                                  \
+    }
+    TCL_HEAD(32 * PER / 2, 32 * PER / 4)   // reading R10: decoder [d_model / 2, d_model / 4, 1]
+#undef TCL_HEAD
+    return false;
+}
+
+template <int PER, bool BF16>
+static bool head_pick(const HeadArgs& a, cudaStream_t s) {
+    // small batches (launch-bound): everything in one launch, 8 candidates per CTA.  Large batches
+    // return false: the caller's pool kernel + SIMT decoder GEMMs keep more rows in flight and
+    // reuse each weight tile across 64-128 candidates (measured: the one-launch head at 65,536
+    // candidates took 0.53 ms for the decoder alone, re-staging W1 per 32 candidates, vs 0.41 ms
+    // for the whole five-launch head).  Both compute every candidate with the same operations in
+    // the same order: bit-identical, so the switch does not break batch invariance (tested).
+    if (a.n < 8192) return head_dims<PER, BF16, 8, true>(a, s);
+    return false;
+}
+
+bool launch_head_fused(const HeadArgs& a, cudaStream_t s) {
+    if (a.n == 0) return true;
+    if (a.h1 != a.dm / 2 || a.h2 != a.dm / 4) return false;
+    const bool bf = a.F != nullptr;
+    switch (a.dm) {
+        case 64: return bf ? head_pick<2, true>(a, s) : head_pick<2, false>(a, s);
+        case 128: return bf ? head_pick<4, true>(a, s) : head_pick<4, false>(a, s);
+        case 256: return bf ? head_pick<8, true>(a, s) : head_pick<8, false>(a, s);
+        default: return false;
+    }
+}
+
 __global__ void k_welford(const float* __restrict__ score, const int32_t* __restrict__ lens, int max_len,
                           int64_t n, int pass, float* __restrict__ mean, float* __restrict__ m2) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;

@@ -65,4 +65,24 @@ cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUt
                            const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s,
                            const CUtensorMap* c2 = nullptr);
 
+// ---- fp32 path on the tensor cores: 3xTF32 GEMM (gemm_tf32.cu) -------------------------------
+struct Tf32GemmParams {
+    int n_tiles;                 // N / BN
+    const int32_t* p_rows;       // device: number of valid rows
+    int epi;                     // 0: Y = acc; 1: Y = SiLU(acc + b) [+ dropout]; 3: H = [H +] acc + b [, out = LN(H)]
+    const float* bias;           // [N] or nullptr
+    float* Y; int ldy;           // epi 0 / 1 output (fp32)
+    float* H; int ldh; int residual;
+    float* out; int ldo;         // epi 3: LayerNorm output (fp32) or nullptr (needs n_tiles == 1)
+    const float* ln_g; const float* ln_b; float eps;
+    DropoutCtx drop; int site; const int32_t* row_cand; const int32_t* cu;
+};
+// bn in {32, 64, 128, 256}; k <= 256 (K-blocks of 32 fp32); both weight halves resident.
+bool tf32_gemm_supported(int bn, int k);
+// A: fp32 [rows][K] map (box {32, 128}, 128B swizzle); B / Blo: W_hi / W_lo [N][K] (box {32, bn}).
+cudaError_t launch_gemm_tf32(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& blo,
+                             const Tf32GemmParams& p, int bn, int k, int num_sms, cudaStream_t s);
+// hi = w with the low 13 mantissa bits cleared, lo = tf32_rna(w - hi), element-wise (n floats).
+void launch_tf32_split(const float* w, int64_t n, float* hi, float* lo, cudaStream_t s);
+
 }  // namespace tcl

@@ -63,6 +63,22 @@ def test_score_parity_fp32(torch_cuda, oracle, name, disc):
     print(f"{name} disc={disc}: n={len(l)} max|err|={err:.3e} score std={ref.std():.3e}")
 
 
+@pytest.mark.parametrize("name", ["large", "rdu"])
+def test_score_parity_fp32_wide(torch_cuda, oracle, name):
+    """The fp32 path (3xTF32 row GEMMs, several N tiles per row, residual epilogue) at d_model 256
+    and 128, including MC dropout through the tensor-core epilogue."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup(name, n=300, dims_over=dict(precision=inputs.PREC_FP32))
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    err = _check_scores(got, oracle.score(d, w, f, l), d.precision)
+    mean, var = _mc_gpu(torch_cuda, m, f[:48], l[:48], 3, 17, index_base=2)
+    rm, rv = oracle.score_mc(d, w, f[:48], l[:48], 3, 17, index_base=2)
+    _check_scores(mean, rm, d.precision)
+    assert np.all(np.abs(var - rv) <= 2 * TOL[d.precision] * np.sqrt(np.maximum(rv, 1e-8)) + 1e-7)
+    print(f"{name} fp32: max|err|={err:.3e}")
+
+
 def test_score_parity_bf16_large_small_batch(torch_cuda, oracle):
     from paper_2604_12891_b200 import Model
     d, w, f, l = _setup("large", n=384)
@@ -213,6 +229,17 @@ def test_permutation_and_batch_invariance_bitexact(torch_cuda, name):
     # shard invariance: a fresh model (fresh workspace) on a shard
     m2 = Model(w, d)
     assert np.array_equal(_gpu_score(torch_cuda, m2, f[250:750], l[250:750]), s[250:750])
+
+
+@pytest.mark.parametrize("name,prec", [("tuning", inputs.PREC_FP32), ("large", inputs.PREC_BF16_PROJ)])
+def test_head_forms_bitexact(torch_cuda, name, prec):
+    """The one-launch head (batches < 8,192) and the five-launch head (larger batches) compute each
+    candidate identically: a 9,000-candidate batch and its 300-candidate slice agree bit for bit."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup(name, n=9000, dims_over=dict(precision=prec))
+    m = Model(w, d)
+    s = _gpu_score(torch_cuda, m, f, l)
+    assert np.array_equal(_gpu_score(torch_cuda, m, f[4000:4300], l[4000:4300]), s[4000:4300])
 
 
 def test_edge_lengths_and_invalid(torch_cuda, oracle):
