@@ -164,19 +164,30 @@ __global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // token position inside its candidate for rows ck * 16 + lane (lanes 0..15): two dependent
-    // global loads, issued one chunk ahead like the x rows
-    auto positions = [&](int64_t ck) -> int {
-        const int64_t r = ck * kTC + lane;
-        return (ck < n_chunks && lane < kTC && r < P) ? (int)(r - __ldg(a.cu + __ldg(a.row_cand + r))) : 0;
+    // candidate of rows ck * 16 - H + lane (lanes 0 .. 18; -1 outside [0, P)): one load per lane,
+    // issued one chunk ahead like the x rows; a row's tap j (1..H) lies inside its candidate iff the
+    // rows back to it carry the same candidate id
+    auto cands = [&](int64_t ck) -> int {
+        const int64_t r = ck * kTC - H + lane;
+        return (ck < n_chunks && lane < L::kRows && r >= 0 && r < P) ? __ldg(a.row_cand + r) : -1;
     };
     int64_t ck = (int64_t)blockIdx.x * L::kWarps + warp;
     fetch(ck);
-    int tpos_next = positions(ck);
+    int rc_next = cands(ck);
     for (; ck < n_chunks; ck += wstep) {
         const int64_t r0 = ck * kTC;
         const int tc = (int)(P - r0 < kTC ? P - r0 : kTC);
-        const int tpos = tpos_next;
+        // tpos (lane t < 16) = number of taps 1..H of row r0 + t inside its candidate
+        int tpos = 0;
+        {
+            const int rc = rc_next;
+            const int self = __shfl_sync(0xffffffffu, rc, (lane + H) & 31);
+#pragma unroll
+            for (int j = 1; j <= H; ++j) {
+                const int prev = __shfl_sync(0xffffffffu, rc, (lane + H - j) & 31);
+                if (tpos == j - 1 && prev == self) tpos = j;
+            }
+        }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
         // ---- 1. conv + SiLU.  win[j] = x at row t - 1 - j (channel pairs, packed fp32x2 math)
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
         }
         __syncwarp();               // every ldmatrix of the tile is done: request the next chunk's x
         fetch(ck + wstep);
-        tpos_next = positions(ck + wstep);
+        rc_next = cands(ck + wstep);
         // B, C columns [R, R + 2N) to the packet; dt_r columns [0, R) -> dt_proj A fragments
         const bool row_lo = g < tc, row_hi = g + 8 < tc;
         uint8_t* prow_lo = pk + (r0 + g) * (int64_t)a.pk_ld;
