@@ -368,7 +368,9 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     units = (mc or 1) * (d.n_layer if dom in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan",
                                                 "out_proj", "mixer", "mixprep") else 1)
     traffic = None  # DRAM bytes per launch of this kernel from one ncu --set full capture (profiles/)
-    tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
+    tp = os.path.join(ROOT, "profiles", "round2_traffic.json")
+    if not os.path.exists(tp):
+        tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
     if os.path.exists(tp):
         tj = json.load(open(tp)).get(dom)
         if tj and args.config == "large":

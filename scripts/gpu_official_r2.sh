@@ -1,0 +1,20 @@
+# Round-2 evidence: GPU tests, smoke, bench (N=1 default + strong-scaling form), reference arm, every
+# config, accuracy (full-size `large`), launch list + per-kernel ncu captures.
+cd $GRAFT_REPO_ROOT
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -3
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -3
+python bench.py > gpurun_out/bench_r2.json 2> gpurun_out/bench_r2.err; tail -2 gpurun_out/bench_r2.err; cut -c1-300 gpurun_out/bench_r2.json
+python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_reference_r2.json 2>/dev/null; cut -c1-200 gpurun_out/bench_reference_r2.json
+bash scripts/configs_gpu.sh
+echo -n "== long 131072 :: "; timeout 900 python bench.py --config long --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null > gpurun_out/bench_long.json; python -c "import json; d=json.load(open('gpurun_out/bench_long.json')); print(round(d['value']), round(d['ms_per_step'],3), round(d['e2e']['value']))"
+timeout 1500 python scripts/measure_configs.py --full-large 2>&1 | tail -8
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+for k in k_scan k_mixprep k_gemm_tc k_gemm_ln; do
+  ncu --set full --import-source on --clock-control none -k regex:$k -s 4 -c 1 -o gpurun_out/prof_r2_$k python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+done
+for k in k_enc12 k_topk_radix k_pack k_pool_bf16; do
+  ncu --set full --import-source on --clock-control none -k regex:$k -s 3 -c 1 -o gpurun_out/prof_r2_$k python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+done
+ncu --set full --import-source on --clock-control none -k regex:k_gemm_tf32 -s 6 -c 1 -o gpurun_out/prof_r2_k_gemm_tf32 python bench.py --config tuning --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ncu --set full --import-source on --clock-control none -k regex:k_head -s 2 -c 1 -o gpurun_out/prof_r2_k_head python bench.py --config paper --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
+ls gpurun_out/prof_r2_*

@@ -21,30 +21,34 @@ def run(*args):
 def main():
     name = sys.argv[1] if len(sys.argv) > 1 else "round1_ncu"
     tname = sys.argv[2] if len(sys.argv) > 2 else "round1_traffic"
-    parts = ["# Round 1 — ncu evidence (large config: 65,536 candidates, L=64, d_model 256, 4 layers, bf16 projections)\n",
+    prefix = sys.argv[3] if len(sys.argv) > 3 else "official"
+    rnd = name.split("_")[0].replace("round", "Round ")
+    parts = [f"# {rnd} — ncu evidence (large config: 65,536 candidates, L=64, d_model 256, 4 layers, bf16 projections)\n",
              "Source: `scripts/gpu_official.sh` on one B200 via gpurun. Full captures: `ncu --set full --clock-control none "
              "--import-source on -k regex:<kernel> -s 4 -c 1 python bench.py --steps 1 --warmup 3`; launch list: `ncu "
              "--metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`. ncu times are "
              "serialised and cold-cache: compare shares, not absolutes; bench.py's CUDA-event stage times are the live "
              "numbers. (k_ex2 / k_tanh / k_ffma / k_ffma2 are bench.py's peak microbenchmarks, run outside the timed "
              "region; k_pack / k_pool_bf16 captures use -s 3.)\n", "## Bench line of the same build\n"]
-    for f in ("bench_official.json", "bench_reference.json"):
+    for f in (f"bench_{prefix}.json", f"bench_reference_{prefix}.json", "bench_reference.json"):
         p = os.path.join(OUT, f)
         if os.path.exists(p):
             parts.append("```json\n" + open(p).read().strip() + "\n```\n")
     parts.append("## Launch list (all kernels of 2 timed + 3 warm-up steps + setup)\n")
-    parts.append(run("launches", os.path.join(OUT, "launches_official.csv")))
+    parts.append(run("launches", os.path.join(OUT, f"launches_{prefix}.csv")))
     parts.append("## Per-kernel full captures\n")
-    reps = sorted(f for f in os.listdir(OUT) if f.startswith("prof_official_") and f.endswith(".ncu-rep"))
-    order = ["k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_simt", "k_topk_radix", "k_pool_bf16", "k_pack"]
+    reps = sorted(f for f in os.listdir(OUT) if f.startswith(f"prof_{prefix}_") and f.endswith(".ncu-rep"))
+    order = ["k_scan", "k_mixprep", "k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_tf32", "k_head",
+             "k_gemm_simt", "k_topk_radix", "k_pool_bf16", "k_pack"]
     reps.sort(key=lambda f: next((i for i, k in enumerate(order) if k in f), 99))
     for f in reps:
         parts.append(run("report", os.path.join(OUT, f)))
     open(os.path.join(ROOT, "profiles", name + ".md"), "w").write("\n".join(parts))
     # traffic per launch of the dominant kernels
     traffic = {}
-    for key, rep in (("mixer", "k_mixer_fused"), ("in_proj", "k_gemm_tc"), ("out_proj", "k_gemm_ln")):
-        p = os.path.join(OUT, f"prof_official_{rep}.ncu-rep")
+    for key, rep in (("scan", "k_scan"), ("mixprep", "k_mixprep"), ("mixer", "k_mixer_fused"), ("in_proj", "k_gemm_tc"),
+                     ("out_proj", "k_gemm_ln"), ("encoder", "k_enc12")):
+        p = os.path.join(OUT, f"prof_{prefix}_{rep}.ncu-rep")
         if not os.path.exists(p):
             continue
         csv = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv", "--metrics",
@@ -60,7 +64,7 @@ def main():
             return float(row[i].replace(",", "")) * mult.get(units[i], 1)
         traffic[key] = {"kernel": row[hdr.index("Kernel Name")][:60], "dram_bytes_read": val("dram__bytes_read.sum"),
                         "dram_bytes_write": val("dram__bytes_write.sum"),
-                        "source": f"profiles/{name}.md (prof_official_{rep}.ncu-rep)"}
+                        "source": f"profiles/{name}.md (prof_{prefix}_{rep}.ncu-rep)"}
     if traffic:
         json.dump(traffic, open(os.path.join(ROOT, "profiles", tname + ".json"), "w"), indent=1)
     print("wrote", name, list(traffic))

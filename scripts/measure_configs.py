@@ -20,6 +20,7 @@ import inputs  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--sample", type=int, default=512)
+    ap.add_argument("--full-large", action="store_true", help="score all 65,536 `large` candidates with the oracle")
     args = ap.parse_args()
     import torch
     from oracle import oracle as O
@@ -30,7 +31,7 @@ def main():
         c = inputs.config(name)
         d = c["dims"]
         w = inputs.make_weights(d, c["seed"])
-        n = min(c["n"], args.sample if name in ("large", "long") else c["n"])
+        n = min(c["n"], args.sample if name == "long" or (name == "large" and not args.full_large) else c["n"])
         f, l = inputs.make_features(d, n, c["seed"] + 1, workload=wl[name])
         m = Model(w, d)
         ft, lt = torch.from_numpy(f).cuda(), torch.from_numpy(l).cuda()
@@ -53,6 +54,13 @@ def main():
         res["max_abs_err"] = float(err.max())
         res["max_rel_err_vs_max1"] = float((err / np.maximum(1.0, np.abs(ref))).max())
         res["score_std"] = float(ref.std())
+        res["max_abs_err_over_std"] = float(err.max() / ref.std())
+        rel = err / np.maximum(np.abs(ref), 1e-30)
+        res["rel_err_median"] = float(np.median(rel))
+        res["rel_err_p99"] = float(np.percentile(rel, 99))
+        rg = np.argsort(np.argsort(got, kind="stable"), kind="stable")
+        rr = np.argsort(np.argsort(ref, kind="stable"), kind="stable")
+        res["spearman"] = float(np.corrcoef(rg, rr)[0, 1])
         k = c["topk"] or 16
         gi = np.argsort(-got, kind="stable")[:k]
         ri, _ = O.topk(ref, k)
