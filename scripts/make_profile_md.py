@@ -24,7 +24,7 @@ def main():
     prefix = sys.argv[3] if len(sys.argv) > 3 else "official"
     rnd = name.split("_")[0].replace("round", "Round ")
     parts = [f"# {rnd} — ncu evidence (large config: 65,536 candidates, L=64, d_model 256, 4 layers, bf16 projections)\n",
-             "Source: `scripts/gpu_official.sh` on one B200 via gpurun. Full captures: `ncu --set full --clock-control none "
+             f"Source: `scripts/gpu_official{'_r2' if prefix == 'r2' else ''}.sh` on one B200 via gpurun. Full captures: `ncu --set full --clock-control none "
              "--import-source on -k regex:<kernel> -s 4 -c 1 python bench.py --steps 1 --warmup 3`; launch list: `ncu "
              "--metrics gpu__time_duration.sum --clock-control none` over `bench.py --steps 2 --warmup 3`. ncu times are "
              "serialised and cold-cache: compare shares, not absolutes; bench.py's CUDA-event stage times are the live "
