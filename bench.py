@@ -137,8 +137,8 @@ def stage_model(d, P: int, n: int):
         "x_proj": dict(flops=2 * P * di * (R + 2 * N), bytes=P * di * 4 + P * (R + 2 * N) * 4),
         "dt_proj": dict(flops=2 * P * R * di, bytes=P * R * 4 + P * di * 4),
         # scan: u, delta, z in; g out (fp32) + B, C per token; N exps per (t, d).  bf16 path (split
-        # mixer): the packet (u, Delta fp16, B, C fp32, SiLU(z) bf16) in, g (bf16) out
-        "scan": (dict(bytes=P * (6 * di + 8 * N) + P * di * 2, exps=P * di * N) if bf16 else
+        # mixer): the packet (u, Delta fp16, B, C fp32) and SiLU(z) (bf16) in, g (bf16) out
+        "scan": (dict(bytes=P * (4 * di + 8 * N) + P * di * 2 + P * di * 2, exps=P * di * N) if bf16 else
                  dict(bytes=P * di * (3 * 4 + act) + P * 2 * N * 4, exps=P * di * N)),
         # bf16 mixer prep: x (bf16) in; u, Delta (fp16), B, C (fp32) out; x_proj + dt_proj flops
         "mixprep": dict(bytes=P * di * 2 + P * (4 * di + 8 * N), flops=2 * P * di * (R + 2 * N) + 2 * P * R * di),

@@ -310,6 +310,7 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         TAKE(Gb, rows * di);
         w.pk_ld = mixer_packet_bytes(di, d.d_state);
         TAKE(Pk, rows * w.pk_ld);
+        TAKE(GZb, rows * di);
         const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
         __nv_bfloat16* E1b = w.XZb;
         __nv_bfloat16* E2b = w.XZb + rows * e1;
@@ -324,7 +325,7 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
         // split mixer: in_proj writes x as [rows][di] (the XZb storage) and SiLU(z) into the packet
         ok = ok && make_tmap_bf16(&w.tmXo, w.XZb, di, rows, (uint64_t)di * 2, 64, 32) &&
-             make_tmap_bf16(&w.tmGZo, w.Pk + mixer_packet_gz_offset(di, d.d_state), di, rows, (uint64_t)w.pk_ld, 64, 32);
+             make_tmap_bf16(&w.tmGZo, w.GZb, di, rows, (uint64_t)di * 2, 64, 32);
         ok = ok && make_tmap_f32(&w.tmHf, w.H, dm, rows, (uint64_t)dm * 4, 32, 32);
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
         const int nt_in = 2 * di / m->bn_in;
@@ -712,8 +713,8 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
             TcGemmParams p = base();
             p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            // SiLU(z) (the scan's gate) is formed in this HBM-bound epilogue (idle SFU) and written
-            // straight into the mixer packet; x goes to its own [rows][di] buffer for k_mixprep
+            // SiLU(z) (the scan's gate) is formed in this HBM-bound epilogue (idle SFU); x and SiLU(z)
+            // go to their own [rows][di] buffers (k_mixprep reads x, k_scan reads SiLU(z))
             p.silu_from = di;
             p.split_col = di;
             // A tiles shared by TMA multicast inside clusters of 2 CTAs (N tiles 2j, 2j+1 of the same
@@ -744,7 +745,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         {   // the selective scan + D skip + gate (SFU-bound)
             ProfScope ps(m, TCL_PROF_SCAN, s);
             ScanBf16Args a{};
-            a.Pk = w.Pk; a.G = w.Gb;
+            a.Pk = w.Pk; a.GZ = w.GZb; a.G = w.Gb;
             a.A2 = m->A2 + (size_t)l * di * N; a.invA = m->invA + (size_t)l * di * N; a.Dv = q.Dv;
             a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.disc = d.disc;
             if ((e = launch_scan_bf16(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "scan");
@@ -1262,8 +1263,11 @@ tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t ro
         if (cols != want) return set_error(TCL_EINVAL, "cols does not match the buffer");
         std::vector<uint8_t> pk((size_t)rows * w.pk_ld);
         CUDA_TRY(cudaMemcpy(pk.data(), w.Pk, pk.size(), cudaMemcpyDeviceToHost));
-        std::vector<uint16_t> xb((size_t)rows * di);
-        if (nm == "XZ") CUDA_TRY(cudaMemcpy(xb.data(), w.XZb, xb.size() * 2, cudaMemcpyDeviceToHost));
+        std::vector<uint16_t> xb((size_t)rows * di), zb((size_t)rows * di);
+        if (nm == "XZ") {
+            CUDA_TRY(cudaMemcpy(xb.data(), w.XZb, xb.size() * 2, cudaMemcpyDeviceToHost));
+            CUDA_TRY(cudaMemcpy(zb.data(), w.GZb, zb.size() * 2, cudaMemcpyDeviceToHost));
+        }
         auto bf = [](uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; };
         auto hf = [](uint16_t h) { __half_raw r; r.x = h; return __half2float(__half(r)); };
         for (int64_t r = 0; r < rows; ++r) {
@@ -1272,7 +1276,7 @@ tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t ro
                 float v;
                 uint16_t h;
                 if (nm == "XZ" && c < di) v = bf(xb[(size_t)r * di + c]);
-                else if (nm == "XZ") { memcpy(&h, row + 4 * di + 8 * N + 2 * (c - di), 2); v = bf(h); }
+                else if (nm == "XZ") v = bf(zb[(size_t)r * di + c - di]);
                 else if (nm == "U") { memcpy(&h, row + 2 * c, 2); v = hf(h); }
                 else if (nm == "DELTA") { memcpy(&h, row + 2 * di + 2 * c, 2); v = hf(h); }
                 else memcpy(&v, row + 4 * di + 4 * c, 4);

@@ -121,9 +121,10 @@ struct Workspace {
     __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden
     __nv_bfloat16* Ab = nullptr;   // [rows][dm]    LN_l(H)
     __nv_bfloat16* Gb = nullptr;   // [rows][di]    gated scan output
-    uint8_t* Pk = nullptr;         // [rows][pk_ld] mixer packet: u, Delta (fp16), B, C (fp32), SiLU(z) (bf16)
-    int pk_ld = 0;                 // packet row bytes (6 di + 8 N)
-    CUtensorMap tmXo, tmGZo;       // in_proj outputs: x -> XZb as [rows][di] (box {64, 32}); SiLU(z) -> packet
+    uint8_t* Pk = nullptr;         // [rows][pk_ld] mixer packet: u, Delta (fp16), B, C (fp32)
+    int pk_ld = 0;                 // packet row bytes (4 di + 8 N)
+    __nv_bfloat16* GZb = nullptr;  // [rows][di] SiLU(z), the scan's gate (in_proj epilogue)
+    CUtensorMap tmXo, tmGZo;       // in_proj outputs: x -> XZb as [rows][di], SiLU(z) -> GZb (box {64, 32})
     CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
     CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
     CUtensorMap tmHf, tmAo;                            // residual stream fp32 (box {32,32}), LN out (box {64,32})

@@ -12,12 +12,14 @@
 // phase split: 2.73 ms scan alone vs 3.86 ms fused at `large`).  Here that work runs in an
 // HBM-bound kernel of its own, and the scan kernel does nothing but the recurrence.
 //
-// The two kernels meet in a per-token "mixer packet" (one row per packed token, written by three
-// producers, read by the scan as ONE contiguous bulk copy per 16-token chunk):
-//     [ u fp16 x DI | Delta fp16 x DI | B, C fp32 x 2N | SiLU(z) bf16 x DI ]      (6 DI + 8 N bytes)
-// u and Delta are stored in fp16 (10-bit mantissa: 8x finer than bf16; both are bounded: u is a
-// SiLU of a 4-tap conv, Delta a softplus), B and C in fp32; SiLU(z) comes from the in_proj
-// epilogue (bf16, the GEMM output precision of this path).
+// The two kernels meet in a per-token "mixer packet" written by k_mixprep (one row per packed
+// token, read by the scan as ONE contiguous bulk copy per 16-token chunk):
+//     [ u fp16 x DI | Delta fp16 x DI | B, C fp32 x 2N ]                          (4 DI + 8 N bytes)
+// plus the gate SiLU(z) [P][DI] bf16 that the in_proj epilogue writes contiguously (a second bulk
+// copy per chunk; written into the packet rows instead, the strided 128-byte row pieces cost the
+// in_proj 0.08 ms per layer at `large`: 0.735 vs 0.657 ms).  u and Delta are stored in fp16 (10-bit
+// mantissa: 8x finer than bf16; both are bounded: u is a SiLU of a 4-tap conv, Delta a softplus),
+// B and C in fp32.
 //
 // Work decomposition (both kernels): persistent CTAs of DI threads, thread d owns channel d; each
 // CTA owns the packed rows of a contiguous candidate range (balanced by rows) and walks them in
@@ -314,9 +316,10 @@ __global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
 // ============================================================================ k_scan
 template <int DI, int N, int STAGES>
 struct ScanSmem {
-    static constexpr int kRow = 6 * DI + 8 * N;                    // packet row bytes
-    static constexpr int kPk = 0;                                  // [STAGES][16][kRow]
-    static constexpr int kBar = kPk + STAGES * kTC * kRow;         // STAGES mbarriers
+    static constexpr int kRow = 4 * DI + 8 * N;                    // packet row bytes
+    static constexpr int kStage = kTC * (kRow + 2 * DI);           // 16 packet rows, then 16 SiLU(z) rows
+    static constexpr int kPk = 0;                                  // [STAGES][kStage]
+    static constexpr int kBar = kPk + STAGES * kStage;             // STAGES mbarriers
     static constexpr int kStarts = kBar + 8 * STAGES + 8;
     static constexpr int kBytes = kStarts + 4 * kStartWords;
 };
@@ -348,9 +351,10 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
     int64_t k_next = rr.c0;
     auto issue = [&](int64_t r, int b) {
         if (d == 0 && r < rr.r_end) {
-            const uint32_t bytes = (uint32_t)(rr.r_end - r < kTC ? rr.r_end - r : kTC) * kRow;
-            tc::mbar_arrive_expect_tx(&bar[b], bytes);
-            bulk_g2s(pk_s + b * kTC * kRow, a.Pk + r * (int64_t)kRow, bytes, &bar[b]);
+            const uint32_t rows = (uint32_t)(rr.r_end - r < kTC ? rr.r_end - r : kTC);
+            tc::mbar_arrive_expect_tx(&bar[b], rows * (kRow + 2 * DI));
+            bulk_g2s(pk_s + b * L::kStage, a.Pk + r * (int64_t)kRow, rows * kRow, &bar[b]);
+            bulk_g2s(pk_s + b * L::kStage + kTC * kRow, a.GZ + r * (int64_t)DI, rows * 2 * DI, &bar[b]);
         }
     };
 #pragma unroll
@@ -365,7 +369,8 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
         const uint32_t starts = chunk_starts(bits, st_w, chunk, a.cu, k_next, rr.c1, r0, tc);
         tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
         parity ^= 1u << buf;
-        const uint8_t* row = pk_s + buf * kTC * kRow;
+        const uint8_t* row = pk_s + buf * L::kStage;
+        const __nv_bfloat16* gzp = reinterpret_cast<const __nv_bfloat16*>(pk_s + buf * L::kStage + kTC * kRow) + d;
         __nv_bfloat16* gout = a.G + r0 * DI + d;
         // one token: the row pointer advances by a compile-time stride, so in the unrolled
         // full-chunk loop every shared-memory access is base + immediate
@@ -378,7 +383,7 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
             const float dl = __half2float(reinterpret_cast<const __half*>(row + 2 * DI)[d]);
             const float4* B4 = reinterpret_cast<const float4*>(row + 4 * DI);
             const float4* C4 = reinterpret_cast<const float4*>(row + 4 * DI + 4 * N);
-            const float gz = __bfloat162float(reinterpret_cast<const __nv_bfloat16*>(row + 4 * DI + 8 * N)[d]);
+            const float gz = __bfloat162float(gzp[0]);
             const float2 dl2 = make_float2(dl, dl);
             const float2 u2 = make_float2(u, u);
             float2 y2 = make_float2(0.f, 0.f), y2b = make_float2(0.f, 0.f);
@@ -419,6 +424,7 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
             const float y = fmaf(Dv, u, (y2.x + y2b.x) + (y2.y + y2b.y));
             gout[0] = __float2bfloat16_rn(y * gz);
             row += kRow;
+            gzp += DI;
             gout += DI;
         };
         if (tc == kTC) {
@@ -484,7 +490,7 @@ static cudaError_t prep_rp(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
 
 }  // namespace mx
 
-int mixer_packet_bytes(int di, int N) { return 6 * di + 8 * N; }
+int mixer_packet_bytes(int di, int N) { return 4 * di + 8 * N; }
 
 cudaError_t launch_mixprep(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
     using namespace mx;

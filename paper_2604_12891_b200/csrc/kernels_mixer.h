@@ -7,10 +7,10 @@
 namespace tcl {
 
 // ---- split mixer (mixer_split.cu): k_mixprep (conv + x_proj + dt_proj) then k_scan (recurrence).
-// Mixer packet, one row of mixer_packet_bytes(DI, N) = 6 DI + 8 N bytes per packed token:
-//   [ u fp16 x DI | Delta fp16 x DI | B fp32 x N, C fp32 x N | SiLU(z) bf16 x DI ]
+// Mixer packet, one row of mixer_packet_bytes(DI, N) = 4 DI + 8 N bytes per packed token:
+//   [ u fp16 x DI | Delta fp16 x DI | B fp32 x N, C fp32 x N ]; the gate SiLU(z) is a separate
+//   [P][DI] bf16 array (in_proj epilogue).
 int mixer_packet_bytes(int di, int N);
-inline int mixer_packet_gz_offset(int di, int N) { return 4 * di + 8 * N; }
 
 struct MixPrepArgs {
     const __nv_bfloat16* X;              // in_proj x part [P][DI] (bf16, rows contiguous)
@@ -27,7 +27,8 @@ struct MixPrepArgs {
 cudaError_t launch_mixprep(const MixPrepArgs& a, int num_sms, cudaStream_t s);
 
 struct ScanBf16Args {
-    const uint8_t* Pk;                   // mixer packet [P][6 DI + 8 N bytes] (all four parts)
+    const uint8_t* Pk;                   // mixer packet [P][4 DI + 8 N bytes]
+    const __nv_bfloat16* GZ;             // SiLU(z) [P][DI] (in_proj epilogue)
     __nv_bfloat16* G;                    // gated output [P][DI]
     const float* A2;                     // [DI][N]  A * log2(e)
     const float* invA;                   // [DI][N]  1 / A   (ZOH)
