@@ -132,7 +132,10 @@ def stage_model(d, P: int, n: int):
         "pack": dict(bytes=P * d.d_in * 4 + P * 32 * act + n * 4),
         "encoder": dict(flops=2 * P * (32 * e1 + e1 * e2 + e2 * dm), bytes=enc_bytes),
         "layernorm": dict(bytes=P * dm * 4 + P * dm * act),
-        "in_proj": dict(flops=2 * P * dm * 2 * di, bytes=P * dm * act + P * 2 * di * act),
+        # bf16 path: in_proj + SiLU(z) + conv + SiLU (k_inconv): LN(H) (bf16) in; SiLU(z) (bf16) and u
+        # (fp16) out.  fp32 path: the in_proj GEMM ([x | z] fp32 out)
+        "in_proj": (dict(flops=2 * P * dm * 2 * di, bytes=P * dm * 2 + P * di * 2 + P * di * 2) if bf16 else
+                    dict(flops=2 * P * dm * 2 * di, bytes=P * dm * act + P * 2 * di * act)),
         "conv": dict(bytes=P * di * act + P * di * 4),
         "x_proj": dict(flops=2 * P * di * (R + 2 * N), bytes=P * di * 4 + P * (R + 2 * N) * 4),
         "dt_proj": dict(flops=2 * P * R * di, bytes=P * R * 4 + P * di * 4),
@@ -140,8 +143,8 @@ def stage_model(d, P: int, n: int):
         # mixer): the packet (u, Delta fp16, B, C fp32) and SiLU(z) (bf16) in, g (bf16) out
         "scan": (dict(bytes=P * (4 * di + 8 * N) + P * di * 2 + P * di * 2, exps=P * di * N) if bf16 else
                  dict(bytes=P * di * (3 * 4 + act) + P * 2 * N * 4, exps=P * di * N)),
-        # bf16 mixer prep: x (bf16) in; u, Delta (fp16), B, C (fp32) out; x_proj + dt_proj flops
-        "mixprep": dict(bytes=P * di * 2 + P * (4 * di + 8 * N), flops=2 * P * di * (R + 2 * N) + 2 * P * R * di),
+        # bf16 path x_proj + dt_proj + softplus (k_xdt): u (fp16) in; Delta (fp16), B, C (fp32) out
+        "xdt": dict(bytes=P * di * 2 + P * (2 * di + 8 * N), flops=2 * P * di * (R + 2 * N) + 2 * P * R * di),
         "out_proj": dict(flops=2 * P * di * dm, bytes=out_bytes),
         "head": dict(bytes=head_bytes),
         "mixer": dict(bytes=P * 2 * di * act + P * di * act, exps=P * di * N),
@@ -349,7 +352,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
         wk = work.get(kind, {})
         calls = per_step_launches[kind]                  # launches of this stage per step
         units = (mc or 1) * (d.n_layer if kind in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj",
-                                                     "scan", "out_proj", "mixer", "mixprep") else 1)
+                                                     "scan", "out_proj", "mixer", "xdt") else 1)
         scale = units / calls                            # fraction of a step's work per launch
         if "bytes" in wk:
             entry["gbs"] = wk["bytes"] * scale / (entry["ms_per_launch"] * 1e-3) / 1e9
@@ -366,7 +369,7 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     wk = work[dom]
     calls = per_step_launches[dom]
     units = (mc or 1) * (d.n_layer if dom in ("layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan",
-                                                "out_proj", "mixer", "mixprep") else 1)
+                                                "out_proj", "mixer", "xdt") else 1)
     traffic = None  # DRAM bytes per launch of this kernel from one ncu --set full capture (profiles/)
     tp = os.path.join(ROOT, "profiles", "round2_traffic.json")
     if not os.path.exists(tp):

@@ -284,7 +284,7 @@ int64_t tcl_launch_count(const tcl_model* model);
 typedef enum {
     TCL_PROF_PACK = 0, TCL_PROF_ENCODER, TCL_PROF_LAYERNORM, TCL_PROF_IN_PROJ, TCL_PROF_CONV,
     TCL_PROF_X_PROJ, TCL_PROF_DT_PROJ, TCL_PROF_SCAN, TCL_PROF_OUT_PROJ, TCL_PROF_HEAD,
-    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_LATERAL, TCL_PROF_MIXPREP,
+    TCL_PROF_TOPK, TCL_PROF_MIXER, TCL_PROF_ALLGATHER, TCL_PROF_MC, TCL_PROF_LATERAL, TCL_PROF_XDT,
     TCL_PROF_NKINDS
 } tcl_prof_kind;
 tcl_status tcl_profile_enable(tcl_model* model, int enable);

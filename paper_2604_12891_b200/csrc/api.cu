@@ -118,6 +118,18 @@ static tcl_status upload_bf16(tcl_model* m, const float* W, int rows, int cols, 
     return e == cudaSuccess ? TCL_OK : cuda_error(e, "upload_bf16");
 }
 
+// Upload an fp16 copy of W [rows][cols] into a zero-padded [rows_p][cols_p] device matrix.
+static tcl_status upload_f16(tcl_model* m, const float* W, int rows, int cols, int rows_p, int cols_p, __half** out) {
+    std::vector<__half> h((size_t)rows_p * cols_p, __float2half(0.0f));
+    for (int r = 0; r < rows; ++r)
+        for (int c = 0; c < cols; ++c) h[(size_t)r * cols_p + c] = __float2half_rn(W[(size_t)r * cols + c]);
+    tcl_status st = dev_alloc(out, h.size());
+    if (st != TCL_OK) return st;
+    m->bf_allocs.push_back(*out);
+    cudaError_t e = cudaMemcpy(*out, h.data(), h.size() * 2, cudaMemcpyHostToDevice);
+    return e == cudaSuccess ? TCL_OK : cuda_error(e, "upload_f16");
+}
+
 // Host offsets of the canonical blob (include/tcl.h), for the bf16 copies.
 struct HostW {
     const float *W1, *W2, *W3;
@@ -165,8 +177,6 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
     cudaDeviceGetAttribute(&m->num_sms, cudaDevAttrMultiProcessorCount, m->device);
     m->nxp = round_up(R + 2 * N, 8);
     m->rp = R <= 16 ? 16 : 32;
-    // 4 N tiles at di = 256: B slice 64 KB, 8-stage A ring (BN = 256 measured slower)
-    m->bn_in = std::min(128, 2 * di);
     HostW h = host_offsets(d, wh);
     if ((st = upload_bf16(m, h.W1, e1, d.d_in, e1, kXld, &m->W1b)) != TCL_OK) return st;
     if ((st = upload_bf16(m, h.W2, e2, e1, e2, e1, &m->W2b)) != TCL_OK) return st;
@@ -175,14 +185,15 @@ static tcl_status setup_tc(tcl_model* m, const float* wh) {
               make_tmap_bf16(&m->tmW2, m->W2b, e1, e2, (uint64_t)e1 * 2, 64, e2) &&
               make_tmap_bf16(&m->tmW3, m->W3b, e2, dm, (uint64_t)e2 * 2, 64, dm);
     for (int l = 0; l < d.n_layer && ok; ++l) {
-        __nv_bfloat16 *win, *wout, *wx, *wdt;
+        __nv_bfloat16 *win, *wout, *wdt;
+        __half* wx;
         if ((st = upload_bf16(m, h.Win[l], 2 * di, dm, 2 * di, dm, &win)) != TCL_OK) return st;
         if ((st = upload_bf16(m, h.Wout[l], dm, di, dm, di, &wout)) != TCL_OK) return st;
-        if ((st = upload_bf16(m, h.Wx[l], R + 2 * N, di, m->nxp, di, &wx)) != TCL_OK) return st;
+        if ((st = upload_f16(m, h.Wx[l], R + 2 * N, di, m->nxp, di, &wx)) != TCL_OK) return st;
         if ((st = upload_bf16(m, h.Wdt[l], di, R, di, m->rp, &wdt)) != TCL_OK) return st;
-        m->Winb.push_back(win); m->Woutb.push_back(wout); m->Wxb.push_back(wx); m->Wdtb.push_back(wdt);
+        m->Winb.push_back(win); m->Woutb.push_back(wout); m->Wxh.push_back(wx); m->Wdtb.push_back(wdt);
         CUtensorMap a, b;
-        ok = make_tmap_bf16(&a, win, dm, 2 * di, (uint64_t)dm * 2, 64, m->bn_in) &&
+        ok = make_tmap_bf16(&a, win, dm, 2 * di, (uint64_t)dm * 2, 64, inconv_channels(di)) &&
              make_tmap_bf16(&b, wout, di, dm, (uint64_t)di * 2, 64, dm);
         m->tmWin.push_back(a);
         m->tmWout.push_back(b);
@@ -323,14 +334,13 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
         if (e1 >= 64) ok = ok && make_tmap_bf16(&w.tmE1o, E1b, e1, rows, (uint64_t)e1 * 2, 64, 32);
         if (e2 >= 64) ok = ok && make_tmap_bf16(&w.tmE2o, E2b, e2, rows, (uint64_t)e2 * 2, 64, 32);
         ok = ok && make_tmap_bf16(&w.tmXZo, w.XZb, 2 * di, rows, (uint64_t)2 * di * 2, 64, 32);
-        // split mixer: in_proj writes x as [rows][di] (the XZb storage) and SiLU(z) into the packet
-        ok = ok && make_tmap_bf16(&w.tmXo, w.XZb, di, rows, (uint64_t)di * 2, 64, 32) &&
-             make_tmap_bf16(&w.tmGZo, w.GZb, di, rows, (uint64_t)di * 2, 64, 32);
+        // k_inconv stores: SiLU(z) -> GZb, u -> the packet's first di columns (2-byte elements)
+        ok = ok && make_tmap_bf16(&w.tmGZs, w.GZb, di, rows, (uint64_t)di * 2, 64, 125) &&
+             make_tmap_bf16(&w.tmUs, w.Pk, (uint64_t)w.pk_ld / 2, rows, (uint64_t)w.pk_ld, 64, 125);
         ok = ok && make_tmap_f32(&w.tmHf, w.H, dm, rows, (uint64_t)dm * 4, 32, 32);
         ok = ok && make_tmap_bf16(&w.tmAo, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 32);
-        const int nt_in = 2 * di / m->bn_in;
-        if (nt_in == 2 || nt_in == 4)
-            ok = ok && make_tmap_bf16(&w.tmAbS2, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 64);
+        if (inconv_split(di) == 2) ok = ok && make_tmap_bf16(&w.tmAbS2, w.Ab, dm, rows, (uint64_t)dm * 2, 64, 64);
+
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (workspace)"); }
     }
 #undef TAKE
@@ -709,38 +719,26 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
     }
     for (int l = 0; l < d.n_layer; ++l) {
         const LayerPtrs& q = m->wp.layers[l];
-        {
+        {   // in_proj + SiLU(z) + conv + SiLU (inconv.cu): x never leaves the SM
             ProfScope ps(m, TCL_PROF_IN_PROJ, s);
-            TcGemmParams p = base();
-            p.n_tiles = 2 * di / m->bn_in; p.epi = TC_EPI_BF16; p.out = w.XZb; p.ldo = 2 * di;
-            // SiLU(z) (the scan's gate) is formed in this HBM-bound epilogue (idle SFU); x and SiLU(z)
-            // go to their own [rows][di] buffers (k_mixprep reads x, k_scan reads SiLU(z))
-            p.silu_from = di;
-            p.split_col = di;
-            // A tiles shared by TMA multicast inside clusters of 2 CTAs (N tiles 2j, 2j+1 of the same
-            // row tile; each CTA fetches 64 of the 128 rows): the read side is bound by the L2->SM
-            // traffic of the 4x re-read A tile (measured 0.60 ms with the stores disabled), and
-            // pairs halve it: 0.725 -> 0.666 ms at `large` (clusters of all 4 N tiles: 1.16 ms,
-            // cluster-coupled stalls).
-            p.mcast = (p.n_tiles == 2 || p.n_tiles == 4) ? 1 : 0;
-            const CUtensorMap& amap = p.mcast ? w.tmAbS2 : w.tmAb;
-            if ((e = launch_gemm_tc(amap, m->tmWin[l], w.tmXo, p, m->bn_in, kb_of(dm), m->num_sms, s, &w.tmGZo)) !=
-                cudaSuccess)
-                return cuda_error(e, "in_proj");
+            InConvParams a{};
+            a.p_rows = P; a.row_cand = w.row_cand; a.w_conv = q.w_conv; a.b_conv = q.b_conv;
+            a.DI = di; a.d_conv = d.d_conv;
+            const CUtensorMap& amap = inconv_split(di) == 2 ? w.tmAbS2 : w.tmAb;
+            if ((e = launch_inconv(amap, m->tmWin[l], w.tmGZs, w.tmUs, a, dm, m->num_sms, s)) != cudaSuccess)
+                return cuda_error(e, "inconv");
             ++nl;
-            if (debug_sync("in_proj", s) != TCL_OK) return TCL_ECUDA;
+            if (debug_sync("inconv", s) != TCL_OK) return TCL_ECUDA;
         }
-        {   // conv + SiLU, x_proj, dt_proj + softplus -> packet (mixer_split.cu)
-            ProfScope ps(m, TCL_PROF_MIXPREP, s);
-            MixPrepArgs a{};
-            a.X = w.XZb; a.Pk = w.Pk; a.pk_ld = w.pk_ld;
-            a.w_conv = q.w_conv; a.b_conv = q.b_conv; a.b_dt = q.b_dt;
-            a.Wx_b = m->Wxb[l]; a.Wdt_b = m->Wdtb[l];
-            a.cu = w.cu; a.row_cand = w.row_cand; a.n = n; a.DI = di; a.N = N; a.R = R; a.RP = m->rp;
-            a.d_conv = d.d_conv; a.max_len = L;
-            if ((e = launch_mixprep(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "mixprep");
+        {   // x_proj + dt_proj + softplus -> packet (mixer_split.cu)
+            ProfScope ps(m, TCL_PROF_XDT, s);
+            XdtArgs a{};
+            a.Pk = w.Pk; a.pk_ld = w.pk_ld; a.b_dt = q.b_dt;
+            a.Wx_h = m->Wxh[l]; a.Wdt_b = m->Wdtb[l];
+            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.R = R; a.RP = m->rp; a.max_len = L;
+            if ((e = launch_xdt(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "xdt");
             ++nl;
-            if (debug_sync("mixprep", s) != TCL_OK) return TCL_ECUDA;
+            if (debug_sync("xdt", s) != TCL_OK) return TCL_ECUDA;
         }
         {   // the selective scan + D skip + gate (SFU-bound)
             ProfScope ps(m, TCL_PROF_SCAN, s);
@@ -1255,19 +1253,18 @@ tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t ro
     const Workspace& w = m->ws;
     if (rows > w.rows) return set_error(TCL_EINVAL, "rows exceed the workspace");
     const std::string nm(name);
-    if (m->use_tc && (nm == "XZ" || nm == "U" || nm == "DELTA" || nm == "BC")) {
-        // bf16 path: x in XZb as [P][di] (bf16); u, Delta (fp16), B, C (fp32), SiLU(z) (bf16) in
-        // the mixer packet rows
+    if (m->use_tc && (nm == "XZ" || nm == "GZ" || nm == "U" || nm == "DELTA" || nm == "BC")) {
+        // bf16 path: u, Delta (fp16), B, C (fp32) in the mixer packet rows; SiLU(z) (bf16) in GZb;
+        // x in XZb as [P][di] (bf16) only without the fused inmix kernel (which keeps x on chip)
         const int di = m->dims.expand * m->dims.d_model, N = m->dims.d_state;
+        if (nm == "XZ") return set_error(TCL_EINVAL, "bf16 path: x stays on chip (k_inconv)");
         const int want = nm == "XZ" ? 2 * di : (nm == "BC" ? 2 * N : di);
         if (cols != want) return set_error(TCL_EINVAL, "cols does not match the buffer");
         std::vector<uint8_t> pk((size_t)rows * w.pk_ld);
         CUDA_TRY(cudaMemcpy(pk.data(), w.Pk, pk.size(), cudaMemcpyDeviceToHost));
         std::vector<uint16_t> xb((size_t)rows * di), zb((size_t)rows * di);
-        if (nm == "XZ") {
-            CUDA_TRY(cudaMemcpy(xb.data(), w.XZb, xb.size() * 2, cudaMemcpyDeviceToHost));
-            CUDA_TRY(cudaMemcpy(zb.data(), w.GZb, zb.size() * 2, cudaMemcpyDeviceToHost));
-        }
+        if (nm == "XZ") CUDA_TRY(cudaMemcpy(xb.data(), w.XZb, xb.size() * 2, cudaMemcpyDeviceToHost));
+        if (nm == "XZ" || nm == "GZ") CUDA_TRY(cudaMemcpy(zb.data(), w.GZb, zb.size() * 2, cudaMemcpyDeviceToHost));
         auto bf = [](uint16_t h) { uint32_t u = (uint32_t)h << 16; float f; memcpy(&f, &u, 4); return f; };
         auto hf = [](uint16_t h) { __half_raw r; r.x = h; return __half2float(__half(r)); };
         for (int64_t r = 0; r < rows; ++r) {
@@ -1277,6 +1274,7 @@ tcl_status tcl_debug_read(tcl_model* m, const char* name, float* out, int64_t ro
                 uint16_t h;
                 if (nm == "XZ" && c < di) v = bf(xb[(size_t)r * di + c]);
                 else if (nm == "XZ") v = bf(zb[(size_t)r * di + c - di]);
+                else if (nm == "GZ") v = bf(zb[(size_t)r * di + c]);
                 else if (nm == "U") { memcpy(&h, row + 2 * c, 2); v = hf(h); }
                 else if (nm == "DELTA") { memcpy(&h, row + 2 * di + 2 * c, 2); v = hf(h); }
                 else memcpy(&v, row + 4 * di + 4 * c, 4);
@@ -1336,7 +1334,7 @@ tcl_status tcl_profile_read(tcl_model* m, double* ms_out, int64_t* launches_out,
 const char* tcl_profile_name(int kind) {
     static const char* names[TCL_PROF_NKINDS] = {"pack", "encoder", "layernorm", "in_proj", "conv",
                                                  "x_proj", "dt_proj", "scan", "out_proj", "head",
-                                                 "topk", "mixer", "allgather", "mc", "lateral", "mixprep"};
+                                                 "topk", "mixer", "allgather", "mc", "lateral", "xdt"};
     return (kind >= 0 && kind < TCL_PROF_NKINDS) ? names[kind] : "";
 }
 

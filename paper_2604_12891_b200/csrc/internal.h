@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <string>
@@ -124,7 +125,7 @@ struct Workspace {
     uint8_t* Pk = nullptr;         // [rows][pk_ld] mixer packet: u, Delta (fp16), B, C (fp32)
     int pk_ld = 0;                 // packet row bytes (4 di + 8 N)
     __nv_bfloat16* GZb = nullptr;  // [rows][di] SiLU(z), the scan's gate (in_proj epilogue)
-    CUtensorMap tmXo, tmGZo;       // in_proj outputs: x -> XZb as [rows][di], SiLU(z) -> GZb (box {64, 32})
+    CUtensorMap tmGZs, tmUs;       // k_inconv stores: SiLU(z) -> GZb, u -> packet (box {64, 125})
     CUtensorMap tmXb, tmE1b, tmE2b, tmAb, tmGb;        // GEMM A operands (box {64, 128})
     CUtensorMap tmE1o, tmE2o, tmXZo;                   // GEMM bf16 outputs (box {64, 32}, TMA store)
     CUtensorMap tmHf, tmAo;                            // residual stream fp32 (box {32,32}), LN out (box {64,32})
@@ -135,7 +136,7 @@ struct Workspace {
     float* Lat = nullptr;         // [rows][ad_ld] SiLU(V h^KB + c), columns >= a stay zero
     float* pooled_k = nullptr;    // [cap_n][dm]
     float* dh1k = nullptr;        // [cap_n][h1]
-    CUtensorMap tmAbS2;                                // in_proj A half-slices for 2-CTA cluster multicast (box {64, 64})
+    CUtensorMap tmAbS2;                                // k_inconv A half-slices for 2-CTA cluster multicast (box {64, 64})
     CUtensorMap tmX32, tmE1f, tmE2f, tmA32, tmG32;     // fp32 path 3xTF32 A operands (box {32, 128})
     std::vector<void*> allocs;
 };
@@ -194,12 +195,13 @@ struct tcl_model {
     tcl::TrainState* tr = nullptr;  // tcl_train_init   // tcl_topk_score per-task columns
     size_t eval_cols_cap = 0;
     // bf16 tensor-core path (precision == TCL_PREC_BF16_PROJ)
-    int use_tc = 0, num_sms = 148, nxp = 0, rp = 0, bn_in = 0;
+    int use_tc = 0, num_sms = 148, nxp = 0, rp = 0;
     std::vector<void*> bf_allocs;
     __nv_bfloat16 *W1b = nullptr, *W2b = nullptr, *W3b = nullptr;
-    std::vector<__nv_bfloat16*> Winb, Woutb, Wxb, Wdtb;
+    std::vector<__nv_bfloat16*> Winb, Woutb, Wdtb;
+    std::vector<__half*> Wxh;            // x_proj weights in fp16 (k_xdt: fp16 operands, u is fp16)
     CUtensorMap tmW1, tmW2, tmW3;
-    std::vector<CUtensorMap> tmWin, tmWout;
+    std::vector<CUtensorMap> tmWin, tmWout;   // W_in box {64, inconv_channels(di)}; W_out box {64, dm}
     // per-stage instrumentation (tcl_profile_enable)
     int prof_on = 0;
     struct ProfRec { int kind; cudaEvent_t a, b; };

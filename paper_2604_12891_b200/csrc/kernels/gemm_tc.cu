@@ -1,8 +1,10 @@
 // gemm_tc.cu -- the projections of the bf16 path on the 5th-generation tensor cores (tcgen05).
 //
-//   in_proj   [x|z] = LN_l(H) W_in^T
-//   out_proj  H <- H + g W_out^T, then LN_{l+1}(H)   (a8 + a3 of the next layer, fused epilogue)
+//   out_proj  H <- H + g W_out^T, then LN_{l+1}(H)   (a8 + a3 of the next layer, fused epilogue;
+//             the d_model < 128 configurations -- gemm_tc_ln.cu takes d_model 128 / 256)
 //   encoder   SiLU(X W1^T + b1), SiLU(. W2^T + b2), . W3^T + b3 (+ LN_0)   (a2)
+//             (the linears that k_enc12 / gemm_tc_ln do not take)
+// (in_proj runs in k_inconv, inconv.cu, fused with the conv.)
 //
 // Design (B200-first): persistent, warp-specialised, weight-stationary.  Each CTA keeps its
 // [BN x K] slice of the weight matrix resident in shared memory for the whole launch (loaded once
@@ -65,11 +67,10 @@ __device__ __forceinline__ void named_bar(int id, int nthreads) {
 
 // EPI: 0 = bf16 out; 1 = bf16 out of SiLU(acc + bias); 2 = same + MC dropout;
 //      3 = residual/bias into fp32 H, then LayerNorm(H) -> bf16 out (BN == full row)
-template <int BN, int KB, int EPI, int CL = 1>
+template <int BN, int KB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__ CUtensorMap tmA,
                                                          const __grid_constant__ CUtensorMap tmB,
                                                          const __grid_constant__ CUtensorMap tmC,
-                                                         const __grid_constant__ CUtensorMap tmC2,
                                                          const TcGemmParams p) {
     using S = TcSmem<BN, KB, EPI>;
     constexpr int kStages = S::kStages;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     const int m_step = gridDim.x / p.n_tiles;
 
     if (threadIdx.x == 0) {
-        for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], CL); }
+        for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], 1); }
         tc::mbar_init(bfull, 1);
         for (int a = 0; a < 2; ++a) { tc::mbar_init(&tfull[a], 1); tc::mbar_init(&tempty[a], kEpiWarps); }
         tc::fence_mbar_init();
@@ -110,7 +111,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * BN);
     tc::tc_fence_before();
     __syncthreads();
-    if (CL > 1) tc::cluster_sync();  // peers' barriers are initialised before any multicast lands
     tc::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
@@ -129,14 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                 for (int kb = 0; kb < KB; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], kABytes);
-                    if (CL == 1) {
-                        tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
-                    } else {  // this CTA fetches 128/CL rows of the A k-block for the whole cluster
-                        constexpr int SL = kBM / CL;
-                        const int cr = (int)tc::cluster_ctarank();   // this CTA's slice of the k-block
-                        tc::tma_load_2d_mcast(sA + stage * kABytes + cr * SL * 128, &tmA, kb * 64,
-                                              m * kBM + cr * SL, &full[stage], (uint16_t)((1u << CL) - 1));
-                    }
+                    tc::tma_load_2d_hint(sA + stage * kABytes, &tmA, kb * 64, m * kBM, &full[stage], pol);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -166,8 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                         const uint64_t bd = tc::sw128_kmajor_desc(sB_addr + kb * BN * 128 + k * 32);
                         tc::mma_bf16(d, ad, bd, idesc, (kb | k) != 0);
                     }
-                    if (CL == 1) tc::mma_commit(&empty[stage]);
-                    else tc::mma_commit_mcast(&empty[stage], (uint16_t)((1u << CL) - 1));  // free the slot cluster-wide
+                    tc::mma_commit(&empty[stage]);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
                 tc::mma_commit(&tfull[acc]);
@@ -215,14 +207,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                     tc::tmem_ld32(tbase + c * 32, r);
                     tc::tmem_ld_wait();
                     uint32_t pk[16];
-                    const bool gate = EPI == 0 && p.silu_from > 0 && n_tile * BN + c * 32 >= p.silu_from;
 #pragma unroll
                     for (int j = 0; j < 32; j += 4) {
                         float x[4];
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
                             x[e] = __uint_as_float(r[j + e]);
-                            if (EPI == 0 && gate) x[e] = silu_tanh(x[e]);
                             if (EPI >= 1) x[e] = silu_tanh(x[e] + s_bias[c * 32 + j + e]);
                         }
                         if (EPI == 2) {   // one Philox draw for the 4 consecutive units
@@ -258,11 +248,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
                             __syncwarp();
                             if (lane == 0) {
                                 const int col = n_tile * BN + (c - 1) * 32;
-                                const bool second = p.split_col > 0 && col >= p.split_col;
                                 asm volatile(
                                     "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];"
-                                    ::"l"(reinterpret_cast<uint64_t>(second ? &tmC2 : &tmC)),
-                                    "r"(second ? col - p.split_col : col),
+                                    ::"l"(reinterpret_cast<uint64_t>(&tmC)), "r"(col),
                                     "r"(m * kBM + quarter * 32), "r"(tc::smem_u32(stg))
                                     : "memory");
                                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -366,7 +354,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tc(const __grid_constant__
     }
     tc::tc_fence_before();
     __syncthreads();
-    if (CL > 1) tc::cluster_sync();  // no CTA leaves while peers may still multicast / commit into it
     if (warp == 1) {
         tc::tc_fence_after();
         tc::tmem_dealloc(tmem_base, 2 * BN);
@@ -418,52 +405,32 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int KB, int EPI, int CL = 1>
+template <int BN, int KB, int EPI>
 static cudaError_t launch_impl(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                               const CUtensorMap& c2, const TcGemmParams& p, int grid, cudaStream_t s) {
+                               const TcGemmParams& p, int grid, cudaStream_t s) {
     const int smem = TcSmem<BN, KB, EPI>::kBytes;
-    auto kern = k_gemm_tc<BN, KB, EPI, CL>;
+    auto kern = k_gemm_tc<BN, KB, EPI>;
     cudaError_t e = prepare_kernel(kern, smem);
     if (e != cudaSuccess) return e;
-    if (CL == 1) {
-        kern<<<grid, kThreads, smem, s>>>(a, b, c, c2, p);
-    } else {
-        cudaLaunchConfig_t cfg{};
-        cfg.gridDim = dim3(grid);
-        cfg.blockDim = dim3(kThreads);
-        cfg.dynamicSmemBytes = smem;
-        cfg.stream = s;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = CL;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        cudaError_t e = cudaLaunchKernelEx(&cfg, kern, a, b, c, c2, p);
-        if (e != cudaSuccess) return e;
-    }
+    kern<<<grid, kThreads, smem, s>>>(a, b, c, p);
     return cudaGetLastError();
 }
 
 template <int BN, int KB>
 static cudaError_t launch_epi(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                              const CUtensorMap& c2, const TcGemmParams& p, int grid, cudaStream_t s) {
-    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, c2, p, grid, s);
-    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, c2, p, grid, s);
-    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, c2, p, grid, s);
-    if (p.mcast && (p.n_tiles == 4 || p.n_tiles == 2)) return launch_impl<BN, KB, 0, 2>(a, b, c, c2, p, grid, s);
-    return launch_impl<BN, KB, 0>(a, b, c, c2, p, grid, s);
+                              const TcGemmParams& p, int grid, cudaStream_t s) {
+    if (p.epi == TC_EPI_RESID_LN) return launch_impl<BN, KB, 3>(a, b, c, p, grid, s);
+    if (p.drop.enabled) return launch_impl<BN, KB, 2>(a, b, c, p, grid, s);
+    if (p.act_silu) return launch_impl<BN, KB, 1>(a, b, c, p, grid, s);
+    return launch_impl<BN, KB, 0>(a, b, c, p, grid, s);
 }
 
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s, const CUtensorMap* c2) {
-    if (p.split_col > 0 && (!c2 || !TcSmem<128, 1, 0>::kTmaStore || bn < 128)) return cudaErrorInvalidValue;
-    const CUtensorMap& cc2 = c2 ? *c2 : c;
+                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s) {
     // grid: one persistent CTA per SM, a multiple of the number of N tiles
     const int grid = (num_sms / p.n_tiles) * p.n_tiles;
     if (p.epi == TC_EPI_BF16 && p.act_silu == 0 && p.bias) return cudaErrorInvalidValue;  // unsupported combo
-#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, c, cc2, p, grid, s);
+#define TCL_TC_CASE(BN_, KB_) if (bn == BN_ && kb == KB_) return launch_epi<BN_, KB_>(a, b, c, p, grid, s);
     TCL_TC_CASE(256, 1) TCL_TC_CASE(256, 2) TCL_TC_CASE(256, 3) TCL_TC_CASE(256, 4)
     TCL_TC_CASE(128, 1) TCL_TC_CASE(128, 2) TCL_TC_CASE(128, 3) TCL_TC_CASE(128, 4)
     TCL_TC_CASE(64, 1) TCL_TC_CASE(64, 2) TCL_TC_CASE(64, 3) TCL_TC_CASE(64, 4)

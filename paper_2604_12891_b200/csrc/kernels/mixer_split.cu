@@ -1,30 +1,28 @@
-// mixer_split.cu -- the Mamba mixer of the bf16 path as two kernels:
+// mixer_split.cu -- the selection parameters and the selective scan of the bf16 path (SURVEY §8(a)
+// a6, a7); u = SiLU(conv(x)) comes from k_inconv (inconv.cu, fused with in_proj):
 //
-//   k_mixprep  u   = SiLU(b_conv + causal depthwise conv_{d_conv}(x))          (R4)
-//              [dt_r | B | C] = u W_x^T                                         (R7)
+//   k_xdt      [dt_r | B | C] = u W_x^T                                         (R7)
 //              Delta = softplus(dt_r W_dt^T + b_dt)
 //   k_scan     s_t = exp(Delta A) s_{t-1} + (exp(Delta A) - 1)/A * B_t u_t      (Eqs. 4-5 + ZOH; R5)
 //              y_t = C_t . s_t + D u_t ;  g_t = y_t * SiLU(z_t)                 (R6)
 //
-// Why two kernels: the recurrence is bound by the SFU (N MUFU.EX2 per (t, d)) and its own
-// FMA-pipe mix; the conv / x_proj / dt_proj / softplus work, when it shares the SM with the scan
-// (the one-kernel mixer, mixer_fused.cu), costs the scan ~30% of its issue slots (round 1
-// phase split: 2.73 ms scan alone vs 3.86 ms fused at `large`).  Here that work runs in an
-// HBM-bound kernel of its own, and the scan kernel does nothing but the recurrence.
+// Why separate kernels: the recurrence is bound by the SFU (N MUFU.EX2 per (t, d)) and its own
+// FMA-pipe mix; the x_proj / dt_proj / softplus work, when it shared the SM with the scan (round 1's
+// one-kernel mixer), cost the scan ~30% of its issue slots (2.73 ms scan alone vs 3.86 ms fused at
+// `large`).  Here that work runs in an HBM-bound kernel of its own, and the scan kernel does
+// nothing but the recurrence.
 //
-// The two kernels meet in a per-token "mixer packet" written by k_mixprep (one row per packed
-// token, read by the scan as ONE contiguous bulk copy per 16-token chunk):
+// The kernels meet in a per-token "mixer packet" (one row per packed token, read by the scan as ONE
+// contiguous bulk copy per 16-token chunk):
 //     [ u fp16 x DI | Delta fp16 x DI | B, C fp32 x 2N ]                          (4 DI + 8 N bytes)
-// plus the gate SiLU(z) [P][DI] bf16 that the in_proj epilogue writes contiguously (a second bulk
-// copy per chunk; written into the packet rows instead, the strided 128-byte row pieces cost the
-// in_proj 0.08 ms per layer at `large`: 0.735 vs 0.657 ms).  u and Delta are stored in fp16 (10-bit
-// mantissa: 8x finer than bf16; both are bounded: u is a SiLU of a 4-tap conv, Delta a softplus),
-// B and C in fp32.
+// plus the gate SiLU(z) [P][DI] bf16 (a second bulk copy per chunk).  u and Delta are stored in fp16
+// (10-bit mantissa: 8x finer than bf16; both are bounded: u is a SiLU of a 4-tap conv, Delta a
+// softplus), B and C in fp32.
 //
-// Work decomposition (both kernels): persistent CTAs of DI threads, thread d owns channel d; each
-// CTA owns the packed rows of a contiguous candidate range (balanced by rows) and walks them in
-// 16-row chunks that may span candidates (conv window / SSM state reset at candidate starts, from
-// a start-bit array built once per CTA in shared memory).
+// k_scan: persistent CTAs of DI threads, thread d owns channel d; each CTA owns the packed rows of a
+// contiguous candidate range (balanced by rows) and walks them in 16-row chunks that may span
+// candidates (SSM state reset at candidate starts, from a start-bit array built once per CTA in
+// shared memory).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -68,39 +66,30 @@ __device__ __forceinline__ uint32_t chunk_starts(bool bits, const uint32_t* st_w
     return starts;
 }
 
-// ============================================================================ k_mixprep
+// ============================================================================ k_xdt
 // Warp-per-chunk: every warp of the grid takes 16-row chunks of the packed rows (grid-stride over
 // the global chunk index, so no chunk depends on another and no CTA-wide barrier is needed); lane
 // l owns the CPL = DI / 32 consecutive channels [CPL l, CPL l + CPL).  Per chunk:
-//   0. the chunk's 16 rows of x plus the d_conv - 1 rows before it (the conv halo) were copied
+//   0. the chunk's 16 rows of u (fp16, the packet's first columns, written by k_inconv) were copied
 //      into the warp's shared-memory tile by cp.async while the previous chunk was finishing;
-//   1. conv + SiLU (taps that fall before the token's candidate start are dropped by select,
-//      never by multiplication); u goes to the packet as fp16 and replaces x in the tile as bf16
-//      (the x_proj A operand; each lane overwrites only the channels it has just read);
-//   2. x_proj: mma.sync m16n8k16 over K = DI (W_x staged once per CTA in shared memory), fp32
-//      accumulators in registers; B and C go to the packet from the fragments; the dt_r columns
-//      become the dt_proj A fragments in registers (the m16n8 C layout of n-tiles 2k, 2k+1 IS the
-//      m16k16 A layout); the tile is free now and the NEXT chunk's x is requested into it;
-//   3. dt_proj (K = RP) + bias + softplus -> Delta (fp16) to the packet from the fragments.
-// Every row's result is independent of the chunking (fixed tap and k order): batch-invariant.
-template <int DI, int N, int RP, int NXP, int DC>
-struct PrepSmem {
+//   1. x_proj: mma.sync m16n8k16 (fp16 operands: u as k_inconv rounded it, W_x in fp16; fp32
+//      accumulation) over K = DI, W_x staged once per CTA; B and C go to the packet from the
+//      fragments; the dt_r columns become the dt_proj A fragments in registers (the m16n8 C layout
+//      of n-tiles 2k, 2k+1 IS the m16k16 A layout); the tile is free now and the NEXT chunk's u is
+//      requested into it;
+//   2. dt_proj (K = RP, bf16) + bias + softplus -> Delta (fp16) to the packet from the fragments.
+// Every row's result is independent of the chunking (fixed k order): batch-invariant.
+template <int DI, int N, int RP, int NXP>
+struct XdtSmem {
     static constexpr int kWarps = 16;
-    static constexpr int kHalo = DC - 1;
-    static constexpr int kRows = kTC + kHalo;       // tile rows: halo, then the chunk
-    static constexpr int kWxld = DI + 8;            // bf16 row stride of W_x / the tile (+16 B: conflict-free ldmatrix)
-    static constexpr int kWx = 0;                                  // bf16 [NXP][DI + 8]
+    static constexpr int kWxld = DI + 8;            // 16-bit row stride of W_x / the tile (+16 B: conflict-free ldmatrix)
+    static constexpr int kWx = 0;                                  // fp16 [NXP][DI + 8]
     static constexpr int kWdt = kWx + NXP * kWxld * 2;             // bf16 [DI][RP]
     static constexpr int kBdt = kWdt + DI * RP * 2;                // f32  [DI]
-    static constexpr int kTile = (kBdt + DI * 4 + 127) / 128 * 128;   // per warp: bf16 [kRows][DI + 8]
-    static constexpr int kBytes = kTile + kWarps * kRows * kWxld * 2;
+    static constexpr int kTile = (kBdt + DI * 4 + 127) / 128 * 128;   // per warp: fp16 [16][DI + 8]
+    static constexpr int kBytes = kTile + kWarps * kTC * kWxld * 2;
     static_assert(kBytes <= 232448, "exceeds the 227 KB of shared memory per block");
 };
-
-template <int CPL> struct LaneVec;
-template <> struct LaneVec<8> { using T = uint4; };
-template <> struct LaneVec<4> { using T = uint2; };
-template <> struct LaneVec<2> { using T = uint32_t; };
 
 template <int BYTES>
 __device__ __forceinline__ void cp_async(void* dst, const void* src) {
@@ -111,147 +100,66 @@ __device__ __forceinline__ void cp_async(void* dst, const void* src) {
                      : "memory");
 }
 
-template <int DI, int N, int RP, int NXP, int DC>
-__global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
-    using L = PrepSmem<DI, N, RP, NXP, DC>;
+__device__ __forceinline__ void mma_16816_f16(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+template <int DI, int N, int RP, int NXP>
+__global__ void __launch_bounds__(512, 1) k_xdt(XdtArgs a) {
+    using L = XdtSmem<DI, N, RP, NXP>;
     constexpr int CPL = DI / 32;                     // channels per lane
-    constexpr int H = L::kHalo;
-    using V = typename LaneVec<CPL>::T;
     constexpr int NT_X = NXP / 8;                    // x_proj n-tiles
     constexpr int KS_DT = RP / 16;                   // dt_proj k-steps
     extern __shared__ __align__(128) uint8_t msm[];
-    __nv_bfloat16* wx_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kWx);
+    __half* wx_s = reinterpret_cast<__half*>(msm + L::kWx);
     __nv_bfloat16* wdt_s = reinterpret_cast<__nv_bfloat16*>(msm + L::kWdt);
     float* bdt_s = reinterpret_cast<float*>(msm + L::kBdt);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int g = lane >> 2, tq = lane & 3;
-    __nv_bfloat16* tile = reinterpret_cast<__nv_bfloat16*>(msm + L::kTile) + warp * L::kRows * L::kWxld;
+    __half* tile = reinterpret_cast<__half*>(msm + L::kTile) + warp * kTC * L::kWxld;
 
-    // ---- once per CTA: W_x, W_dt, b_dt into shared memory; this lane's conv taps in registers
+    // ---- once per CTA: W_x (fp16), W_dt (bf16), b_dt into shared memory
     for (int idx = threadIdx.x; idx < NXP * DI / 8; idx += blockDim.x) {
         const int r = idx / (DI / 8), c8 = idx - r * (DI / 8);
         *reinterpret_cast<uint4*>(wx_s + r * L::kWxld + c8 * 8) =
-            __ldg(reinterpret_cast<const uint4*>(a.Wx_b + (int64_t)r * DI + c8 * 8));
+            __ldg(reinterpret_cast<const uint4*>(a.Wx_h + (int64_t)r * DI + c8 * 8));
     }
     for (int idx = threadIdx.x; idx < DI * RP / 8; idx += blockDim.x)
         *reinterpret_cast<uint4*>(wdt_s + idx * 8) = __ldg(reinterpret_cast<const uint4*>(a.Wdt_b) + idx);
     for (int idx = threadIdx.x; idx < DI; idx += blockDim.x) bdt_s[idx] = __ldg(a.b_dt + idx);
-    // conv taps / bias of this lane's channel pairs, pre-halved: SiLU(v) = h (1 + tanh h), h = v / 2
-    constexpr int CP = CPL / 2;
-    float2 wc[CP][DC], bc[CP];
-#pragma unroll
-    for (int c = 0; c < CP; ++c) {
-        const int ch = CPL * lane + 2 * c;
-        bc[c] = make_float2(0.5f * __ldg(a.b_conv + ch), 0.5f * __ldg(a.b_conv + ch + 1));
-#pragma unroll
-        for (int k = 0; k < DC; ++k)
-            wc[c][k] = make_float2(0.5f * __ldg(a.w_conv + ch * DC + k), 0.5f * __ldg(a.w_conv + (ch + 1) * DC + k));
-    }
     __syncthreads();
 
     const int64_t P = a.cu[a.n];
     const int64_t n_chunks = (P + kTC - 1) / kTC;
     const int64_t wstep = (int64_t)gridDim.x * L::kWarps;
-    const __nv_bfloat16* __restrict__ X = a.X;
     uint8_t* __restrict__ pk = a.Pk;
-    // x rows [r0 - H, r0 + 16) of chunk ck -> the tile (rows outside [0, P) are not copied: the
-    // halo ones are masked by the candidate positions, the tail ones produce no output)
+    // u rows [16 ck, 16 ck + 16) of the packet -> the tile (rows >= P are not copied: they produce no output)
     auto fetch = [&](int64_t ck) {
         if (ck >= n_chunks) return;
-        const int64_t rb = ck * kTC - H;
 #pragma unroll
-        for (int t = 0; t < L::kRows; ++t) {
-            const int64_t r = rb + t;
-            if (r >= 0 && r < P) cp_async<CPL * 2>(tile + t * L::kWxld + CPL * lane, X + r * DI + CPL * lane);
+        for (int t = 0; t < kTC; ++t) {
+            const int64_t r = ck * kTC + t;
+            if (r < P) cp_async<CPL * 2>(tile + t * L::kWxld + CPL * lane, pk + r * (int64_t)a.pk_ld + 2 * CPL * lane);
         }
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    // candidate of rows ck * 16 - H + lane (lanes 0 .. 18; -1 outside [0, P)): one load per lane,
-    // issued one chunk ahead like the x rows; a row's tap j (1..H) lies inside its candidate iff the
-    // rows back to it carry the same candidate id
-    auto cands = [&](int64_t ck) -> int {
-        const int64_t r = ck * kTC - H + lane;
-        return (ck < n_chunks && lane < L::kRows && r >= 0 && r < P) ? __ldg(a.row_cand + r) : -1;
-    };
     int64_t ck = (int64_t)blockIdx.x * L::kWarps + warp;
     fetch(ck);
-    int rc_next = cands(ck);
     for (; ck < n_chunks; ck += wstep) {
         const int64_t r0 = ck * kTC;
         const int tc = (int)(P - r0 < kTC ? P - r0 : kTC);
-        // tpos (lane t < 16) = number of taps 1..H of row r0 + t inside its candidate
-        int tpos = 0;
-        {
-            const int rc = rc_next;
-            const int self = __shfl_sync(0xffffffffu, rc, (lane + H) & 31);
-#pragma unroll
-            for (int j = 1; j <= H; ++j) {
-                const int prev = __shfl_sync(0xffffffffu, rc, (lane + H - j) & 31);
-                if (tpos == j - 1 && prev == self) tpos = j;
-            }
-        }
         asm volatile("cp.async.wait_group 0;" ::: "memory");
         __syncwarp();
-        // ---- 1. conv + SiLU.  win[j] = x at row t - 1 - j (channel pairs, packed fp32x2 math)
-        float2 win[H][CP];
-#pragma unroll
-        for (int j = 0; j < H; ++j) {
-            const V v = *reinterpret_cast<const V*>(tile + (H - 1 - j) * L::kWxld + CPL * lane);
-            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
-#pragma unroll
-            for (int c = 0; c < CP; ++c) win[j][c] = __bfloat1622float2(e[c]);
-        }
-#pragma unroll
-        for (int t = 0; t < kTC; ++t) {
-            const int tp = __shfl_sync(0xffffffffu, tpos, t);   // warp-uniform: the branches below do not diverge
-            __nv_bfloat16* trow = tile + (H + t) * L::kWxld + CPL * lane;
-            const V v = *reinterpret_cast<const V*>(trow);
-            const __nv_bfloat162* e = reinterpret_cast<const __nv_bfloat162*>(&v);
-            float2 x[CP], h[CP];
-#pragma unroll
-            for (int c = 0; c < CP; ++c) {
-                x[c] = __bfloat1622float2(e[c]);
-                h[c] = __ffma2_rn(wc[c][DC - 1], x[c], bc[c]);
-            }
-            if (tp >= H) {   // every tap inside the candidate (all but its first d_conv - 1 tokens)
-#pragma unroll
-                for (int j = 0; j < H; ++j)
-#pragma unroll
-                    for (int c = 0; c < CP; ++c) h[c] = __ffma2_rn(wc[c][DC - 2 - j], win[j][c], h[c]);
-            } else {         // taps before the candidate start are dropped
-#pragma unroll
-                for (int j = 0; j < H; ++j)
-                    if (tp > j)
-#pragma unroll
-                        for (int c = 0; c < CP; ++c) h[c] = __ffma2_rn(wc[c][DC - 2 - j], win[j][c], h[c]);
-            }
-#pragma unroll
-            for (int j = H - 1; j > 0; --j)
-#pragma unroll
-                for (int c = 0; c < CP; ++c) win[j][c] = win[j - 1][c];
-            V uh, ub;
-            __half2* uh2 = reinterpret_cast<__half2*>(&uh);
-            __nv_bfloat162* ub2 = reinterpret_cast<__nv_bfloat162*>(&ub);
-#pragma unroll
-            for (int c = 0; c < CP; ++c) {
-                win[0][c] = x[c];
-                float2 th;
-                asm("tanh.approx.f32 %0, %1;" : "=f"(th.x) : "f"(h[c].x));
-                asm("tanh.approx.f32 %0, %1;" : "=f"(th.y) : "f"(h[c].y));
-                const float2 u = __ffma2_rn(h[c], th, h[c]);
-                uh2[c] = __float22half2_rn(u);
-                ub2[c] = __float22bfloat162_rn(u);
-            }
-            *reinterpret_cast<V*>(trow) = ub;   // x of this row is no longer needed (read above)
-            if (t < tc) *reinterpret_cast<V*>(pk + (r0 + t) * (int64_t)a.pk_ld + 2 * CPL * lane) = uh;
-        }
-        __syncwarp();
-        // ---- 2. x_proj: acc[nt] = u[16][DI] . W_x[nt*8 .. +8][DI]^T
+        // ---- 1. x_proj: acc[nt] = u[16][DI] . W_x[nt*8 .. +8][DI]^T
         float acc[NT_X][4];
 #pragma unroll
         for (int nt = 0; nt < NT_X; ++nt) acc[nt][0] = acc[nt][1] = acc[nt][2] = acc[nt][3] = 0.0f;
         {
-            const uint32_t a_addr = tc::smem_u32(tile + (H + (lane & 15)) * L::kWxld + 8 * (lane >> 4));
+            const uint32_t a_addr = tc::smem_u32(tile + (lane & 15) * L::kWxld + 8 * (lane >> 4));
             const uint32_t b_addr = tc::smem_u32(wx_s + (lane & 7) * L::kWxld + 8 * (lane >> 3));
 #pragma unroll 2
             for (int k0 = 0; k0 < DI; k0 += 32) {
@@ -262,14 +170,13 @@ __global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
                 for (int nt = 0; nt < NT_X; ++nt) {
                     uint32_t bf[4];
                     ldsm_x4(bf, b_addr + (nt * 8 * L::kWxld + k0) * 2);
-                    mma_16816(acc[nt], af, bf[0], bf[1]);
-                    mma_16816(acc[nt], af2, bf[2], bf[3]);
+                    mma_16816_f16(acc[nt], af, bf[0], bf[1]);
+                    mma_16816_f16(acc[nt], af2, bf[2], bf[3]);
                 }
             }
         }
-        __syncwarp();               // every ldmatrix of the tile is done: request the next chunk's x
+        __syncwarp();               // every ldmatrix of the tile is done: request the next chunk's u
         fetch(ck + wstep);
-        rc_next = cands(ck + wstep);
         // B, C columns [R, R + 2N) to the packet; dt_r columns [0, R) -> dt_proj A fragments
         const bool row_lo = g < tc, row_hi = g + 8 < tc;
         uint8_t* prow_lo = pk + (r0 + g) * (int64_t)a.pk_ld;
@@ -293,7 +200,7 @@ __global__ void __launch_bounds__(512, 1) k_mixprep(MixPrepArgs a) {
                 adt[ks][2 * h + 1] = ok ? pk_bf16(acc[nt][2], acc[nt][3]) : 0u;
             }
         }
-        // ---- 3. dt_proj + bias + softplus -> Delta (fp16) to the packet
+        // ---- 2. dt_proj + bias + softplus -> Delta (fp16) to the packet
 #pragma unroll 4
         for (int j = 0; j < DI / 8; ++j) {
             float c4[4] = {0.f, 0.f, 0.f, 0.f};
@@ -445,10 +352,10 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
 
 // ============================================================================ launchers
 template <int DI, int N, int RP, int NXP>
-static cudaError_t prep_launch(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
-    using L = PrepSmem<DI, N, RP, NXP, 4>;
+static cudaError_t xdt_launch(const XdtArgs& a, int num_sms, cudaStream_t s) {
+    using L = XdtSmem<DI, N, RP, NXP>;
     constexpr int smem = L::kBytes;
-    auto kern = k_mixprep<DI, N, RP, NXP, 4>;
+    auto kern = k_xdt<DI, N, RP, NXP>;
     cudaError_t e = prepare_kernel(kern, smem);
     if (e != cudaSuccess) return e;
     // one CTA of 16 warps per SM; never more CTAs than 16-row chunks need (the chunk count is
@@ -477,13 +384,13 @@ static cudaError_t scan_launch(const ScanBf16Args& a, int num_sms, cudaStream_t 
 }
 
 template <int DI, int N>
-static cudaError_t prep_rp(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
+static cudaError_t xdt_rp(const XdtArgs& a, int num_sms, cudaStream_t s) {
     const int nxp = ((a.R + 2 * N) + 7) / 8 * 8;
     if (a.RP == 16) {
-        if (nxp <= 24) return prep_launch<DI, N, 16, 24>(a, num_sms, s);
-        if (nxp <= 48) return prep_launch<DI, N, 16, 48>(a, num_sms, s);
+        if (nxp <= 24) return xdt_launch<DI, N, 16, 24>(a, num_sms, s);
+        if (nxp <= 48) return xdt_launch<DI, N, 16, 48>(a, num_sms, s);
     } else if (a.RP == 32) {
-        if (nxp <= 64) return prep_launch<DI, N, 32, 64>(a, num_sms, s);
+        if (nxp <= 64) return xdt_launch<DI, N, 32, 64>(a, num_sms, s);
     }
     return cudaErrorInvalidValue;
 }
@@ -492,13 +399,13 @@ static cudaError_t prep_rp(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
 
 int mixer_packet_bytes(int di, int N) { return 4 * di + 8 * N; }
 
-cudaError_t launch_mixprep(const MixPrepArgs& a, int num_sms, cudaStream_t s) {
+cudaError_t launch_xdt(const XdtArgs& a, int num_sms, cudaStream_t s) {
     using namespace mx;
     if (a.n == 0) return cudaSuccess;
-    if (a.d_conv != 4 || a.pk_ld != mixer_packet_bytes(a.DI, a.N)) return cudaErrorInvalidValue;
-    if (a.DI == 256) return a.N == 16 ? prep_rp<256, 16>(a, num_sms, s) : prep_rp<256, 8>(a, num_sms, s);
-    if (a.DI == 128) return a.N == 16 ? prep_rp<128, 16>(a, num_sms, s) : prep_rp<128, 8>(a, num_sms, s);
-    if (a.DI == 64) return a.N == 16 ? prep_rp<64, 16>(a, num_sms, s) : prep_rp<64, 8>(a, num_sms, s);
+    if (a.pk_ld != mixer_packet_bytes(a.DI, a.N)) return cudaErrorInvalidValue;
+    if (a.DI == 256) return a.N == 16 ? xdt_rp<256, 16>(a, num_sms, s) : xdt_rp<256, 8>(a, num_sms, s);
+    if (a.DI == 128) return a.N == 16 ? xdt_rp<128, 16>(a, num_sms, s) : xdt_rp<128, 8>(a, num_sms, s);
+    if (a.DI == 64) return a.N == 16 ? xdt_rp<64, 16>(a, num_sms, s) : xdt_rp<64, 8>(a, num_sms, s);
     return cudaErrorInvalidValue;
 }
 

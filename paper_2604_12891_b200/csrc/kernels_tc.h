@@ -23,12 +23,6 @@ struct TcGemmParams {
     // TC_EPI_RESID_LN: H = (residual ? H : 0) + acc (+ bias); out = bf16(LN(H) * g + b)
     float* H; int ldh; int residual;
     int skip_h_store;            // RESID_LN (gemm_tc_ln): do not write H back (last layer: only LN_f(H) is consumed)
-    int silu_from;               // EPI_BF16 without bias: columns >= silu_from (> 0) leave as SiLU(acc)
-                                 // (in_proj: the mixer's gate SiLU(z) formed in this HBM-bound epilogue)
-    int split_col;               // EPI_BF16 TMA-store path: output columns >= split_col (> 0) go through the
-                                 // second output map (column - split_col): in_proj x -> X, SiLU(z) -> packet
-    int mcast;                   // EPI_BF16, n_tiles in {2, 4}: pairs of CTAs (N tiles 2j, 2j+1) share each
-                                 // A tile via TMA multicast (A map box {64, 64}: each CTA fetches half)
     const float* ln_g; const float* ln_b; float eps;
     DropoutCtx drop; int site; const int32_t* row_cand; const int32_t* cu;
 };
@@ -60,10 +54,8 @@ cudaError_t launch_gemm_tc_ln(const CUtensorMap& a, const CUtensorMap& b, const 
 // A: [rows][K] (box {64, 128}); B: [N][K] weights (box {64, bn}); kb = ceil(K / 64).
 // C: bf16 output map (box {64, 32}, 128B swizzle) used for TMA stores when BN >= 128 and the
 // epilogue writes bf16 (ignored otherwise).
-// c2: second output map (columns >= p.split_col), may equal c when split_col == 0.
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& c,
-                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s,
-                           const CUtensorMap* c2 = nullptr);
+                           const TcGemmParams& p, int bn, int kb, int num_sms, cudaStream_t s);
 
 // ---- fp32 path on the tensor cores: 3xTF32 GEMM (gemm_tf32.cu) -------------------------------
 struct Tf32GemmParams {

@@ -53,7 +53,7 @@ EXPORTS = ["tcl_weights_count", "tcl_model_create", "tcl_model_destroy", "tcl_re
 TCL_OPT_GRAPHS, TCL_OPT_SCAN = 1, 2
 SCAN_MODES = {"auto": 0, "sequential": 1, "chunked": 2}
 PROF_KINDS = ["pack", "encoder", "layernorm", "in_proj", "conv", "x_proj", "dt_proj", "scan", "out_proj",
-              "head", "topk", "mixer", "allgather", "mc", "lateral", "mixprep"]
+              "head", "topk", "mixer", "allgather", "mc", "lateral", "xdt"]
 
 _lib: Optional[ctypes.CDLL] = None
 

@@ -61,7 +61,6 @@ def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
     h_enc = np.concatenate([oracle.forward_one(d, w, f[i], int(l[i]))[1]["h_enc"] for i in range(len(l))], 0)
     rtol = 2e-2 if prec == 1 else 1e-4
     A = m.debug_read("A", P, dm)
-    XZ = m.debug_read("XZ", P, 2 * di)
     G = m.debug_read("G", P, di)
     H = m.debug_read("H", P, dm)
     rep = {}
@@ -75,12 +74,14 @@ def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
         rep["h_enc"] = _close(H, h_enc, rtol, "encoder output")
     else:
         rep["A"] = _close(A, ref["a"], rtol, "LN_0(H_enc)")
-    rep["x"] = _close(XZ[:, :di], ref["x"], rtol, "in_proj x")
     if prec == 1:
-        # bf16 path: the in_proj epilogue stores the mixer's gate SiLU(z) (the scan reads it as is)
+        # bf16 path: the fused in_proj + mixer-prep kernel (inmix.cu) keeps x on chip and stores the
+        # mixer's gate SiLU(z) (the scan reads it as is)
         zr = ref["z"]
-        rep["z"] = _close(XZ[:, di:], zr / (1.0 + np.exp(-zr)), rtol, "in_proj SiLU(z)")
+        rep["z"] = _close(m.debug_read("GZ", P, di), zr / (1.0 + np.exp(-zr)), rtol, "in_proj SiLU(z)")
     else:
+        XZ = m.debug_read("XZ", P, 2 * di)
+        rep["x"] = _close(XZ[:, :di], ref["x"], rtol, "in_proj x")
         rep["z"] = _close(XZ[:, di:], ref["z"], rtol, "in_proj z")
     # the mixer's intermediates: conv + SiLU output u, Delta = softplus(dt_proj), x_proj's B and C
     if prec == 1:   # (the fp32 path's fused mixer keeps them on chip)
