@@ -309,29 +309,32 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
             tc::tc_fence_after();
             if (xt == 0) TR(1);
             const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * NIN;
-            if (xt == 0) bulk_wait_read0();           // the previous u store has read the x tile
-            named_bar(2, 32 * kXWarps);
-            if (xt == 0) TR(2);
-            // ---- x -> the x tile (bf16: the conv's input precision of the unfused path)
+            // ---- x -> registers (bf16: the conv's input precision of the unfused path), the buffer freed,
+            // then -> the x tile once the previous u store has read it (the TMEM loads overlap that read)
+            constexpr int NXC = HB * (XCW / 16);      // 16-column chunks of this thread
+            uint32_t xs[NXC][8];
 #pragma unroll
-            for (int bx = 0; bx < HB; ++bx) {
+            for (int k = 0; k < NXC; ++k) {
+                const int col = (k / (XCW / 16)) * 64 + XCW * cgx + 16 * (k % (XCW / 16));
+                uint32_t v[16];
+                tmem_ld16(tb + col, v);
+                tc::tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < XCW / 16; ++c) {
-                    const int col = bx * 64 + XCW * cgx + 16 * c;
-                    uint32_t v[16];
-                    tmem_ld16(tb + col, v);
-                    tc::tmem_ld_wait();
-                    uint32_t xs[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) xs[q] = pk_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-                    uint8_t* xb = sX + bx * (kBM * 128);
-                    *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8)) = make_uint4(xs[0], xs[1], xs[2], xs[3]);
-                    *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(xs[4], xs[5], xs[6], xs[7]);
-                }
+                for (int q = 0; q < 8; ++q) xs[k][q] = pk_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
             }
             tc::tc_fence_before();           // this warp's x of tile j is read: (with group Z) the buffer is free
             __syncwarp();
             if (lane == 0) tc::mbar_arrive(&aempty[b]);
+            if (xt == 0) bulk_wait_read0();           // the previous u store has read the x tile
+            named_bar(2, 32 * kXWarps);
+            if (xt == 0) TR(2);
+#pragma unroll
+            for (int k = 0; k < NXC; ++k) {
+                const int col = (k / (XCW / 16)) * 64 + XCW * cgx + 16 * (k % (XCW / 16));
+                uint8_t* xb = sX + (col / 64) * (kBM * 128);
+                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8)) = make_uint4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
+                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(xs[k][4], xs[k][5], xs[k][6], xs[k][7]);
+            }
             // candidate starts of rows rw - 3 .. rw + RW - 1 (bit l = row rw - 3 + l)
             const int cp = __shfl_up_sync(0xffffffffu, cc, 1);
             const uint32_t starts = __ballot_sync(0xffffffffu, lane >= 1 && in && cc != cp);
@@ -397,6 +400,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
                     }
                 }
             }
+            if (xt == 0) TR(4);
             tc::fence_proxy_async();
             named_bar(2, 32 * kXWarps);
             if (xt == 0) {   // u rows 3 .. 127 -> the packet's u columns (the box starts at tile row 3)
@@ -404,7 +408,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
                 for (int bx = 0; bx < HB; ++bx) tma_store_2d(&tmU, ch0 + bx * 64, m * kOut, sX + bx * (kBM * 128) + kHalo * 128);
                 bulk_commit();
             }
-            if (xt == 0) TR(4);
             if (xt == 0) TR(5);
         }
         if (xt == 0) bulk_wait0();

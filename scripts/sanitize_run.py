@@ -1,6 +1,7 @@
 """One small invocation of every kernel family, for compute-sanitizer (memcheck / racecheck /
 synccheck / initcheck): fp32 path (tiny: SIMT + 3xTF32 GEMMs, fp32 mixer, both scan modes),
-bf16 path (tiny d_model 64 and large at n = 64: tcgen05 GEMMs with TMA, mixprep, scan, encoder),
+bf16 path (tiny d_model 64, tuning d_model 128 and large at n = 64: tcgen05 GEMMs with TMA, k_inconv
+(2-CTA cluster at large), k_xdt, scan, encoder),
 MC dropout, top-k (radix + bitonic), the multi-GPU key halves, RDU selection, Top-k score, one
 training step.  Graph replay is off so every launch is a plain kernel launch."""
 import sys
@@ -45,6 +46,7 @@ def run(name, prec, n, scan=None):
 run("tiny", 0, 200)
 run("tiny", 0, 200, scan="chunked")
 run("tiny", 1, 200)
+run("tuning", 1, 300)
 run("large", 1, 64)
 m, d, ft, lt = run("paper", 0, 256)
 # RDU selection + Top-k score
