@@ -31,11 +31,11 @@
 // DI = 64 runs with N = 128.
 //
 // Roles (576 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer,
-// warps 2..9 = group Z (SiLU(z) -> staging -> TMA store), warps 10..17 = group X (x -> staging,
-// conv -> u in place -> TMA store).  The groups work independently (own staging tile, own named
-// barrier), so the SFU-heavy SiLU(z) of one tile overlaps the conv of another.  TMEM: two
-// accumulator buffers of [x | z] (2 HC columns), each freed when both groups have drained it: the
-// MMAs of tile j + 1 run while the epilogue works on tile j.
+// warps 2..9 = group Z (the TMEM side: SiLU(z) -> staging -> TMA store, then x -> the x tile),
+// warps 10..17 = group X (conv -> u in place -> TMA store).  The groups hand the x tile back and
+// forth through two mbarriers (x staged / u store has read it), so SiLU(z) and the x staging of
+// tile j + 1 overlap the conv of tile j.  TMEM: two accumulator buffers of [x | z] (2 HC columns)
+// freed once group Z has drained them: the MMAs of tile j + 1 run while the epilogue works on j.
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -129,7 +129,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
     uint64_t* bfull = empty + kStages;
     uint64_t* afull = bfull + 1;     // [2] in_proj accumulators
     uint64_t* aempty = afull + 2;    // [2]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+    uint64_t* xfull = aempty + 2;    // the x tile holds x of the next tile (group Z -> group X)
+    uint64_t* xfree = xfull + 1;     // the u store has read the x tile (group X -> group Z)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xfree + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = SPLIT == 2 ? tc::cluster_ctarank() : 0u;
@@ -143,7 +145,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
     if (threadIdx.x == 0) {
         for (int st = 0; st < kStages; ++st) { tc::mbar_init(&full[st], 1); tc::mbar_init(&empty[st], SPLIT); }
         tc::mbar_init(bfull, 1);
-        for (int a = 0; a < 2; ++a) { tc::mbar_init(&afull[a], 1); tc::mbar_init(&aempty[a], kEpiWarps); }
+        for (int a = 0; a < 2; ++a) { tc::mbar_init(&afull[a], 1); tc::mbar_init(&aempty[a], kZWarps); }
+        tc::mbar_init(xfull, 32 * kZWarps);
+        tc::mbar_init(xfree, 1);
         tc::fence_mbar_init();
     }
     if (warp == 1) tc::tmem_alloc(tmem_slot, 2 * NIN);
@@ -210,8 +214,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
         }
         __syncwarp();
     } else if (warp < 10) {
-        // ---------------- group Z (warps 2..9): SiLU(z) -> staging -> TMA store.  Lane quarter
-        // warp % 4, 32-channel half (warp - 2) / 4 of each 64-channel box; thread = row.
+        // ---------------- group Z (warps 2..9): the TMEM side.  SiLU(z) -> staging -> TMA store, then x ->
+        // the x tile for group X.  Lane quarter warp % 4, 32-channel half (warp - 2) / 4 of each
+        // 64-channel block; thread = row.
         const int zt = threadIdx.x - 64;              // 0 .. 255
         const int quarter = warp & 3;
         const int half = (warp - 2) >> 2;
@@ -241,11 +246,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
                     *reinterpret_cast<uint4*>(sZ + sw_off(r, (col % 64) / 8)) = make_uint4(zs[0], zs[1], zs[2], zs[3]);
                     *reinterpret_cast<uint4*>(sZ + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(zs[4], zs[5], zs[6], zs[7]);
                 }
-                if (bx == HB - 1) {
-                    tc::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) tc::mbar_arrive(&aempty[b]);   // z of tile j is read
-                }
                 tc::fence_proxy_async();
                 named_bar(1, 256);
                 if (zt == 0) {   // SiLU(z) rows 3 .. 127 -> GZ (the box starts at tile row 3: 128-byte aligned,
@@ -254,22 +254,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
                     bulk_commit();
                 }
             }
+            // ---- x -> registers (bf16: the conv's input precision of the unfused path), the TMEM buffer
+            // freed, then -> the x tile once group X's u store of the previous tile has read it
+            uint32_t xs[HC / 32][8];
+#pragma unroll
+            for (int k = 0; k < HC / 32; ++k) {
+                const int col = (k / 2) * 64 + half * 32 + 16 * (k % 2);
+                uint32_t v[16];
+                tmem_ld16(tb - HC + col, v);
+                tc::tmem_ld_wait();
+#pragma unroll
+                for (int q = 0; q < 8; ++q) xs[k][q] = pk_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+            }
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&aempty[b]);   // x and z of tile j are read
+            if (j > 0) tc::mbar_wait(xfree, (j - 1) & 1);
+#pragma unroll
+            for (int k = 0; k < HC / 32; ++k) {
+                const int col = (k / 2) * 64 + half * 32 + 16 * (k % 2);
+                uint8_t* xb = sX + (col / 64) * (kBM * 128);
+                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8)) = make_uint4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
+                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(xs[k][4], xs[k][5], xs[k][6], xs[k][7]);
+            }
+            tc::mbar_arrive(xfull);                        // (release: this thread's x row is in the tile)
         }
         if (zt == 0) bulk_wait0();
     } else {
-        // ---------------- group X (warps 10..25): x -> the x tile; conv + SiLU -> u in place -> TMA store.
-        // TMEM phase: lane quarter warp % 4, 16-channel column group (warp - 10) / 4 of each 64-channel
-        // block; conv: warp = rows [8 xw, 8 xw + 8) (+ the 3 halo rows before them), lane = CPL
+        // ---------------- group X (warps 10..17): conv + SiLU over the x tile group Z staged -> u in place ->
+        // TMA store.  Warp = rows [16 xw, 16 xw + 16) (+ the 3 halo rows before them), lane = CPL
         // consecutive channels.
         constexpr int CPL = HC / 32;                  // conv channels per lane
         constexpr int CP = CPL / 2;                   // channel pairs per lane
         constexpr int RW = kBM / kXWarps;             // conv rows per warp
-        const int xt = threadIdx.x - 64 - 32 * kZWarps;   // 0 .. 511
-        const int xw = warp - 2 - kZWarps;            // 0 .. 15
-        const int quarter = warp & 3;
-        const int cgx = xw >> 2;                      // column group of the TMEM phase
-        constexpr int XCW = 64 / (kXWarps / 4);       // its columns per 64-channel block
-        const int r = quarter * 32 + lane;
+        const int xt = threadIdx.x - 64 - 32 * kZWarps;   // 0 .. 255
+        const int xw = warp - 2 - kZWarps;            // 0 .. 7
         const int64_t P = rows;
         float2 wc[CP][4], bc[CP];                     // taps / bias pre-halved: SiLU(v) = h (1 + tanh h), h = v / 2
 #pragma unroll
@@ -301,40 +320,11 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
         int cc_next = cand_tile(0);
         for (int j = 0; j < n_my; ++j) {
             const int m = unit + j * n_units;
-            const int b = j & 1;
             const int cc = cc_next;
             cc_next = cand_tile(j + 1);
             if (xt == 0) TR(0);
-            tc::mbar_wait(&afull[b], (j >> 1) & 1);
-            tc::tc_fence_after();
-            if (xt == 0) TR(1);
-            const uint32_t tb = tmem_base + ((uint32_t)(quarter * 32) << 16) + b * NIN;
-            // ---- x -> registers (bf16: the conv's input precision of the unfused path), the buffer freed,
-            // then -> the x tile once the previous u store has read it (the TMEM loads overlap that read)
-            constexpr int NXC = HB * (XCW / 16);      // 16-column chunks of this thread
-            uint32_t xs[NXC][8];
-#pragma unroll
-            for (int k = 0; k < NXC; ++k) {
-                const int col = (k / (XCW / 16)) * 64 + XCW * cgx + 16 * (k % (XCW / 16));
-                uint32_t v[16];
-                tmem_ld16(tb + col, v);
-                tc::tmem_ld_wait();
-#pragma unroll
-                for (int q = 0; q < 8; ++q) xs[k][q] = pk_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
-            }
-            tc::tc_fence_before();           // this warp's x of tile j is read: (with group Z) the buffer is free
-            __syncwarp();
-            if (lane == 0) tc::mbar_arrive(&aempty[b]);
-            if (xt == 0) bulk_wait_read0();           // the previous u store has read the x tile
-            named_bar(2, 32 * kXWarps);
+            tc::mbar_wait(xfull, j & 1);              // group Z has staged x of tile j
             if (xt == 0) TR(2);
-#pragma unroll
-            for (int k = 0; k < NXC; ++k) {
-                const int col = (k / (XCW / 16)) * 64 + XCW * cgx + 16 * (k % (XCW / 16));
-                uint8_t* xb = sX + (col / 64) * (kBM * 128);
-                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8)) = make_uint4(xs[k][0], xs[k][1], xs[k][2], xs[k][3]);
-                *reinterpret_cast<uint4*>(xb + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(xs[k][4], xs[k][5], xs[k][6], xs[k][7]);
-            }
             // candidate starts of rows rw - 3 .. rw + RW - 1 (bit l = row rw - 3 + l)
             const int cp = __shfl_up_sync(0xffffffffu, cc, 1);
             const uint32_t starts = __ballot_sync(0xffffffffu, lane >= 1 && in && cc != cp);
@@ -407,6 +397,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
 #pragma unroll
                 for (int bx = 0; bx < HB; ++bx) tma_store_2d(&tmU, ch0 + bx * 64, m * kOut, sX + bx * (kBM * 128) + kHalo * 128);
                 bulk_commit();
+                bulk_wait_read0();                    // the store has read the tile: group Z may refill it
+                tc::mbar_arrive(xfree);
             }
             if (xt == 0) TR(5);
         }
