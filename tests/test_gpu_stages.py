@@ -99,3 +99,61 @@ def test_stage_parity_one_layer(torch_cuda, oracle, name, prec):
     rep["score"] = float(np.abs(scores - ref_scores).max())
     assert np.all(np.abs(scores - ref_scores) <= rtol * np.maximum(1, np.abs(ref_scores)))
     print(name, "prec", prec, {k: f"{v:.2e}" for k, v in rep.items()})
+
+
+def _seam_lens(L, n_tiles=8, stride=125):
+    """Lengths whose candidate starts fall on every row 125 m + d, d in -3..3, for m = 1..n_tiles (the
+    row-tile seams of k_inconv: tile m covers rows [125 m - 3, 125 m + 125), its first 3 rows being the
+    conv halo) and around its 16-row conv groups, with filler candidates of length <= L in between:
+    lengths 1, 2, 3 at the seams, and candidates that start in one tile's halo and end in the next."""
+    starts = {0}
+    for m in range(1, n_tiles + 1):
+        starts.update(stride * m + d for d in range(-3, 4))
+    # ... and around the 16-row conv groups inside the tiles (a group's 3 halo rows are the rows
+    # before it): tile-local rows 16 k + d, d in -2..1, in every other tile
+    for m in range(0, n_tiles + 1, 2):
+        for k in range(1, 8):
+            starts.update(stride * m - 3 + 16 * k + d for d in range(-2, 2))
+    end = stride * (n_tiles + 1)
+    pos = sorted(starts)
+    full = [pos[0]]
+    for a in pos[1:] + [end]:
+        while a - full[-1] > L:
+            full.append(full[-1] + min(L, 37))   # fillers (37: not a divisor of the stride)
+        full.append(a)
+    return np.diff(np.array(full)).astype(np.int32)
+
+
+@pytest.mark.parametrize("name", ["large", "paper", "tiny"])
+def test_inconv_tile_seams_bf16(torch_cuda, oracle, name):
+    """k_inconv's conv halo at the row-tile seams: u, Delta, B, C and SiLU(z) of every row of a
+    1-layer bf16 model against the oracle's stage dumps, with candidate starts placed on each of the
+    7 rows around every seam (d_inner 256: 2-CTA cluster; 128; 64)."""
+    from paper_2604_12891_b200 import Model
+    c = inputs.config(name)
+    d = c["dims"].replace(n_layer=1, precision=1)
+    w = inputs.make_weights(d, c["seed"])
+    lens = _seam_lens(d.max_len)
+    n = len(lens)
+    f, _ = inputs.make_features(d, n, c["seed"] + 5, workload="large")
+    m = Model(w, d)
+    ft, lt = torch_cuda.from_numpy(f).cuda(), torch_cuda.from_numpy(lens).cuda()
+    s = torch_cuda.empty(n, dtype=torch_cuda.float32, device="cuda")
+    m.tcl_score(ft, lt, s)
+    m.tcl_sync_error()
+    P = int(lens.sum())
+    di = d.d_inner
+    ref = {k: [] for k in ("u", "delta", "B", "C", "z")}
+    for i in range(n):
+        _, st = oracle.forward_one(d, w, f[i], int(lens[i]))
+        for k in ref:
+            ref[k].append(st[f"layer0.{k}"])
+    ref = {k: np.concatenate(v, 0) for k, v in ref.items()}
+    rtol = 2e-2
+    _close(m.debug_read("U", P, di), ref["u"], rtol, "conv + SiLU u")
+    _close(m.debug_read("DELTA", P, di), ref["delta"], rtol, "Delta")
+    BC = m.debug_read("BC", P, 2 * d.d_state)
+    _close(BC[:, :d.d_state], ref["B"], rtol, "B")
+    _close(BC[:, d.d_state:], ref["C"], rtol, "C")
+    zr = ref["z"]
+    _close(m.debug_read("GZ", P, di), zr / (1.0 + np.exp(-zr)), rtol, "SiLU(z)")
