@@ -375,9 +375,19 @@ def run_ours(args, cfg, d, n, k, world, rank, local_rank):
     if not os.path.exists(tp):
         tp = os.path.join(ROOT, "profiles", "round1_traffic.json")
     if os.path.exists(tp):
-        tj = json.load(open(tp)).get(dom)
+        tall = json.load(open(tp))
+        tj = tall.get(dom)
         if tj and args.config == "large":
             traffic = tj["dram_bytes_read"] + tj["dram_bytes_write"]
+        # per-stage pipe utilisation of the same ncu captures (tensor pipe of the projections, XU of the
+        # scan): ncu-sourced, at this configuration only
+        if args.config == "large" and d.precision == inputs.PREC_BF16_PROJ:
+            for kind, entry in kernels.items():
+                tk = tall.get(kind)
+                if tk and "tensor_pipe_pct" in tk:
+                    entry["ncu"] = {"tensor_pipe_pct": tk["tensor_pipe_pct"], "xu_pipe_pct": tk.get("xu_pipe_pct"),
+                                    "dram_bytes_per_launch": tk["dram_bytes_read"] + tk["dram_bytes_write"],
+                                    "source": tk.get("source")}
     if "exps" in wk:
         roof = {"bound": "alu", "achieved": de["ex2_per_s"] / 1e12, "peak": mb["ex2"] / 1e12,
                 "unit": "Tex2/s", "frac": de["sfu_frac"],

@@ -9,7 +9,7 @@ bash scripts/configs_gpu.sh
 echo -n "== long 131072 :: "; timeout 900 python bench.py --config long --steps 5 --warmup 3 --no-cpu-baseline 2>/dev/null > gpurun_out/bench_long.json; python -c "import json; d=json.load(open('gpurun_out/bench_long.json')); print(round(d['value']), round(d['ms_per_step'],3), round(d['e2e']['value']))"
 timeout 1500 python scripts/measure_configs.py --full-large 2>&1 | tail -8
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r2.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-for k in k_scan k_mixprep k_gemm_tc k_gemm_ln; do
+for k in k_scan k_inconv k_xdt k_gemm_ln; do
   ncu --set full --import-source on --clock-control none -k regex:$k -s 4 -c 1 -o gpurun_out/prof_r2_$k python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 done
 for k in k_enc12 k_topk_radix k_pack k_pool_bf16; do

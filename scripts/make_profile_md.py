@@ -38,7 +38,7 @@ def main():
     parts.append(run("launches", os.path.join(OUT, f"launches_{prefix}.csv")))
     parts.append("## Per-kernel full captures\n")
     reps = sorted(f for f in os.listdir(OUT) if f.startswith(f"prof_{prefix}_") and f.endswith(".ncu-rep"))
-    order = ["k_scan", "k_mixprep", "k_mixer_fused", "k_gemm_tc", "k_gemm_ln", "k_enc12", "k_gemm_tf32", "k_head",
+    order = ["k_scan", "k_inconv", "k_xdt", "k_gemm_ln", "k_enc12", "k_gemm_tc", "k_gemm_tf32", "k_head",
              "k_gemm_simt", "k_topk_radix", "k_pool_bf16", "k_pack"]
     reps.sort(key=lambda f: next((i for i, k in enumerate(order) if k in f), 99))
     for f in reps:
@@ -46,13 +46,12 @@ def main():
     open(os.path.join(ROOT, "profiles", name + ".md"), "w").write("\n".join(parts))
     # traffic per launch of the dominant kernels
     traffic = {}
-    for key, rep in (("scan", "k_scan"), ("mixprep", "k_mixprep"), ("mixer", "k_mixer_fused"), ("in_proj", "k_gemm_tc"),
-                     ("out_proj", "k_gemm_ln"), ("encoder", "k_enc12")):
+    for key, rep in (("scan", "k_scan"), ("in_proj", "k_inconv"), ("xdt", "k_xdt"), ("out_proj", "k_gemm_ln"),
+                     ("encoder", "k_enc12")):
         p = os.path.join(OUT, f"prof_{prefix}_{rep}.ncu-rep")
         if not os.path.exists(p):
             continue
-        csv = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv", "--metrics",
-                              "dram__bytes_read.sum,dram__bytes_write.sum"], capture_output=True, text=True).stdout
+        csv = subprocess.run(["ncu", "-i", p, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
         lines = [l for l in csv.splitlines() if l.startswith('"')]
         hdr = [h.strip('"') for h in lines[0].split('","')]
         units = [h.strip('"') for h in lines[1].split('","')]
@@ -60,10 +59,15 @@ def main():
         mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
 
         def val(m):
-            i = hdr.index(m)
+            # exact metric name, else the (section-prefixed) column that ends with it
+            i = hdr.index(m) if m in hdr else next(k for k, h in enumerate(hdr) if h.endswith(m))
             return float(row[i].replace(",", "")) * mult.get(units[i], 1)
         traffic[key] = {"kernel": row[hdr.index("Kernel Name")][:60], "dram_bytes_read": val("dram__bytes_read.sum"),
                         "dram_bytes_write": val("dram__bytes_write.sum"),
+                        # tcgen05 / mma.sync activity: the realtime tensor-pipe counter (the plain
+                        # sm__pipe_tensor_cycles_active mirrors the XU issue counter on this part)
+                        "tensor_pipe_pct": val("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed"),
+                        "xu_pipe_pct": val("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active"),
                         "source": f"profiles/{name}.md (prof_{prefix}_{rep}.ncu-rep)"}
     if traffic:
         json.dump(traffic, open(os.path.join(ROOT, "profiles", tname + ".json"), "w"), indent=1)
