@@ -233,18 +233,22 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
             for (int bx = 0; bx < HB; ++bx) {
                 if (zt == 0) bulk_wait_read0();       // the previous SiLU(z) box store has read the staging tile
                 named_bar(1, 256);
-#pragma unroll
-                for (int c = 0; c < 2; ++c) {
-                    const int col = bx * 64 + half * 32 + 16 * c;
-                    uint32_t v[16];
-                    tmem_ld16(tb + col, v);
+                {
+                    const int col = bx * 64 + half * 32;    // 32 columns: one TMEM load, one wait
+                    uint32_t v[32];
+                    tc::tmem_ld32(tb + col, v);
                     tc::tmem_ld_wait();
-                    uint32_t zs[8];
 #pragma unroll
-                    for (int q = 0; q < 8; ++q)
-                        zs[q] = pk_bf16(silu_tanh(__uint_as_float(v[2 * q])), silu_tanh(__uint_as_float(v[2 * q + 1])));
-                    *reinterpret_cast<uint4*>(sZ + sw_off(r, (col % 64) / 8)) = make_uint4(zs[0], zs[1], zs[2], zs[3]);
-                    *reinterpret_cast<uint4*>(sZ + sw_off(r, (col % 64) / 8 + 1)) = make_uint4(zs[4], zs[5], zs[6], zs[7]);
+                    for (int c = 0; c < 2; ++c) {
+                        uint32_t zs[8];
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            zs[q] = pk_bf16(silu_tanh(__uint_as_float(v[16 * c + 2 * q])),
+                                            silu_tanh(__uint_as_float(v[16 * c + 2 * q + 1])));
+                        const int ck = (col % 64) / 8 + 2 * c;
+                        *reinterpret_cast<uint4*>(sZ + sw_off(r, ck)) = make_uint4(zs[0], zs[1], zs[2], zs[3]);
+                        *reinterpret_cast<uint4*>(sZ + sw_off(r, ck + 1)) = make_uint4(zs[4], zs[5], zs[6], zs[7]);
+                    }
                 }
                 tc::fence_proxy_async();
                 named_bar(1, 256);
@@ -258,13 +262,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_inconv(const __grid_constant__ 
             // freed, then -> the x tile once group X's u store of the previous tile has read it
             uint32_t xs[HC / 32][8];
 #pragma unroll
-            for (int k = 0; k < HC / 32; ++k) {
-                const int col = (k / 2) * 64 + half * 32 + 16 * (k % 2);
-                uint32_t v[16];
-                tmem_ld16(tb - HC + col, v);
+            for (int bx = 0; bx < HB; ++bx) {
+                uint32_t v[32];
+                tc::tmem_ld32(tb - HC + bx * 64 + half * 32, v);   // 32 columns: one TMEM load, one wait
                 tc::tmem_ld_wait();
 #pragma unroll
-                for (int q = 0; q < 8; ++q) xs[k][q] = pk_bf16(__uint_as_float(v[2 * q]), __uint_as_float(v[2 * q + 1]));
+                for (int c = 0; c < 2; ++c)
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        xs[2 * bx + c][q] = pk_bf16(__uint_as_float(v[16 * c + 2 * q]), __uint_as_float(v[16 * c + 2 * q + 1]));
             }
             tc::tc_fence_before();
             __syncwarp();
