@@ -525,3 +525,30 @@ def test_chunked_scan_parity_and_invariance(torch_cuda, oracle, name, disc):
     m2.scan_mode("chunked")
     assert np.array_equal(_gpu_score(torch_cuda, m2, f[300:650], l[300:650]), got[300:650])
     print(f"{name} disc={disc} chunked: max|err|={err:.3e} vs sequential {np.abs(got - s_seq).max():.2e}")
+
+
+# Non-default dimensions: the templated kernels' other instantiations (d_inner != d_model through
+# expand 2, d_state 8, other dt_ranks), on both precision paths.  Each case runs the full model
+# against the oracle; the bf16 path also checks the ranking (reading R18).
+@pytest.mark.parametrize("base,over", [
+    ("tuning", dict(expand=2)),                  # d_model 128 -> d_inner 256 (N 8): k_inconv 2-CTA split, K = 128
+    ("tiny", dict(expand=2)),                    # d_model 64 -> d_inner 128 (N 16)
+    ("large", dict(n_layer=1, d_state=8)),       # d_inner 256 with N 8: 8-float B / C, k_xdt's NXP 32
+    ("large", dict(n_layer=2, dt_rank=8)),       # dt_r narrower than ceil(d_model / 16)
+    ("tuning", dict(d_state=16, dt_rank=4)),     # d_model 128 with N 16 and dt_rank 4
+])
+@pytest.mark.parametrize("prec", [inputs.PREC_FP32, inputs.PREC_BF16_PROJ])
+def test_score_parity_other_dims(torch_cuda, oracle, base, over, prec):
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup(base, n=400, dims_over=dict(over, precision=prec), workload="large")
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    ref = oracle.score(d, w, f, l)
+    err = _check_scores(got, ref, d.precision)
+    msg = f"{base} {over} prec {prec}: max|err|={err:.3e} std={ref.std():.3e}"
+    if prec == inputs.PREC_BF16_PROJ:
+        from scipy.stats import spearmanr
+        rho = spearmanr(got, ref).correlation
+        assert rho >= 0.999, f"spearman {rho:.5f}"
+        msg += f" spearman={rho:.6f}"
+    print(msg)
