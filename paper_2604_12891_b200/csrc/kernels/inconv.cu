@@ -1,7 +1,7 @@
 // inconv.cu -- in_proj + SiLU(z) + causal depthwise conv + SiLU of the bf16 path in ONE tcgen05
 // kernel (PAPER.md:446 in_proj, P:570 conv; readings R4, R25):
 //
-//   [x | z] = LN_l(H) W_in^T                      (transposed: x^T = W_x-slice . A^T, M = channels)
+//   [x | z] = LN_l(H) W_in^T                      (tcgen05: M = 128 rows, N = 2 HC channels)
 //   GZ = SiLU(z)                                  -> [P][DI] bf16, the scan's gate
 //   u  = SiLU(b_conv + causal conv_4(x))          -> the mixer packet's u columns (fp16)
 //
@@ -9,13 +9,12 @@
 // HBM (1 KB per token and layer at `large`).  k_xdt (mixer_split.cu) then turns u into dt_r, B, C
 // and Delta.
 //
-// Layout: the MMA is row-oriented (M = 128 rows, N = 2 HC channels: [x | z]).  The epilogue drains
-// SiLU(z) and x from TMEM (thread = row, 16-byte shared stores) into two 128B-swizzled staging tiles
-// [rows][channels]; the conv then walks the x tile with lane = HC/32 consecutive channels and warp =
-// one row at a time (8-byte shared loads / stores, conflict-free), writes u in place, and TMA stores
-// move SiLU(z) and u to HBM.  Every memory instruction is 8-16 bytes wide per lane (2-byte
-// per-lane stores, global or shared, were the bound of the transposed variants: ~2.7-6.6 cycles per
-// warp instruction).
+// Layout: the epilogue drains SiLU(z) and x from TMEM (thread = row, 16-byte shared stores) into
+// 128B-swizzled staging tiles [rows][channels]; the conv then walks the x tile with lane = HC/32
+// consecutive channels and warp = one row at a time (8-byte shared loads / stores, conflict-free),
+// writes u in place, and TMA stores move SiLU(z) and u to HBM.  Every memory instruction is 8-16
+// bytes wide per lane (2-byte per-lane stores, global or shared, were the bound of the transposed
+// variants -- in_proj as W . A^T with TMEM lane = channel -- at ~2.7-6.6 cycles per warp instruction).
 //
 // Tiles overlap: tile m covers the packed rows [125 m - 3, 125 m + 125); its first d_conv - 1 = 3
 // rows are the conv halo of row 125 m (recomputed by the MMA, never stored), so a tile needs
@@ -26,9 +25,7 @@
 // DI = 256: the 512 x 256 bf16 in_proj weight does not fit one SM, so CTA h of a 2-CTA cluster owns
 // channels [128 h, 128 h + 128) of x and of z (a 256-row, 128 KB weight slice, resident); both
 // CTAs take the same row tiles and share each A tile by TMA multicast (each fetches 64 rows).
-// DI <= 128: one CTA owns all channels.
-//
-// DI = 64 runs with N = 128.
+// DI <= 128: one CTA owns all channels (DI = 64 runs with N = 128).
 //
 // Roles (576 threads): warp 0 = TMA producer, warp 1 = TMEM allocator + single-thread MMA issuer,
 // warps 2..9 = group Z (the TMEM side: SiLU(z) -> staging -> TMA store, then x -> the x tile),
