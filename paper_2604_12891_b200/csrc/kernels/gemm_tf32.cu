@@ -21,7 +21,8 @@
 //                element-wise split keeps the swizzled layout, so no address math is needed
 //   warps 6..13  epilogue: warp w drains TMEM lanes 32 (w % 4).., column half (w - 6) / 4
 // fp32 accumulators double-buffered in TMEM (2 x BN columns): the epilogue of tile i overlaps the
-// MMAs of tile i+1.  Epilogues (fp32 outputs, one row per thread, 128-bit stores):
+// MMAs of tile i+1.  Epilogues (fp32 outputs; thread = row for the arithmetic, global rows read and
+// written coalesced through a per-warp staging tile, EpiStage):
 //   0  Y = acc                                   (in_proj)
 //   1  Y = SiLU(acc + b) [inverted dropout]      (encoder linears 1, 2; MC sites 0, 1, R17)
 //   3  H = [H +] acc + b, then A = LN(H) if out   (out_proj + residual (+ next LN); encoder linear 3)
@@ -44,11 +45,13 @@ template <int BN, int KB>
 struct Smem {
     static constexpr int kBBytes = KB * BN * 128;                    // one weight matrix (hi or lo)
     static constexpr int kStageBytes = 2 * kKBBytes;                 // A_hi + A_lo of one K-block
-    static constexpr int kStagesRaw = (220 * 1024 - 2 * kBBytes) / kStageBytes;
+    static constexpr int kStgBytes = kEpiWarps * 32 * 16 * 4;         // epilogue staging [warp][32 rows][16 fp32]
+    static constexpr int kStagesRaw = (220 * 1024 - kStgBytes - 2 * kBBytes) / kStageBytes;
     static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
     static constexpr int kOffB = 0;                                  // W_hi, then W_lo
     static constexpr int kOffA = 2 * kBBytes;                        // stage s: A_hi at s*2K, A_lo at s*2K + K
-    static constexpr int kOffPar = kOffA + kStages * kStageBytes;    // bias, ln_g, ln_b  [3][BN] fp32
+    static constexpr int kOffStg = kOffA + kStages * kStageBytes;
+    static constexpr int kOffPar = kOffStg + kStgBytes;              // bias, ln_g, ln_b  [3][BN] fp32
     static constexpr int kOffRed = kOffPar + 3 * BN * 4;             // LN partials [2][128] float2
     static constexpr int kOffBar = kOffRed + 2 * 128 * 8;
     static constexpr int kBytes = kOffBar + 512 + 1024;
@@ -85,6 +88,48 @@ __device__ __noinline__ u32x4 drop_words_tf(const DropoutCtx& d, int unit4, int 
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
+
+// Epilogue staging of one warp: 32 rows x 16 fp32 (2 KB), 16-byte group g of row r stored at group
+// g ^ ((r >> 1) & 3).  The TMEM layout gives thread = row; global rows are written and read
+// coalesced through this tile instead (lane -> row 8 i + lane / 4, group lane % 4: one 128-bit
+// access covers 8 rows x 64 contiguous bytes, against 32 rows x 16 bytes per thread-row access).
+// Both access patterns are bank-conflict-free (each 8-lane phase covers all 32 banks).
+struct EpiStage {
+    float* t;
+    int lane;
+    __device__ __forceinline__ float4* at(int r, int g) const { return reinterpret_cast<float4*>(t + r * 16 + 4 * (g ^ ((r >> 1) & 3))); }
+    // thread = row: write / read its 16 values
+    __device__ __forceinline__ void put_row(const float* x) const {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) *at(lane, g) = make_float4(x[4 * g], x[4 * g + 1], x[4 * g + 2], x[4 * g + 3]);
+    }
+    __device__ __forceinline__ void get_row(float* x) const {
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const float4 v = *at(lane, g);
+            x[4 * g] = v.x; x[4 * g + 1] = v.y; x[4 * g + 2] = v.z; x[4 * g + 3] = v.w;
+        }
+    }
+    // coalesced: rows [0, 32) of the warp at base (row stride ld floats), rows >= nvalid skipped
+    __device__ __forceinline__ void load_global(float4 (&v)[4], const float* base, int64_t ld, int nvalid) const {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = 8 * i + (lane >> 2);
+            v[i] = r < nvalid ? *reinterpret_cast<const float4*>(base + r * ld + 4 * (lane & 3)) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    __device__ __forceinline__ void put_global(const float4 (&v)[4]) const {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) *at(8 * i + (lane >> 2), lane & 3) = v[i];
+    }
+    __device__ __forceinline__ void store_global(float* base, int64_t ld, int nvalid) const {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int r = 8 * i + (lane >> 2);
+            if (r < nvalid) *reinterpret_cast<float4*>(base + r * ld + 4 * (lane & 3)) = *at(r, lane & 3);
+        }
+    }
+};
 
 template <int BN, int KB, int EPI>
 __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant__ CUtensorMap tmA,
@@ -229,18 +274,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
         const int quarter = warp & 3;
         const int half = (warp - kEpi0) >> 2;
         const int rloc = quarter * 32 + lane;
+        const EpiStage st{reinterpret_cast<float*>(smem + S::kOffStg) + (warp - kEpi0) * 32 * 16, lane};
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int m = m_first; m < num_m; m += m_step) {
             const int row = m * kBM + rloc;
-            const bool valid = row < rows;
+            const int row0 = m * kBM + quarter * 32;          // the warp's first row
+            const int nvalid = rows - row0;                    // rows of the warp inside [0, rows)
             tc::mbar_wait(&tfull[acc], acc_phase);
             tc::tc_fence_after();
             const uint32_t tbase = tmem_base + ((uint32_t)(quarter * 32) << 16) + acc * BN;
             if constexpr (EPI != 3) {
                 int cand = 0, token = 0;
-                if (EPI == 1 && p.drop.enabled && valid) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
-                float* orow = p.Y + (int64_t)row * p.ldy + n_tile * BN;
+                if (EPI == 1 && p.drop.enabled && row < rows) { cand = p.row_cand[row]; token = row - p.cu[cand]; }
+                float* obase = p.Y + (int64_t)row0 * p.ldy + n_tile * BN;
 #pragma unroll 1
                 for (int c = half; c < NCH; c += 2) {
                     uint32_t r[32];
@@ -262,44 +309,51 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
                             x[j + 3] = dropout_apply_word(p.drop, x[j + 3], wd.w);
                         }
                     }
-                    if (valid) {
-                        float4* dst = reinterpret_cast<float4*>(orow + c * 32);
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) dst[q] = make_float4(x[4 * q], x[4 * q + 1], x[4 * q + 2], x[4 * q + 3]);
+                    for (int h = 0; h < 2; ++h) {
+                        st.put_row(x + 16 * h);
+                        __syncwarp();
+                        st.store_global(obase + c * 32 + 16 * h, p.ldy, nvalid);
+                        __syncwarp();
                     }
                 }
             } else {
-                // pass 1: v = [H +] acc + b; store H; keep v in TMEM; partial row sum
-                float* hrow = p.H + (int64_t)row * p.ldh + n_tile * BN;   // this CTA's columns
+                // pass 1: v = [H +] acc + b; store H; keep v in TMEM; partial row sum.  The residual
+                // rows arrive coalesced (issued before the TMEM load) and are transposed through
+                // the staging tile.
+                float* hbase = p.H + (int64_t)row0 * p.ldh + n_tile * BN;   // this CTA's columns
                 float sum = 0.f;
 #pragma unroll 1
                 for (int c = half; c < NCH; c += 2) {
+                    float4 hg[4];
+                    if (p.residual) st.load_global(hg, hbase + c * 32, p.ldh, nvalid);
                     uint32_t r[32];
                     tc::tmem_ld32(tbase + c * 32, r);
-                    float hv[32];
-                    if (p.residual && valid) {
-                        const float4* h4 = reinterpret_cast<const float4*>(hrow + c * 32);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q) {
-                            const float4 o = h4[q];
-                            hv[4 * q] = o.x; hv[4 * q + 1] = o.y; hv[4 * q + 2] = o.z; hv[4 * q + 3] = o.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int q = 0; q < 32; ++q) hv[q] = 0.0f;
-                    }
                     tc::tmem_ld_wait();
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const float v = hv[j] + (__uint_as_float(r[j]) + s_bias[c * 32 + j]);
-                        hv[j] = v;
-                        sum += v;
-                        r[j] = __float_as_uint(v);
-                    }
-                    if (valid) {
-                        float4* o4 = reinterpret_cast<float4*>(hrow + c * 32);
+                    for (int h = 0; h < 2; ++h) {
+                        float hv[16];
+                        if (p.residual) {
+                            st.put_global(hg);
+                            __syncwarp();
+                            if (h == 0) st.load_global(hg, hbase + c * 32 + 16, p.ldh, nvalid);   // next half in flight
+                            st.get_row(hv);
+                        } else {
 #pragma unroll
-                        for (int q = 0; q < 8; ++q) o4[q] = make_float4(hv[4 * q], hv[4 * q + 1], hv[4 * q + 2], hv[4 * q + 3]);
+                            for (int q = 0; q < 16; ++q) hv[q] = 0.0f;
+                        }
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const int jj = 16 * h + j;
+                            const float v = hv[j] + (__uint_as_float(r[jj]) + s_bias[c * 32 + jj]);
+                            hv[j] = v;
+                            sum += v;
+                            r[jj] = __float_as_uint(v);
+                        }
+                        st.put_row(hv);   // own row only: no hazard with this thread's get_row above
+                        __syncwarp();
+                        st.store_global(hbase + c * 32 + 16 * h, p.ldh, nvalid);
+                        __syncwarp();
                     }
                     if (p.out) tc::tmem_st32(tbase + c * 32, r);
                 }
@@ -323,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
                     s_red[half * 128 + rloc].y = sq;
                     named_bar(1 + quarter, 64);
                     const float rstd = rsqrtf((s_red[rloc].y + s_red[128 + rloc].y) * (1.0f / BN) + p.eps);
-                    float* arow = p.out + (int64_t)row * p.ldo;
+                    float* abase = p.out + (int64_t)row0 * p.ldo;
 #pragma unroll 1
                     for (int c = half; c < NCH; c += 2) {
                         uint32_t r[32];
@@ -333,10 +387,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             a[j] = (__uint_as_float(r[j]) - mean) * rstd * s_g[c * 32 + j] + s_b[c * 32 + j];
-                        if (valid) {
-                            float4* dst = reinterpret_cast<float4*>(arow + c * 32);
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) dst[q] = make_float4(a[4 * q], a[4 * q + 1], a[4 * q + 2], a[4 * q + 3]);
+                        for (int h = 0; h < 2; ++h) {
+                            st.put_row(a + 16 * h);
+                            __syncwarp();
+                            st.store_global(abase + c * 32 + 16 * h, p.ldo, nvalid);
+                            __syncwarp();
                         }
                     }
                     named_bar(1 + quarter, 64);  // s_red reuse guard for the next tile
