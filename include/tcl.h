@@ -108,7 +108,8 @@ tcl_status tcl_model_create(const float* weights_host, size_t n_floats, const tc
 tcl_status tcl_model_destroy(tcl_model* model);
 
 /* Optional pre-allocation of the workspace for batches of up to n_max candidates (no allocation
- * happens in later calls with n <= n_max).  mc_passes_max is accepted for API symmetry. */
+ * happens in later calls with n <= n_max, or, for tcl_score_mc, n <= n_max and n_passes <=
+ * mc_passes_max: the MC passes run batched, n_passes x n virtual candidates per forward). */
 tcl_status tcl_reserve(tcl_model* model, int64_t n_max, int32_t mc_passes_max);
 
 /* Score n candidates.

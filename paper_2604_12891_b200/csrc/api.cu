@@ -291,6 +291,7 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     TAKE(dh1, chunk_n * d.dec_dims[0]);
     TAKE(dh2, chunk_n * d.dec_dims[1]);
     TAKE(dsc, chunk_n);
+    TAKE(lens_mc, chunk_n);
     if (m->kb) {
         TAKE(Hk, rows * dm);
         TAKE(E1k, rows * d.enc_dims[0]);
@@ -364,9 +365,10 @@ static tcl_status ensure_topk_tmp(tcl_model* m, int64_t n, int k) {
 }
 
 // ------------------------------------------------------------------------------ head
-// LN_f + masked mean (warp per candidate), then the decoder MLP as three small
-// fp32 GEMMs over the candidates (weights stream through shared memory once per 64 candidates);
-// MC passes fold each pass' score into (mean, M2) with Welford's update.
+// LN_f + masked mean (warp per candidate), then the decoder MLP (head.cu: one
+// launch below 8,192 candidates; above, the pool kernel and three small fp32 GEMMs over the
+// candidates); MC passes fold each pass' score into (mean, M2) with Welford's update (batched MC
+// passes: the scores of all passes, then one reduction, launch_mc_reduce).
 static void run_head(tcl_model* m, const int32_t* lens, int64_t n, float* scores, const DropoutCtx& drop,
                      float* mc_mean, cudaStream_t s, bool lnf_in_ab = false) {
     const tcl_dims& d = m->dims;
@@ -540,7 +542,8 @@ struct F32Run {
 // to that site and enters the AC's GEMM as a second K segment against diag(alpha) U (the lateral
 // sum joins the same accumulators, before bias and activation).  MC dropout: AC column only.
 static void forward_chunk_kbac(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
-                               float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+                               float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s,
+                               int64_t n_src = 0) {
     const tcl_dims& d = m->dims;
     Workspace& w = m->ws;
     const tcl_model* kb = m->kb;
@@ -552,7 +555,7 @@ static void forward_chunk_kbac(tcl_model* m, const float* feats, const int32_t* 
     {
         ProfScope ps(m, TCL_PROF_PACK, s);
         launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++m->launches;
-        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++m->launches;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s, n_src); ++m->launches;
     }
     float* E1 = w.U;
     float* E2 = w.Delta;
@@ -607,7 +610,8 @@ static void forward_chunk_kbac(tcl_model* m, const float* feats, const int32_t* 
 // One chunk of candidates [0, n) (pointers already offset).  If mc_mean != nullptr the head
 // accumulates Welford statistics for pass drop.pass instead of writing scores.
 static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
-                          float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+                          float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s,
+                          int64_t n_src = 0) {
     const tcl_dims& d = m->dims;
     Workspace& w = m->ws;
     const int L = d.max_len, dm = d.d_model;
@@ -616,7 +620,7 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     {
         ProfScope ps(m, TCL_PROF_PACK, s);
         launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++m->launches;
-        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s); ++m->launches;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, w.X, nullptr, w.row_cand, s, n_src); ++m->launches;
     }
     // encoder: SiLU after linears 1 and 2 (R1), dropout sites 0, 1 (R17)
     float* E1 = w.U;      // aliases: encoder hidden states live in the mixer buffers
@@ -659,7 +663,8 @@ static tcl_status debug_sync(const char* where, cudaStream_t s) {
 // The bf16 projection path (precision == TCL_PREC_BF16_PROJ): tcgen05 GEMMs with fused
 // epilogues for the encoder / in_proj / out_proj(+LN), one fused mixer kernel per layer.
 static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32_t* lens, int64_t n,
-                                   float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+                                   float* scores, const DropoutCtx& drop, float* mc_mean, cudaStream_t s,
+                                   int64_t n_src = 0) {
     const tcl_dims& d = m->dims;
     Workspace& w = m->ws;
     const int L = d.max_len, dm = d.d_model, di = d.expand * d.d_model, N = d.d_state, R = d.dt_rank;
@@ -673,7 +678,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
     {
         ProfScope ps(m, TCL_PROF_PACK, s);
         launch_lens_prefix(lens, n, L, w.cu, m->d_err, s); ++nl;
-        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, nullptr, w.Xb, w.row_cand, s); ++nl;
+        launch_pack(feats, lens, w.cu, n, L, d.d_in, kXld, nullptr, w.Xb, w.row_cand, s, n_src); ++nl;
     }
     if (debug_sync("pack", s) != TCL_OK) return TCL_ECUDA;
     auto base = [&]() {
@@ -771,15 +776,16 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
     return TCL_OK;
 }
 
+// n_src > 0: candidate i takes the features of candidate i mod n_src (batched MC passes).
 static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, float* scores,
-                              const DropoutCtx& drop, float* mc_mean, cudaStream_t s) {
+                              const DropoutCtx& drop, float* mc_mean, cudaStream_t s, int64_t n_src = 0) {
     if (m->use_tc) {
-        tcl_status st = forward_chunk_tc(m, feats, lens, n, scores, drop, mc_mean, s);
+        tcl_status st = forward_chunk_tc(m, feats, lens, n, scores, drop, mc_mean, s, n_src);
         if (st != TCL_OK) return st;
         return debug_sync("forward_chunk_tc", s);
     }
-    if (m->kb) forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s);
-    else forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s);
+    if (m->kb) forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s, n_src);
+    else forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s, n_src);
     const cudaError_t e = cudaGetLastError();   // launch-configuration errors of the fp32 kernels
     if (e != cudaSuccess) return cuda_error(e, m->kb ? "forward_chunk_kbac" : "forward_chunk");
     return debug_sync(m->kb ? "forward_chunk_kbac" : "forward_chunk", s);
@@ -1052,7 +1058,9 @@ tcl_status tcl_model_destroy(tcl_model* m) {
 tcl_status tcl_reserve(tcl_model* m, int64_t n_max, int32_t mc_passes_max) {
     if (!m || n_max < 0 || mc_passes_max < 0) return set_error(TCL_EINVAL, "bad argument");
     CUDA_TRY(cudaSetDevice(m->device));
-    return ensure_workspace(m, std::min(n_max, chunk_cap(m)));
+    const int64_t cap = chunk_cap(m);
+    // tcl_score_mc batches its passes: min(n, cap / p) * p <= min(n * p, cap) virtual candidates
+    return ensure_workspace(m, std::min(n_max * std::max<int64_t>(1, mc_passes_max), cap));
 }
 
 tcl_status tcl_score(tcl_model* m, const float* feats, const int32_t* lens, int64_t n, float* scores,
@@ -1094,7 +1102,10 @@ tcl_status tcl_score_mc(tcl_model* m, const float* feats, const int32_t* lens, i
     CUDA_TRY(cudaSetDevice(m->device));
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t cap = chunk_cap(m);
-    tcl_status st = ensure_workspace(m, std::min(n, cap));
+    // the passes run batched: one forward over passes x nc virtual candidates per chunk of nc
+    const int64_t cb = std::max<int64_t>(1, cap / n_passes);
+    const bool batched = cb * n_passes <= cap;
+    tcl_status st = ensure_workspace(m, batched ? std::min(n, cb) * n_passes : std::min(n, cap));
     if (st != TCL_OK) return st;
     GraphKey key;
     key.kind = 1;
@@ -1109,6 +1120,28 @@ tcl_status tcl_score_mc(tcl_model* m, const float* feats, const int32_t* lens, i
         drop.scale = (float)(1.0 / (1.0 - p));
         drop.enabled = 1;
         const size_t stride = (size_t)m->dims.max_len * m->dims.d_in;
+        if (batched) {
+            // virtual candidate v = ps * nc + i is candidate i of pass ps: replicated lengths, the
+            // pack reads features i = v mod nc, the dropout counter takes (ps, i) from v (pass_n);
+            // every kernel is batch-invariant, so each pass scores exactly as a launch of its own
+            for (int64_t off = 0; off < n; off += cb) {
+                const int64_t nc = std::min(cb, n - off);
+                const int64_t nv = nc * n_passes;
+                for (int ps = 0; ps < n_passes; ++ps)
+                    CUDA_TRY(cudaMemcpyAsync(m->ws.lens_mc + ps * nc, lens + off, sizeof(int32_t) * (size_t)nc,
+                                             cudaMemcpyDeviceToDevice, cs));
+                drop.index_base = index_base + off;
+                drop.pass = 0;
+                drop.pass_n = (uint32_t)nc;
+                tcl_status st2 = forward_any(m, feats + off * stride, m->ws.lens_mc, nv, m->ws.dsc, drop, nullptr, cs, nc);
+                if (st2 != TCL_OK) return st2;
+                ProfScope ps(m, TCL_PROF_MC, cs);
+                launch_mc_reduce(m->ws.dsc, lens + off, m->dims.max_len, nc, n_passes, mean + off, var + off, cs);
+                ++m->launches;
+            }
+            CUDA_TRY(cudaGetLastError());
+            return TCL_OK;
+        }
         for (int64_t off = 0; off < n; off += cap) {
             const int64_t nc = std::min(cap, n - off);
             drop.index_base = index_base + off;

@@ -59,11 +59,25 @@ struct DropoutCtx {
     int32_t pass;
     int64_t index_base;
     int enabled;
+    // MC passes batched into one forward (tcl_score_mc): virtual candidate v of the launch is
+    // candidate v mod pass_n of pass (pass + v / pass_n); 0 = one pass per launch (v = candidate)
+    uint32_t pass_n;
 };
+// Philox counter of (unit group, token, site, pass, global candidate index)
+__device__ __forceinline__ u32x4 dropout_counter(const DropoutCtx& d, int unit4, int token, int site,
+                                                 int64_t cand) {
+    uint32_t pass = (uint32_t)d.pass, local = (uint32_t)cand;
+    if (d.pass_n) {
+        const uint32_t q = local / d.pass_n;
+        pass += q;
+        local -= q * d.pass_n;
+    }
+    return {(uint32_t)unit4 >> 2, ((uint32_t)token << 2) | (uint32_t)site, pass,
+            (uint32_t)(d.index_base + local)};
+}
 __device__ __forceinline__ bool dropout_keep(const DropoutCtx& d, int unit, int token, int site,
                                              int64_t cand) {
-    u32x4 c = {(uint32_t)unit >> 2, ((uint32_t)token << 2) | (uint32_t)site, (uint32_t)d.pass,
-               (uint32_t)(d.index_base + cand)};
+    u32x4 c = dropout_counter(d, unit, token, site, cand);
     u32x4 w = philox4x32_10(c, (uint32_t)d.seed, (uint32_t)(d.seed >> 32));
     uint32_t word = (unit & 3) == 0 ? w.x : (unit & 3) == 1 ? w.y : (unit & 3) == 2 ? w.z : w.w;
     return word >= d.thr;
@@ -73,9 +87,7 @@ __device__ __forceinline__ bool dropout_keep(const DropoutCtx& d, int unit, int 
 // u & 3 of the call for unit4 = u & ~3): epilogues that own 4 consecutive units draw once.
 __device__ __forceinline__ u32x4 dropout_words(const DropoutCtx& d, int unit4, int token, int site,
                                                int64_t cand) {
-    u32x4 c = {(uint32_t)unit4 >> 2, ((uint32_t)token << 2) | (uint32_t)site, (uint32_t)d.pass,
-               (uint32_t)(d.index_base + cand)};
-    return philox4x32_10(c, (uint32_t)d.seed, (uint32_t)(d.seed >> 32));
+    return philox4x32_10(dropout_counter(d, unit4, token, site, cand), (uint32_t)d.seed, (uint32_t)(d.seed >> 32));
 }
 __device__ __forceinline__ float dropout_apply_word(const DropoutCtx& d, float v, uint32_t word) {
     return word >= d.thr ? v * d.scale : 0.0f;

@@ -117,6 +117,7 @@ struct Workspace {
     float* dh1 = nullptr;         // [cap_n][h1]  decoder hidden 1
     float* dh2 = nullptr;         // [cap_n][h2]  decoder hidden 2
     float* dsc = nullptr;         // [cap_n]      per-pass score (MC)
+    int32_t* lens_mc = nullptr;   // [cap_n]      lengths of the batched MC passes (pass-major)
     // bf16 tensor-core path
     __nv_bfloat16* Xb = nullptr;   // [rows][kXld]  packed features
     __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden

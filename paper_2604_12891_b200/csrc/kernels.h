@@ -25,9 +25,11 @@ enum : int { ERR_LEN = 1, ERR_TASK = 2 };
 void launch_lens_prefix(const int32_t* lens, int64_t n, int32_t max_len, int32_t* cu, int* err,
                         cudaStream_t s);
 // Gather the real rows of feats [n][L][d_in] into X [P][ldx] (columns d_in..ldx-1 zeroed) and
-// write row_cand[P].  If x_bf16 != nullptr, also writes a bf16 copy [P][ldx].
+// write row_cand[P].  If x_bf16 != nullptr, also writes a bf16 copy [P][ldx].  Candidate i reads
+// the features of candidate i mod n_src (batched MC passes: n = passes * n_src; n_src = n otherwise).
 void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int64_t n, int L,
-                 int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s);
+                 int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s,
+                 int64_t n_src = 0);
 
 // ---- SIMT fp32 GEMM with fused epilogues ------------------------------------------------------
 enum Epi : int { EPI_NONE = 0, EPI_SILU = 1, EPI_SOFTPLUS = 2, EPI_RESID = 3,
@@ -142,6 +144,10 @@ void launch_mask_invalid(const int32_t* lens, int max_len, int64_t n, float* sco
 
 // ---- head: LN_f, masked mean, decoder (a9) ----------------------------------------------------
 void launch_mc_finalize(const float* m2, int64_t n, int passes, float* var, cudaStream_t s);
+// Batched MC passes: score [passes][n] -> Welford over the passes in order 0..passes-1 (the
+// arithmetic of k_welford, pass by pass) -> mean [n], var = M2 / passes [n] (NaN: invalid length).
+void launch_mc_reduce(const float* score, const int32_t* lens, int max_len, int64_t n, int passes, float* mean,
+                      float* var, cudaStream_t s);
 
 // ---- top-k ------------------------------------------------------------------------------------
 // Local top-k keys: k keys (descending, sentinel 0 padded) of scores[0..n) with index_base.

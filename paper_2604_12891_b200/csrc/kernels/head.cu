@@ -124,43 +124,77 @@ void launch_pool_bf16(const void* F, int ldf, int dm, const int32_t* cu, const i
 // v = acc + b, SiLU (+ inverted dropout, sites 2 / 3, token 0) -- the arithmetic of the SIMT
 // GEMMs it replaces, so the scores are bit-identical to the five-launch head; (5) the score is
 // stored (NaN for an invalid length) or folded into the MC Welford statistics.
-template <int CT, int K, int NO, int NOP, bool ACT>
+template <int CT, int K, int NO, int NOP, bool ACT, int TA = 4>
 __device__ __forceinline__ void head_linear(const float* __restrict__ inT, const float* __restrict__ W,
                                             const float* __restrict__ bias, float* __restrict__ outT,
                                             float* ws, const DropoutCtx& drop, int site, int64_t cand0,
                                             int64_t n) {
     // inT [K][CT + 4], outT [NO][CT + 4] (transposed: 4 consecutive candidates are one float4).
-    // Thread -> a 4 x 4 register tile: columns 4 jq .. 4 jq + 3, candidates 4 cq .. 4 cq + 3; each
-    // output is one sequential FFMA chain over k (2 LDS.128 per 16 FFMA).
+    // Thread -> a TA x 4 register tile: columns 4 jq .. 4 jq + 3, candidates TA cq .. TA cq + TA - 1;
+    // each output is one sequential FFMA chain over k (TA / 4 + 1 LDS.128 per 4 TA FFMA).
+    static_assert(TA % 4 == 0, "TA: whole float4 candidate groups");
     constexpr int LD = CT + 4;
-    constexpr int JQ = NOP / 4, CQ = CT / 4;
+    constexpr int JQ = NOP / 4, CQ = CT / TA;
+    static_assert(JQ * CQ <= 256, "head_linear: more register tiles than threads");
     const int jq = threadIdx.x % JQ, cq = threadIdx.x / JQ;
     const bool act_thr = cq < CQ && 4 * jq < NO;
-    float acc[4][4];
+    float acc[TA][4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a)
+    for (int a = 0; a < TA; ++a)
 #pragma unroll
         for (int b = 0; b < 4; ++b) acc[a][b] = 0.0f;
-    for (int k0 = 0; k0 < K; k0 += 32) {
-        __syncthreads();   // ws reuse (and the producer of inT is done)
-        for (int idx = threadIdx.x; idx < NO * 32; idx += 256) {   // W[jj][k0 + kk] -> ws[kk][jj]
-            const int jj = idx >> 5, kk = idx & 31;
-            ws[kk * NOP + jj] = k0 + kk < K ? __ldg(W + (int64_t)jj * K + k0 + kk) : 0.0f;
+    // W is staged 32 k at a time into ws[2][32][NOP] (double-buffered: the next slice's global
+    // loads are in flight while this slice is consumed).  Layout: row kk, float4 group g of
+    // columns 4 g .. 4 g + 3 stored at group g ^ (kk & 7): a warp loads 4 rows x 8 consecutive k
+    // (32-byte segments) and its 32 stores hit 32 distinct banks; the float4 reads of a row stay
+    // conflict-free (a permutation of the row's groups).
+    static_assert(NOP >= 32, "ws swizzle needs >= 8 float4 groups per row");
+    constexpr int kPer = (NO * 32 + 255) / 256;
+    constexpr int kSlices = (K + 31) / 32;
+    float pre[kPer];
+    auto gload = [&](int k0) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int idx = threadIdx.x + 256 * e, lane = idx & 31, c = idx >> 5;
+            const int kk = 8 * (c & 3) + (lane & 7), jj = 4 * (c >> 2) + (lane >> 3);
+            pre[e] = (idx < NO * 32 && jj < NO && k0 + kk < K) ? __ldg(W + (int64_t)jj * K + k0 + kk) : 0.0f;
         }
-        __syncthreads();
+    };
+    auto sstore = [&](float* buf) {
+#pragma unroll
+        for (int e = 0; e < kPer; ++e) {
+            const int idx = threadIdx.x + 256 * e, lane = idx & 31, c = idx >> 5;
+            const int kk = 8 * (c & 3) + (lane & 7), g = c >> 2;
+            if (idx < NO * 32) buf[kk * NOP + 4 * (g ^ (kk & 7)) + (lane >> 3)] = pre[e];
+        }
+    };
+    gload(0);
+    __syncthreads();   // ws reuse (and the producer of inT is done)
+    sstore(ws);
+    __syncthreads();
+    for (int sl = 0; sl < kSlices; ++sl) {
+        const int k0 = 32 * sl;
+        const float* cur = ws + (sl & 1) * 32 * NOP;
+        if (sl + 1 < kSlices) gload(k0 + 32);
         if (act_thr) {
 #pragma unroll 4
             for (int kk = 0; kk < 32; ++kk) {
                 if (k0 + kk >= K) break;
-                const float4 wv = *reinterpret_cast<const float4*>(ws + kk * NOP + 4 * jq);
-                const float4 xv = *reinterpret_cast<const float4*>(inT + (k0 + kk) * LD + 4 * cq);
-                const float xs[4] = {xv.x, xv.y, xv.z, xv.w}, wsv[4] = {wv.x, wv.y, wv.z, wv.w};
+                const float4 wv = *reinterpret_cast<const float4*>(cur + kk * NOP + 4 * (jq ^ (kk & 7)));
+                const float wsv[4] = {wv.x, wv.y, wv.z, wv.w};
 #pragma unroll
-                for (int a = 0; a < 4; ++a)
+                for (int g = 0; g < TA / 4; ++g) {
+                    const float4 xv = *reinterpret_cast<const float4*>(inT + (k0 + kk) * LD + TA * cq + 4 * g);
+                    const float xs[4] = {xv.x, xv.y, xv.z, xv.w};
 #pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a][b] = fmaf(xs[a], wsv[b], acc[a][b]);
+                    for (int a = 0; a < 4; ++a)
+#pragma unroll
+                        for (int b = 0; b < 4; ++b) acc[4 * g + a][b] = fmaf(xs[a], wsv[b], acc[4 * g + a][b]);
+                }
             }
         }
+        if (sl + 1 < kSlices) sstore(ws + ((sl + 1) & 1) * 32 * NOP);
+        __syncthreads();
     }
     if (act_thr) {
 #pragma unroll
@@ -168,25 +202,27 @@ __device__ __forceinline__ void head_linear(const float* __restrict__ inT, const
             const int j = 4 * jq + b;
             if (j >= NO) continue;
             const float bj = __ldg(bias + j);
-            float v4[4];
 #pragma unroll
-            for (int a = 0; a < 4; ++a) {
-                const int c = 4 * cq + a;
-                float v = acc[a][b] + bj;
-                if (ACT) {
-                    v = silu(v);
-                    if (drop.enabled && cand0 + c < n) v = dropout_keep(drop, j, 0, site, cand0 + c) ? v * drop.scale : 0.0f;
+            for (int g = 0; g < TA / 4; ++g) {
+                float v4[4];
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    const int c = TA * cq + 4 * g + a;
+                    float v = acc[4 * g + a][b] + bj;
+                    if (ACT) {
+                        v = silu(v);
+                        if (drop.enabled && cand0 + c < n) v = dropout_keep(drop, j, 0, site, cand0 + c) ? v * drop.scale : 0.0f;
+                    }
+                    v4[a] = v;
                 }
-                v4[a] = v;
+                *reinterpret_cast<float4*>(outT + j * LD + TA * cq + 4 * g) = make_float4(v4[0], v4[1], v4[2], v4[3]);
             }
-            *reinterpret_cast<float4*>(outT + j * LD + 4 * cq) = make_float4(v4[0], v4[1], v4[2], v4[3]);
         }
     }
 }
 
-// CT candidates per CTA; POOL: the masked mean is computed here (one launch for the whole head),
-// else read from a.pooled.  A candidate's arithmetic does not depend on CT or POOL.
-template <int PER, bool BF16, int H1, int H2, int CT, bool POOL>
+// CT candidates per CTA.  A candidate's arithmetic does not depend on CT.
+template <int PER, bool BF16, int H1, int H2, int CT>
 __global__ void __launch_bounds__(256) k_head(HeadArgs a) {
     constexpr int kHeadCT = CT;
     constexpr int dm = 32 * PER;
@@ -197,17 +233,11 @@ __global__ void __launch_bounds__(256) k_head(HeadArgs a) {
     float* pooledT = hsm;                         // [dm][LD]
     float* h1T = pooledT + dm * LD;               // [H1][LD]
     float* h2T = h1T + H1 * LD;                   // [H2][LD]
-    float* ws = h2T + H2 * LD;                    // [32][max(H1P, H2P)]
+    float* ws = h2T + H2 * LD;                    // [2][32][max(H1P, H2P)]
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t c0 = (int64_t)blockIdx.x * kHeadCT;
     // ---- (1) masked mean (of LN_f(H) rows: computed here on the fp32 path, stored bf16 on the bf16 path)
-    if (!POOL) {
-        for (int idx = threadIdx.x; idx < kHeadCT * dm; idx += 256) {
-            const int cc = idx / dm, col = idx - cc * dm;
-            pooledT[col * LD + cc] = c0 + cc < a.n ? a.pooled[(c0 + cc) * dm + col] : 0.0f;
-        }
-    }
-    for (int cc = warp; POOL && cc < kHeadCT; cc += 8) {
+    for (int cc = warp; cc < kHeadCT; cc += 8) {
         const int64_t i = c0 + cc;
         const int T = i < a.n ? a.lens[i] : 0;
         const bool ok = T >= 1 && T <= a.max_len;
@@ -268,8 +298,11 @@ __global__ void __launch_bounds__(256) k_head(HeadArgs a) {
         }
     }
     // ---- (2)-(4) decoder
-    head_linear<CT, dm, H1, H1P, true>(pooledT, a.W1, a.b1, h1T, ws, a.drop, 2, c0, a.n);
-    head_linear<CT, H1, H2, H2P, true>(h1T, a.W2, a.b2, h2T, ws, a.drop, 3, c0, a.n);
+    // candidates per thread: 4, or as many as put every thread to work on a CT-candidate batch
+    constexpr int TA1 = CT * (H1P / 4) > 1024 ? CT * (H1P / 4) / 256 : 4;
+    constexpr int TA2 = CT * (H2P / 4) > 1024 ? CT * (H2P / 4) / 256 : 4;
+    head_linear<CT, dm, H1, H1P, true, TA1>(pooledT, a.W1, a.b1, h1T, ws, a.drop, 2, c0, a.n);
+    head_linear<CT, H1, H2, H2P, true, TA2>(h1T, a.W2, a.b2, h2T, ws, a.drop, 3, c0, a.n);
     __syncthreads();
     // ---- (3) score, then store / Welford
     if (threadIdx.x < kHeadCT) {
@@ -300,14 +333,14 @@ __global__ void __launch_bounds__(256) k_head(HeadArgs a) {
     }
 }
 
-template <int PER, bool BF16, int CT, bool POOL>
+template <int PER, bool BF16, int CT>
 static bool head_dims(const HeadArgs& a, cudaStream_t s) {
     const dim3 grid((unsigned)((a.n + CT - 1) / CT));
 #define TCL_HEAD(H1_, H2_)                                                                                 \
     if (a.h1 == H1_ && a.h2 == H2_) {                                                                 \
         constexpr int H1P = H1_ <= 32 ? 32 : (H1_ <= 64 ? 64 : (H1_ <= 128 ? 128 : 256));           \
-        const int smem = 4 * ((CT + 4) * (32 * PER + H1_ + H2_) + 32 * H1P);                         \
-        auto kern = k_head<PER, BF16, H1_, H2_, CT, POOL>;                                            \
+        const int smem = 4 * ((CT + 4) * (32 * PER + H1_ + H2_) + 2 * 32 * H1P);                     \
+        auto kern = k_head<PER, BF16, H1_, H2_, CT>;                                            \
         if (prepare_kernel(kern, smem) != cudaSuccess) return false;                                  \
         kern<<<grid, 256, smem, s>>>(a);                                                              \
         return true;                                                                                  \
@@ -325,7 +358,11 @@ static bool head_pick(const HeadArgs& a, cudaStream_t s) {
     // candidates took 0.53 ms for the decoder alone, re-staging W1 per 32 candidates, vs 0.41 ms
     // for the whole five-launch head).  Both compute every candidate with the same operations in
     // the same order: bit-identical, so the switch does not break batch invariance (tested).
-    if (a.n < 8192) return head_dims<PER, BF16, 8, true>(a, s);
+    // (measured again with a 64-candidate decoder launch after the pool kernel, weights staged
+    // double-buffered: 0.48 ms for pool + decoder at 65,536 candidates vs 0.42 ms for pool + SIMT
+    // GEMMs -- 8 warps per SM do not hide the FFMA / shared-memory latencies that the SIMT GEMMs'
+    // 24+ warps do)
+    if (a.n < 8192) return head_dims<PER, BF16, 8>(a, s);
     return false;
 }
 
@@ -372,6 +409,32 @@ __global__ void k_mask_invalid(const int32_t* __restrict__ lens, int max_len, in
 void launch_mask_invalid(const int32_t* lens, int max_len, int64_t n, float* scores, cudaStream_t s) {
     if (n == 0) return;
     k_mask_invalid<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(lens, max_len, n, scores);
+}
+
+// Batched MC passes: the per-pass scores of candidate i are score[ps * n + i]; Welford in pass order
+// with k_welford's arithmetic (bit-identical to the pass-by-pass fold), then var = M2 / passes.
+__global__ void k_mc_reduce(const float* __restrict__ score, const int32_t* __restrict__ lens, int max_len,
+                            int64_t n, int passes, float* __restrict__ mean, float* __restrict__ var) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    const int T = lens[i];
+    if (T < 1 || T > max_len) { mean[i] = NAN; var[i] = NAN; return; }
+    float m = 0.0f, q = 0.0f;
+    for (int pass = 0; pass < passes; ++pass) {
+        const float v = score[(int64_t)pass * n + i];
+        const float delta = v - m;
+        const float m_new = m + delta / (float)(pass + 1);
+        q = q + delta * (v - m_new);
+        m = m_new;
+    }
+    mean[i] = m;
+    var[i] = q / (float)passes;
+}
+
+void launch_mc_reduce(const float* score, const int32_t* lens, int max_len, int64_t n, int passes, float* mean,
+                      float* var, cudaStream_t s) {
+    if (n == 0) return;
+    k_mc_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(score, lens, max_len, n, passes, mean, var);
 }
 
 __global__ void k_mc_finalize(const float* __restrict__ m2, int64_t n, int passes,

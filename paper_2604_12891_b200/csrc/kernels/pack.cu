@@ -76,15 +76,16 @@ __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
                                               const int32_t* __restrict__ cu, int64_t n, int L,
                                               int d_in, int ldx, float* __restrict__ X,
                                               __nv_bfloat16* __restrict__ Xb,
-                                              int32_t* __restrict__ row_cand) {
+                                              int32_t* __restrict__ row_cand, int64_t n_src) {
     const int64_t i = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (i >= n) return;
     const int32_t T = lens[i];
     if (T < 1 || T > L) return;
     const int64_t row0 = cu[i];
+    const int64_t isrc = i % n_src;                 // batched MC passes re-read the same features
     if (d_in & 1) {   // odd feature width: column per lane
-        const float* srcs = feats + i * (int64_t)L * d_in;
+        const float* srcs = feats + isrc * (int64_t)L * d_in;
         for (int t = 0; t < T; ++t) {
             const int64_t row = row0 + t;
             for (int c = lane; c < ldx; c += 32) {
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
         return;
     }
     const int hp = d_in >> 1;                       // pairs per row
-    const float2* src = reinterpret_cast<const float2*>(feats + i * (int64_t)L * d_in);
+    const float2* src = reinterpret_cast<const float2*>(feats + isrc * (int64_t)L * d_in);
     const int npairs = T * hp;
     for (int p = lane; p < npairs; p += 32) {
         const int t = p / hp, c = 2 * (p - t * hp);
@@ -117,10 +118,11 @@ __global__ void __launch_bounds__(256) k_pack(const float* __restrict__ feats,
 }
 
 void launch_pack(const float* feats, const int32_t* lens, const int32_t* cu, int64_t n, int L,
-                 int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s) {
+                 int d_in, int ldx, float* X, void* x_bf16, int32_t* row_cand, cudaStream_t s,
+                 int64_t n_src) {
     if (n == 0) return;
     k_pack<<<(unsigned)((n + 7) / 8), 256, 0, s>>>(feats, lens, cu, n, L, d_in, ldx, X,
-                                                   (__nv_bfloat16*)x_bf16, row_cand);
+                                                   (__nv_bfloat16*)x_bf16, row_cand, n_src > 0 ? n_src : n);
 }
 
 }  // namespace tcl

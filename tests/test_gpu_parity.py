@@ -393,6 +393,28 @@ def test_mc_parity(torch_cuda, oracle, name):
     assert np.array_equal(m2, mean[100:]) and np.array_equal(v2, var[100:])
 
 
+def test_mc_batched_passes_across_chunks(torch_cuda, oracle):
+    """tcl_score_mc runs its passes batched (passes x nc virtual candidates per forward, nc =
+    chunk capacity / passes = 16,777 at rdu's max_len 25): 20,000 candidates x 10 passes take two
+    chunks.  A slice straddling the chunk seam is bit-identical to the full batch (masks keyed by
+    (pass, global index)), and sampled candidates on both sides match the oracle."""
+    from paper_2604_12891_b200 import Model
+    c = inputs.config("rdu")
+    d, w, f, l = _setup("rdu", n=20000)
+    passes = c["mc_passes"]
+    m = Model(w, d)
+    mean, var = _mc_gpu(torch_cuda, m, f, l, passes, 99, index_base=5)
+    m2, v2 = _mc_gpu(torch_cuda, m, f[16000:17600], l[16000:17600], passes, 99, index_base=16005)
+    assert np.array_equal(m2, mean[16000:17600]) and np.array_equal(v2, var[16000:17600])
+    sample = np.array([0, 1, 16775, 16776, 16777, 16778, 19999])
+    rm = np.empty(sample.size); rv = np.empty(sample.size)
+    for j, i in enumerate(sample):   # the oracle keys masks by index_base + position: one call each
+        a, b = oracle.score_mc(d, w, f[i:i + 1], l[i:i + 1], passes, 99, index_base=5 + int(i))
+        rm[j], rv[j] = a[0], b[0]
+    _check_scores(mean[sample], rm, d.precision)
+    assert np.all(np.abs(var[sample] - rv) <= 2 * TOL[d.precision] * np.sqrt(np.maximum(rv, 1e-8)) + 1e-7)
+
+
 # ------------------------------------------------------------------------------------ host e2e
 @pytest.mark.parametrize("n", [1000, 20000, 70000])
 def test_score_host_matches_device(torch_cuda, n):
