@@ -13,15 +13,16 @@
 // DI threads owns the packed rows of a row-balanced contiguous candidate range and walks them in
 // chunks of 16 rows that may span candidates; thread d owns channel d (conv window and N states in
 // registers, reset at candidate starts).  Per chunk:
-//   0. the chunk's [x | z] rows (fp32) arrive by one cp.async.bulk into a double buffer, the next
-//      chunk's copy in flight while this one is computed;
+//   0. the chunk's x rows (fp32) arrive by cp.async.bulk (one per row) into a double buffer, the
+//      next chunk's copies in flight while this one is computed; z goes straight to registers;
 //   1. conv + SiLU -> u (smem);
 //   2. x_proj in fp32 FFMA: thread (row r, column group) accumulates its columns over K = DI with
 //      128-bit smem loads (the contraction is 16 x (R + 2N) x DI, far below tensor-core size, and
 //      the fp32 path's 1e-4 parity rules out TF32);
-//   3. dt_proj + softplus: thread d forms its own channel's Delta for the 16 rows (W_dt row in
-//      registers);
+//   3. per token, dt_proj + softplus: thread d forms its own channel's Delta (W_dt row in
+//      registers), then
 //   4. the scan with the fp32 path's accurate ZOH (e^x - 1 by series where Ab - 1 would cancel).
+// (27 KB of shared memory less than staging [x | z] and Delta: 5 CTAs / SM at d_inner 128.)
 // Everything matches the unfused fp32 kernels (mixer.cu, gemm_simt.cu) op for op except the
 // summation order of x_proj.  HBM traffic: x, z in and g out only.
 #include <cstdlib>
@@ -39,10 +40,9 @@ struct Smem {
     static constexpr int kNXP = (NX + 3) / 4 * 4;      // x_proj columns padded to a float4
     static constexpr int kUld = DI + 4;                // +16 B per row: conflict-free float4 rows
     static constexpr int kDbcld = kNXP + 4;
-    static constexpr int kXZ = 0;                                   // f32 [2][16][2 DI] (bulk dst)
-    static constexpr int kU = kXZ + 2 * kTC * 2 * DI * 4;           // f32 [16][DI + 4]
-    static constexpr int kDl = kU + kTC * kUld * 4;                 // f32 [16][DI]
-    static constexpr int kDbc = kDl + kTC * DI * 4;                 // f32 [16][NXP + 4]
+    static constexpr int kXZ = 0;                                   // f32 [2][16][DI]: x rows (bulk dst)
+    static constexpr int kU = kXZ + 2 * kTC * DI * 4;               // f32 [16][DI + 4]
+    static constexpr int kDbc = kU + kTC * kUld * 4;                // f32 [16][NXP + 4]
     static constexpr int kWx = kDbc + kTC * kDbcld * 4;             // f32 [NXP][DI]
     static constexpr int kBar = kWx + kNXP * DI * 4;                // 2 mbarriers
     static constexpr int kStartWords = 512;                         // candidate-start bits
@@ -98,7 +98,6 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
     extern __shared__ __align__(128) uint8_t msm[];
     float* xz_s = reinterpret_cast<float*>(msm + L::kXZ);
     float* u_s = reinterpret_cast<float*>(msm + L::kU);
-    float* dl_s = reinterpret_cast<float*>(msm + L::kDl);
     float* dbc_s = reinterpret_cast<float*>(msm + L::kDbc);
     float* wx_s = reinterpret_cast<float*>(msm + L::kWx);
     uint64_t* bar = reinterpret_cast<uint64_t*>(msm + L::kBar);
@@ -159,11 +158,13 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
     }
     __syncthreads();
     int64_t k_next = c0;
+    // the x half of the chunk's [x | z] rows, one bulk copy per row (z goes straight to registers)
     auto issue = [&](int64_t r, int b) {
         if (d == 0 && r < r_end) {
-            const uint32_t bytes = (uint32_t)(r_end - r < kTC ? r_end - r : kTC) * 2 * DI * 4;
-            tc::mbar_arrive_expect_tx(&bar[b], bytes);
-            bulk_g2s(xz_s + b * kTC * 2 * DI, a.XZ + r * (int64_t)a.ldxz, bytes, &bar[b]);
+            const int nr = (int)(r_end - r < kTC ? r_end - r : kTC);
+            tc::mbar_arrive_expect_tx(&bar[b], (uint32_t)nr * DI * 4);
+            for (int i = 0; i < nr; ++i)
+                bulk_g2s(xz_s + (b * kTC + i) * DI, a.XZ + (r + i) * (int64_t)a.ldxz, DI * 4, &bar[b]);
         }
     };
     issue(r0, 0);
@@ -189,9 +190,16 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
             }
         }
         issue(r0 + kTC, buf ^ 1);
+        // the gate's z of a full chunk: 16 coalesced loads in flight through phases 1-3
+        const float* zg = a.XZ + r0 * (int64_t)a.ldxz + DI + d;
+        float zr[kTC];
+        if (tc == kTC) {
+#pragma unroll
+            for (int tt = 0; tt < kTC; ++tt) zr[tt] = zg[(int64_t)tt * a.ldxz];
+        }
         tc::mbar_wait(&bar[buf], (parity >> buf) & 1u);
         parity ^= 1u << buf;
-        const float* xz = xz_s + buf * kTC * 2 * DI;
+        const float* xz = xz_s + buf * kTC * DI;
 
         // ---- 1. causal conv + SiLU (rows >= tc: u = 0, so x_proj of the stale rows stays finite)
 #pragma unroll
@@ -202,7 +210,7 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
 #pragma unroll
                     for (int k = 0; k < DC; ++k) win[k] = 0.0f;
                 }
-                const float x = xz[tt * 2 * DI + d];
+                const float x = xz[tt * DI + d];
                 float acc = fmaf(wc[DC - 1], x, bconv);
 #pragma unroll
                 for (int k = 0; k < DC - 1; ++k) acc = fmaf(wc[DC - 2 - k], win[k], acc);
@@ -243,24 +251,20 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
             }
         }
         __syncthreads();
-        // ---- 3. dt_proj + softplus: thread d, its channel, the chunk's rows
-#pragma unroll 4
-        for (int tt = 0; tt < kTC; ++tt) {
-            float acc = bdt;
-#pragma unroll
-            for (int q = 0; q < R; ++q) acc = fmaf(dbc_s[tt * L::kDbcld + q], wdt[q], acc);
-            dl_s[tt * DI + d] = softplus_f32(acc);
-        }
-        // ---- 4. selective scan + D skip + gate (each thread reads only its own u / Delta)
+        // ---- 3 + 4. per token: dt_proj + softplus of the thread's channel, then the selective
+        // scan + D skip + gate (each thread reads only its own u); full chunks are unrolled, so
+        // the exponentials of the next tokens overlap the state update of this one
         float* gout = a.G + r0 * a.ldg + d;
-        for (int tt = 0; tt < tc; ++tt) {
+        auto scan_tok = [&](int tt, float z) {
+            float dacc = bdt;
+#pragma unroll
+            for (int q = 0; q < R; ++q) dacc = fmaf(dbc_s[tt * L::kDbcld + q], wdt[q], dacc);
+            const float dl = softplus_f32(dacc);
             if ((starts >> tt) & 1u) {
 #pragma unroll
                 for (int p = 0; p < N / 2; ++p) sv[p] = make_float2(0.f, 0.f);
             }
             const float u = u_s[tt * L::kUld + d];
-            const float dl = dl_s[tt * DI + d];
-            const float z = xz[tt * 2 * DI + DI + d];
             const float* Bt = dbc_s + tt * L::kDbcld + R;
             const float* Ct = Bt + N;
             float y = 0.0f;
@@ -298,8 +302,15 @@ __global__ void __launch_bounds__(DI) k_mixer_f32(MixerF32Args a) {
             }
             y = fmaf(Dv, u, y);
             gout[(int64_t)tt * a.ldg] = y * silu(z);
+        };
+        if (tc == kTC) {
+#pragma unroll
+            for (int tt = 0; tt < kTC; ++tt) scan_tok(tt, zr[tt]);
+        } else {
+#pragma unroll 1
+            for (int tt = 0; tt < tc; ++tt) scan_tok(tt, zg[(int64_t)tt * a.ldxz]);
         }
-        __syncthreads();   // the next chunk overwrites u_s / dl_s / dbc_s and this xz buffer
+        __syncthreads();   // the next chunk overwrites u_s / dbc_s and this x buffer
         buf ^= 1;
         r0 += kTC;
         ++chunk;
