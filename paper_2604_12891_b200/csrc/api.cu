@@ -443,7 +443,8 @@ struct F32Run {
         p.out = lng ? m->ws.A : nullptr; p.ldo = tw.n; p.ln_g = lng; p.ln_b = lnb; p.eps = m->dims.ln_eps;
         p.drop = drop; p.site = site; p.row_cand = m->ws.row_cand; p.cu = m->ws.cu;
         if (epi != 1) p.drop.enabled = 0;
-        launch_gemm_tf32(amap, tw.tm_hi, tw.tm_lo, p, tw.bn, tw.k, m->num_sms, s);
+        const cudaError_t e = launch_gemm_tf32(amap, tw.tm_hi, tw.tm_lo, p, tw.bn, tw.k, m->num_sms, s);
+        if (e != cudaSuccess && m->fwd_err == cudaSuccess) m->fwd_err = e;
         ++m->launches;
     }
 
@@ -784,8 +785,10 @@ static tcl_status forward_any(tcl_model* m, const float* feats, const int32_t* l
         if (st != TCL_OK) return st;
         return debug_sync("forward_chunk_tc", s);
     }
+    m->fwd_err = cudaSuccess;
     if (m->kb) forward_chunk_kbac(m, feats, lens, n, scores, drop, mc_mean, s, n_src);
     else forward_chunk(m, feats, lens, n, scores, drop, mc_mean, s, n_src);
+    if (m->fwd_err != cudaSuccess) return cuda_error(m->fwd_err, "forward_chunk: 3xTF32 GEMM launch refused");
     const cudaError_t e = cudaGetLastError();   // launch-configuration errors of the fp32 kernels
     if (e != cudaSuccess) return cuda_error(e, m->kb ? "forward_chunk_kbac" : "forward_chunk");
     return debug_sync(m->kb ? "forward_chunk_kbac" : "forward_chunk", s);

@@ -185,6 +185,7 @@ struct tcl_model {
     cudaStream_t copy_stream = nullptr;
     std::vector<cudaEvent_t> chunk_events;
     int64_t launches = 0;
+    cudaError_t fwd_err = cudaSuccess;   // a host-side launch refusal inside the fp32 forward (reported by forward_any)
     void* rdu_scratch = nullptr;
     size_t rdu_scratch_cap = 0;
     // KB + AC two-column model (tcl_model_create_kbac): this object holds the AC column

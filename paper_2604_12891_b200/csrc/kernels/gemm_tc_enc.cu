@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_enc12(const __grid_constant__ C
     using S = Smem<E1N, E2N>;
     constexpr int KB1 = S::kKB1;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment (128B-swizzled TMA tiles) as an offset from the shared array, so that every
+    // access below stays in the shared state space (LDS / STS, not generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sW1 = smem + S::kOffW1;
     uint8_t* sW2 = smem + S::kOffW2;
     uint8_t* sX = smem + S::kOffX;

@@ -69,7 +69,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_ln(const __grid_constant__
     constexpr int kStages = S::kStages;
     constexpr int NC = BN / 64;  // 32-column chunks per epilogue warp (its column half)
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment (128B-swizzled TMA tiles) as an offset from the shared array, so that every
+    // access below stays in the shared state space (LDS / STS, not generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     float* s_bias = reinterpret_cast<float*>(smem + S::kOffPar);
     float* s_g = s_bias + BN;
     float* s_b = s_g + BN;

@@ -140,7 +140,9 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
     constexpr int kStages = S::kStages;
     constexpr int NCH = BN / 32;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // 1024-byte alignment (128B-swizzled TMA tiles) as an offset from the shared array, so that every
+    // access below stays in the shared state space (LDS / STS, not generic LD / ST)
+    uint8_t* smem = smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* sB = smem + S::kOffB;
     uint8_t* sA = smem + S::kOffA;
     float* s_bias = reinterpret_cast<float*>(smem + S::kOffPar);
@@ -446,6 +448,7 @@ void launch_tf32_split(const float* w, int64_t n, float* hi, float* lo, cudaStre
     if (n > 0) tf::k_tf32_split<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(w, n, hi, lo);
 }
 
+// Exactly the (bn, kb) pairs instantiated in launch_gemm_tf32 below.
 bool tf32_gemm_supported(int bn, int k) {
     const int kb = (k + 31) / 32;
     return (bn == 32 || bn == 64 || bn == 128 || bn == 256) && (kb == 1 || kb == 2 || kb == 4 || kb == 8) &&
@@ -459,7 +462,7 @@ cudaError_t launch_gemm_tf32(const CUtensorMap& a, const CUtensorMap& b, const C
     const int grid = (num_sms / p.n_tiles) * p.n_tiles;
 #define TCL_TF_CASE(BN_, KB_) \
     if (bn == BN_ && kb == KB_) return tf::launch_epi<BN_, KB_>(a, b, blo, p, grid, s);
-    TCL_TF_CASE(32, 1) TCL_TF_CASE(32, 2) TCL_TF_CASE(32, 4)
+    TCL_TF_CASE(32, 1) TCL_TF_CASE(32, 2) TCL_TF_CASE(32, 4) TCL_TF_CASE(32, 8)
     TCL_TF_CASE(64, 1) TCL_TF_CASE(64, 2) TCL_TF_CASE(64, 4) TCL_TF_CASE(64, 8)
     TCL_TF_CASE(128, 1) TCL_TF_CASE(128, 2) TCL_TF_CASE(128, 4)
     TCL_TF_CASE(256, 1) TCL_TF_CASE(256, 2)

@@ -73,17 +73,17 @@ __device__ __forceinline__ float softplus_f32(float v) {
     return fmaf(y, p, fmaxf(v, 0.0f));
 }
 
-// Accurate e^x - 1 for a pair of states (x2 = x log2 e): the degree-6 series where Ab - 1 would
-// cancel (|x2| < 0.25, as mixer.cu's fp32 scan), as a packed FFMA2 / FMUL2 Horner chain with a
-// per-lane select (no branch: |Delta A| straddles the threshold across the states of one warp).
+// Accurate e^x - 1 for a pair of states (x2 = x log2 e): the degree-5 series where Ab - 1 would
+// cancel (|x2| < 0.25; error bound as mixer.cu's expm1_from: <= 1.4e-6 relative, set at the
+// threshold by Ab - 1), as a packed FFMA2 / FMUL2 Horner chain with a per-lane select (no branch:
+// |Delta A| straddles the threshold across the states of one warp).
 __device__ __forceinline__ float2 expm1_acc2(float2 x2, float2 Ab) {
-    const float2 x = __fmul2_rn(x2, make_float2(kLn2, kLn2));
-    float2 p = __ffma2_rn(x, make_float2(1.0f / 720, 1.0f / 720), make_float2(1.0f / 120, 1.0f / 120));
-    p = __ffma2_rn(p, x, make_float2(1.0f / 24, 1.0f / 24));
-    p = __ffma2_rn(p, x, make_float2(1.0f / 6, 1.0f / 6));
-    p = __ffma2_rn(p, x, make_float2(0.5f, 0.5f));
-    p = __ffma2_rn(p, x, make_float2(1.0f, 1.0f));
-    const float2 ser = __fmul2_rn(x, p);
+    // e^x - 1 = sum_{k=1..5} x^k / k!, x = x2 ln 2, as a polynomial in x2 (coefficients ln2^k / k!)
+    float2 p = __ffma2_rn(x2, make_float2(1.3333558e-3f, 1.3333558e-3f), make_float2(9.6181291e-3f, 9.6181291e-3f));
+    p = __ffma2_rn(p, x2, make_float2(5.5504109e-2f, 5.5504109e-2f));
+    p = __ffma2_rn(p, x2, make_float2(0.24022651f, 0.24022651f));
+    p = __ffma2_rn(p, x2, make_float2(0.69314718f, 0.69314718f));
+    const float2 ser = __fmul2_rn(x2, p);
     const float2 am1 = __fadd2_rn(Ab, make_float2(-1.0f, -1.0f));
     return make_float2(fabsf(x2.x) < 0.25f ? ser.x : am1.x, fabsf(x2.y) < 0.25f ? ser.y : am1.y);
 }

@@ -574,3 +574,13 @@ def test_score_parity_other_dims(torch_cuda, oracle, base, over, prec):
         assert rho >= 0.999, f"spearman {rho:.5f}"
         msg += f" spearman={rho:.6f}"
     print(msg)
+
+
+def test_score_parity_fp32_tf32_bn32_kb8(torch_cuda, oracle):
+    """Encoder widths (256, 96): linear 2 has N = 96 (32-column 3xTF32 tiles) and K = 256 (8 K-blocks),
+    the (bn 32, kb 8) instantiation (missing from the dispatcher before: a silent no-op launch)."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("tuning", n=200, dims_over=dict(n_layer=1, enc_dims=(256, 96, 128), precision=inputs.PREC_FP32))
+    m = Model(w, d)
+    got = _gpu_score(torch_cuda, m, f, l)
+    _check_scores(got, oracle.score(d, w, f, l), d.precision)

@@ -63,13 +63,18 @@ def test_train_step_gradients(torch_cuda, name, n, group):
     assert np.abs(ds - ref_ds).max() <= 1e-3 * np.abs(ref_ds).max()
     g = m.tcl_train_read("grads", inputs.weights_count(d))
     gmax = np.abs(ref_g).max()
+    # dec.b3's gradient is the plain fp32 sum of the n dscores, whose exact value is 0 (antisymmetric
+    # pair lambdas): its error is bounded by the dscores' own errors plus the summation error of n
+    # fp32 additions, n 2^-24 sum |ds| (standard recursive-summation bound)
+    b3_floor = np.abs(ds - ref_ds).sum() + n * 2.0 ** -24 * np.abs(ds).sum()
     for ent in inputs.manifest(d):
         o, cnt = ent["offset"], int(np.prod(ent["shape"]))
         ref = ref_g[o:o + cnt]
         err = np.abs(g[o:o + cnt] - ref).max()
-        # + 1e-6 of the global scale: tensors whose exact gradient vanishes (dec.b3: sum of the
-        # antisymmetric pair lambdas is 0) carry only fp32 cancellation residue
-        assert err <= 1e-3 * np.abs(ref).max() + 1e-6 * gmax, (ent["name"], err, np.abs(ref).max())
+        # + 1e-6 of the global scale: tensors whose exact gradient vanishes carry only fp32
+        # cancellation residue
+        floor = max(1e-6 * gmax, b3_floor if ent["name"] == "dec.b3" else 0.0)
+        assert err <= 1e-3 * np.abs(ref).max() + floor, (ent["name"], err, np.abs(ref).max(), floor)
     # the model is unchanged without apply_update
     assert np.array_equal(m.tcl_train_read("weights", w.size), w)
 
