@@ -239,8 +239,8 @@ static tcl_status setup_tf32(tcl_model* m) {
         t.w = g.w; t.n = g.n; t.k = g.k; t.hi = p; t.lo = p + (size_t)g.n * g.k;
         p += 2 * (size_t)g.n * g.k;
         t.bn = tf32_pick_bn(g.n, g.k, g.full);
-        if (t.bn && !(make_tmap_f32(&t.tm_hi, t.hi, g.k, g.n, (uint64_t)g.k * 4, 32, t.bn) &&
-                      make_tmap_f32(&t.tm_lo, t.lo, g.k, g.n, (uint64_t)g.k * 4, 32, t.bn)))
+        if (t.bn && !(make_tmap_f32_sw64(&t.tm_hi, t.hi, g.k, g.n, (uint64_t)g.k * 4, t.bn) &&
+                      make_tmap_f32_sw64(&t.tm_lo, t.lo, g.k, g.n, (uint64_t)g.k * 4, t.bn)))
             return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (tf32 weights)");
         m->tfw.push_back(t);
     }
@@ -307,11 +307,11 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     }
     if (!m->use_tc) {   // 3xTF32 A operands of the fp32 path (box {32, 128})
         const int e1 = d.enc_dims[0], e2 = d.enc_dims[1];
-        const bool ok = make_tmap_f32(&w.tmX32, w.X, kXld, rows, kXld * 4, 32, 128) &&
-                        make_tmap_f32(&w.tmE1f, w.U, e1, rows, (uint64_t)e1 * 4, 32, 128) &&
-                        make_tmap_f32(&w.tmE2f, w.Delta, e2, rows, (uint64_t)e2 * 4, 32, 128) &&
-                        make_tmap_f32(&w.tmA32, w.A, dm, rows, (uint64_t)dm * 4, 32, 128) &&
-                        make_tmap_f32(&w.tmG32, w.G, di, rows, (uint64_t)di * 4, 32, 128);
+        const bool ok = make_tmap_f32_sw64(&w.tmX32, w.X, kXld, rows, kXld * 4, 128) &&
+                        make_tmap_f32_sw64(&w.tmE1f, w.U, e1, rows, (uint64_t)e1 * 4, 128) &&
+                        make_tmap_f32_sw64(&w.tmE2f, w.Delta, e2, rows, (uint64_t)e2 * 4, 128) &&
+                        make_tmap_f32_sw64(&w.tmA32, w.A, dm, rows, (uint64_t)dm * 4, 128) &&
+                        make_tmap_f32_sw64(&w.tmG32, w.G, di, rows, (uint64_t)di * 4, 128);
         if (!ok) { free_workspace(m); return set_error(TCL_ECUDA, "cuTensorMapEncodeTiled failed (fp32 workspace)"); }
     }
     if (m->use_tc) {

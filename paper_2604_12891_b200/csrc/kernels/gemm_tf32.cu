@@ -13,10 +13,10 @@
 //
 // Design (as gemm_tc.cu): persistent CTA per SM, weight-stationary (the CTA's [BN x K] slice of
 // W_hi and W_lo stays in shared memory, loaded once by TMA), 128-row activation tiles streamed by
-// TMA through a ring of K-blocks (32 fp32 = 128 B per row, 128B-swizzled, K-major -- the same byte
-// layout and descriptors as a bf16 K-block of 64).  Roles (448 threads):
+// TMA through a ring of K-blocks (16 fp32 = 64 B per row, 64B-swizzled, K-major: half-size stages,
+// so that 4+ A loads are in flight next to the resident weights).  Roles (448 threads):
 //   warp 0       TMA producer
-//   warp 1       TMEM allocator + single-thread MMA issuer (12 MMAs per K-block)
+//   warp 1       TMEM allocator + single-thread MMA issuer (6 MMAs per K-block)
 //   warps 2..5   split: A_hi in place (mask) and A_lo (another smem buffer) per landed K-block; the
 //                element-wise split keeps the swizzled layout, so no address math is needed
 //   warps 6..13  epilogue: warp w drains TMEM lanes 32 (w % 4).., column half (w - 6) / 4
@@ -35,19 +35,23 @@ namespace tcl {
 namespace tf {
 
 constexpr int kBM = 128;
-constexpr int kKBBytes = kBM * 128;   // one 128-row x 32-fp32 K-block
+constexpr int kKBBytes = kBM * 64;    // one 128-row x 16-fp32 K-block (64-byte rows, 64B swizzle)
 constexpr int kSplitWarps = 4;
 constexpr int kEpiWarps = 8;
 constexpr int kThreads = 64 + 32 * (kSplitWarps + kEpiWarps);
 constexpr int kEpi0 = 2 + kSplitWarps;   // first epilogue warp
 
+// KB counts 32-wide K units (the dispatcher's kb = ceil(K / 32)); the ring moves 16-wide K-blocks
+// (K2 = 2 KB of them): half-size stages, twice as many in the same shared memory, so more A loads
+// are in flight (measured with 32-wide blocks: 2 stages, the split warps waiting on TMA)
 template <int BN, int KB>
 struct Smem {
-    static constexpr int kBBytes = KB * BN * 128;                    // one weight matrix (hi or lo)
+    static constexpr int K2 = 2 * KB;                                // 16-wide K-blocks
+    static constexpr int kBBytes = K2 * BN * 64;                     // one weight matrix (hi or lo)
     static constexpr int kStageBytes = 2 * kKBBytes;                 // A_hi + A_lo of one K-block
     static constexpr int kStgBytes = kEpiWarps * 32 * 16 * 4;         // epilogue staging [warp][32 rows][16 fp32]
     static constexpr int kStagesRaw = (220 * 1024 - kStgBytes - 2 * kBBytes) / kStageBytes;
-    static constexpr int kStages = kStagesRaw > 6 ? 6 : kStagesRaw;
+    static constexpr int kStages = kStagesRaw > 8 ? 8 : kStagesRaw;
     static constexpr int kOffB = 0;                                  // W_hi, then W_lo
     static constexpr int kOffA = 2 * kBBytes;                        // stage s: A_hi at s*2K, A_lo at s*2K + K
     static constexpr int kOffStg = kOffA + kStages * kStageBytes;
@@ -190,18 +194,18 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
             // ---------------- TMA producer: W_hi, W_lo once; A K-blocks through the ring
             tc::tma_prefetch(&tmA);
             tc::mbar_arrive_expect_tx(bfull, 2 * S::kBBytes);
-            for (int kb = 0; kb < KB; ++kb) {
-                tc::tma_load_2d(sB + kb * BN * 128, &tmB, kb * 32, n_tile * BN, bfull);
-                tc::tma_load_2d(sB + S::kBBytes + kb * BN * 128, &tmBlo, kb * 32, n_tile * BN, bfull);
+            for (int kb = 0; kb < S::K2; ++kb) {
+                tc::tma_load_2d(sB + kb * BN * 64, &tmB, kb * 16, n_tile * BN, bfull);
+                tc::tma_load_2d(sB + S::kBBytes + kb * BN * 64, &tmBlo, kb * 16, n_tile * BN, bfull);
             }
             const uint64_t pol = tc::policy_evict_first();
             int stage = 0;
             uint32_t phase = 0;
             for (int m = m_first; m < num_m; m += m_step) {
-                for (int kb = 0; kb < KB; ++kb) {
+                for (int kb = 0; kb < S::K2; ++kb) {
                     tc::mbar_wait(&empty[stage], phase ^ 1);
                     tc::mbar_arrive_expect_tx(&full[stage], kKBBytes);
-                    tc::tma_load_2d_hint(sA + stage * S::kStageBytes, &tmA, kb * 32, m * kBM, &full[stage], pol);
+                    tc::tma_load_2d_hint(sA + stage * S::kStageBytes, &tmA, kb * 16, m * kBM, &full[stage], pol);
                     if (++stage == kStages) { stage = 0; phase ^= 1; }
                 }
             }
@@ -222,15 +226,15 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
                 tc::mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc::tc_fence_after();
                 const uint32_t d = tmem_base + acc * BN;
-                for (int kb = 0; kb < KB; ++kb) {
+                for (int kb = 0; kb < S::K2; ++kb) {
                     tc::mbar_wait(&split[stage], phase);
                     tc::tc_fence_after();
                     const uint32_t a_hi = sA_addr + stage * S::kStageBytes, a_lo = a_hi + kKBBytes;
-                    const uint32_t b_hi = sB_addr + kb * BN * 128, b_lo = b_hi + S::kBBytes;
+                    const uint32_t b_hi = sB_addr + kb * BN * 64, b_lo = b_hi + S::kBBytes;
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const uint64_t ah = tc::sw128_kmajor_desc(a_hi + k * 32), al = tc::sw128_kmajor_desc(a_lo + k * 32);
-                        const uint64_t bh = tc::sw128_kmajor_desc(b_hi + k * 32), bl = tc::sw128_kmajor_desc(b_lo + k * 32);
+                    for (int k = 0; k < 2; ++k) {   // two 8-deep k steps per 64-byte row
+                        const uint64_t ah = tc::sw64_kmajor_desc(a_hi + k * 32), al = tc::sw64_kmajor_desc(a_lo + k * 32);
+                        const uint64_t bh = tc::sw64_kmajor_desc(b_hi + k * 32), bl = tc::sw64_kmajor_desc(b_lo + k * 32);
                         mma_tf32(d, ah, bh, idesc, (kb | k) != 0);
                         mma_tf32(d, ah, bl, idesc, 1);
                         mma_tf32(d, al, bh, idesc, 1);
@@ -249,7 +253,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_gemm_tf32(const __grid_constant
         int stage = 0;
         uint32_t phase = 0;
         for (int m = m_first; m < num_m; m += m_step) {
-            for (int kb = 0; kb < KB; ++kb) {
+            for (int kb = 0; kb < S::K2; ++kb) {
                 tc::mbar_wait(&full[stage], phase);
                 uint4* hi = reinterpret_cast<uint4*>(sA + stage * S::kStageBytes);
                 uint4* lo = reinterpret_cast<uint4*>(sA + stage * S::kStageBytes + kKBBytes);

@@ -46,6 +46,9 @@ bool make_tmap_bf16(CUtensorMap* m, const void* base, uint64_t inner, uint64_t o
 // 2-D fp32 tensor map, 128B swizzle, box {box_inner (<= 32), box_outer}.
 bool make_tmap_f32(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
                    uint32_t box_inner, uint32_t box_outer);
+// fp32 map with box {16, box_outer} (64-byte rows) and 64-byte swizzle: the 3xTF32 GEMM's operands
+bool make_tmap_f32_sw64(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_bytes,
+                        uint32_t box_outer);
 // Residual + LayerNorm GEMM (gemm_tc_ln.cu): bn = d_model in {128, 256}; H: fp32 map of the
 // residual stream (box {32, 32}); O: bf16 map of the LayerNorm output (box {64, 32}).
 cudaError_t launch_gemm_tc_ln(const CUtensorMap& a, const CUtensorMap& b, const CUtensorMap& h,
