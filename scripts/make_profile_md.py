@@ -61,7 +61,8 @@ def main():
         def val(m):
             # exact metric name, else the (section-prefixed) column that ends with it
             i = hdr.index(m) if m in hdr else next(k for k, h in enumerate(hdr) if h.endswith(m))
-            return float(row[i].replace(",", "")) * mult.get(units[i], 1)
+            v = row[i].replace(",", "")
+            return None if v == "no data" else float(v) * mult.get(units[i], 1)   # None: ncu had no sample
         traffic[key] = {"kernel": row[hdr.index("Kernel Name")][:60], "dram_bytes_read": val("dram__bytes_read.sum"),
                         "dram_bytes_write": val("dram__bytes_write.sum"),
                         # tcgen05 / mma.sync activity: the realtime tensor-pipe counter (the plain
