@@ -222,7 +222,9 @@ static void refresh_tf32(tcl_model* m, cudaStream_t s) {
 static tcl_status setup_tf32(tcl_model* m) {
     const tcl_dims& d = m->dims;
     const int dm = d.d_model, di = d.expand * d.d_model, e1 = d.enc_dims[0], e2 = d.enc_dims[1];
-    const bool fuse_ln = dm == 128 && d.n_layer > 0;   // as forward_chunk
+    // full-row tiles (LayerNorm in the epilogue) for the GEMMs that write the residual stream: at
+    // d_model <= 128 the row fits one 3xTF32 tile (forward_chunk fuses only where they exist)
+    const bool fuse_ln = dm <= 128 && d.n_layer > 0;
     struct G { const float* w; int n, k; bool full; };
     std::vector<G> gs = {{m->W1p, e1, kXld, false}, {m->wp.enc_W2, e2, e1, false}, {m->wp.enc_W3, dm, e2, fuse_ln}};
     for (int l = 0; l < d.n_layer; ++l) {
@@ -627,7 +629,11 @@ static void forward_chunk(tcl_model* m, const float* feats, const int32_t* lens,
     float* E1 = w.U;      // aliases: encoder hidden states live in the mixer buffers
     float* E2 = w.Delta;
     r.tf32 = !m->tfw.empty();
-    r.fuse_ln = dm == 128 && d.n_layer > 0;
+    // LN_l fused into the GEMM that writes the residual stream: the SIMT kernels' LN epilogue
+    // (d_model 128), or full-row 3xTF32 tiles for the encoder's linear 3 and every out_proj but the last
+    bool tf_rows = r.tf32 && m->tfw[2].bn == dm;
+    for (int l = 0; l + 1 < d.n_layer && tf_rows; ++l) tf_rows = m->tfw[4 + 2 * l].bn == dm;
+    r.fuse_ln = d.n_layer > 0 && (dm == 128 || tf_rows);
     if (r.tf32 && m->tfw[0].bn) r.gemm_tf(w.tmX32, m->tfw[0], m->wp.enc_b1, E1, e1, 1, 0, TCL_PROF_ENCODER);
     else r.gemm(w.X, kXld, m->W1p, kXld, m->wp.enc_b1, E1, e1, kXld, e1, EPI_SILU, 0, TCL_PROF_ENCODER);
     if (r.tf32 && m->tfw[1].bn) r.gemm_tf(w.tmE1f, m->tfw[1], m->wp.enc_b2, E2, e2, 1, 1, TCL_PROF_ENCODER);
