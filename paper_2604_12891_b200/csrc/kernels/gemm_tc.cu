@@ -57,7 +57,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 }
 
 // MC-dropout keep test kept out of line: the hot epilogues stay small (no I-cache pressure).
-__device__ __noinline__ u32x4 drop_words(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
+__device__ __forceinline__ u32x4 drop_words(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
     return dropout_words(d, unit4, token, site, cand);
 }
 

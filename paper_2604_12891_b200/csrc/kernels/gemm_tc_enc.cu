@@ -50,7 +50,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 // one Philox draw per 4 consecutive units (kept out of line: small hot epilogues)
-__device__ __noinline__ u32x4 drop_words_enc(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
+__device__ __forceinline__ u32x4 drop_words_enc(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
     return dropout_words(d, unit4, token, site, cand);
 }
 

@@ -85,7 +85,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
     return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
 
-__device__ __noinline__ u32x4 drop_words_tf(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
+__device__ __forceinline__ u32x4 drop_words_tf(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
     return dropout_words(d, unit4, token, site, cand);
 }
 
