@@ -56,7 +56,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
-// MC-dropout keep test kept out of line: the hot epilogues stay small (no I-cache pressure).
+// MC-dropout keep words, inlined (an out-of-line call kept a stack frame and extra registers in every
+// dropout epilogue: measured slower)
 __device__ __forceinline__ u32x4 drop_words(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
     return dropout_words(d, unit4, token, site, cand);
 }

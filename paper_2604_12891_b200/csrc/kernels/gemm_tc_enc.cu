@@ -49,7 +49,7 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<uint32_t*>(&h);
 }
-// one Philox draw per 4 consecutive units (kept out of line: small hot epilogues)
+// one Philox draw per 4 consecutive units (inlined: the out-of-line call kept a stack frame)
 __device__ __forceinline__ u32x4 drop_words_enc(const DropoutCtx& d, int unit4, int token, int site, int64_t cand) {
     return dropout_words(d, unit4, token, site, cand);
 }
