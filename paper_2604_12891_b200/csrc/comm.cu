@@ -128,6 +128,11 @@ tcl_status tcl_topk_global(tcl_model* m, const float* scores, int64_t n_local, i
         ProfScope ps(m, TCL_PROF_ALLGATHER, s);
         ncclResult_t r = ncclAllGather(m->keys_send, m->keys_recv, (size_t)k, ncclUint64, (ncclComm_t)m->comm, s);
         if (r != ncclSuccess) return nccl_error(r, "ncclAllGather");
+        // errors NCCL raises asynchronously (a peer's failure, a network / NVLink fault) surface here
+        ncclResult_t ar = ncclSuccess;
+        r = ncclCommGetAsyncError((ncclComm_t)m->comm, &ar);
+        if (r != ncclSuccess) return nccl_error(r, "ncclCommGetAsyncError");
+        if (ar != ncclSuccess && ar != ncclInProgress) return nccl_error(ar, "ncclAllGather (asynchronous error)");
     }
     return tcl_topk_merge_keys(m, reinterpret_cast<const uint64_t*>(m->keys_recv), (int64_t)m->nranks * k, k, idx, top,
                                stream);

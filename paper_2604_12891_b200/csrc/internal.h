@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>   // header-only NVTX v3 (stage ranges in ProfScope)
 
 #include <string>
 #include <vector>
@@ -216,7 +217,17 @@ struct tcl_model {
 namespace tcl {
 void comm_destroy(tcl_model* m);
 
-// Brackets the launches issued in its scope with CUDA events when profiling is on.
+// NVTX range names of the stage kinds (tcl.h TCL_PROF_*), for nsys / ncu --nvtx timelines
+inline const char* prof_stage_name(int k) {
+    static const char* const names[TCL_PROF_NKINDS] = {
+        "tcl:pack", "tcl:encoder", "tcl:layernorm", "tcl:in_proj", "tcl:conv", "tcl:x_proj", "tcl:dt_proj",
+        "tcl:scan", "tcl:out_proj", "tcl:head", "tcl:topk", "tcl:mixer", "tcl:allgather", "tcl:mc",
+        "tcl:lateral", "tcl:xdt"};
+    return (k >= 0 && k < TCL_PROF_NKINDS) ? names[k] : "tcl:?";
+}
+
+// Brackets the launches issued in its scope with an NVTX range (host side; a no-op without a tool
+// attached) and, when profiling is on, with CUDA events.
 struct ProfScope {
     tcl_model* m; int kind; cudaStream_t s; cudaEvent_t a = nullptr;
     static cudaEvent_t get(tcl_model* m) {
@@ -224,13 +235,16 @@ struct ProfScope {
         cudaEvent_t e; cudaEventCreate(&e); return e;
     }
     ProfScope(tcl_model* m_, int k, cudaStream_t s_) : m(m_), kind(k), s(s_) {
+        nvtxRangePushA(prof_stage_name(k));
         if (m->prof_on) { a = get(m); cudaEventRecord(a, s); }
     }
     ~ProfScope() {
-        if (!a) return;
-        cudaEvent_t b = get(m);
-        cudaEventRecord(b, s);
-        m->prof_recs.push_back({kind, a, b});
+        if (a) {
+            cudaEvent_t b = get(m);
+            cudaEventRecord(b, s);
+            m->prof_recs.push_back({kind, a, b});
+        }
+        nvtxRangePop();
     }
 };
 }

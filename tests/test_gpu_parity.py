@@ -469,6 +469,31 @@ def test_bf16_invalid_lengths_and_host_path(torch_cuda, oracle):
     assert np.isnan(s2[10]) and np.array_equal(s2[ok], good[ok])
 
 
+@pytest.mark.parametrize("name", ["tuning", "large"])
+def test_mc_batched_invalid_lengths_and_one_pass(torch_cuda, name):
+    """Batched MC passes with invalid lengths in the batch: those candidates get NaN mean and var
+    (and TCL_ELEN), every other candidate is bit-identical to the same batch with valid lengths
+    there (masks keyed by (pass, global index)); one pass: var == 0 exactly."""
+    from paper_2604_12891_b200 import Model, TclError
+    torch = torch_cuda
+    d, w, f, l = _setup(name, n=50)
+    m = Model(w, d)
+    mean, var = _mc_gpu(torch, m, f, l, 4, 31, index_base=9)
+    l2 = l.copy()
+    l2[[0, 17, 49]] = [0, d.max_len + 1, -3]
+    mt, vt = torch.empty(50, device="cuda"), torch.empty(50, device="cuda")
+    m.tcl_score_mc(torch.from_numpy(f).cuda(), torch.from_numpy(l2).cuda(), 4, 31, 9, mt, vt)
+    with pytest.raises(TclError):
+        m.tcl_sync_error()
+    m2, v2 = mt.cpu().numpy(), vt.cpu().numpy()
+    bad = np.zeros(50, bool)
+    bad[[0, 17, 49]] = True
+    assert np.all(np.isnan(m2[bad])) and np.all(np.isnan(v2[bad]))
+    assert np.array_equal(m2[~bad], mean[~bad]) and np.array_equal(v2[~bad], var[~bad])
+    m1, v1 = _mc_gpu(torch, m, f, l, 1, 31, index_base=9)
+    assert np.all(v1 == 0) and np.all(np.isfinite(m1))
+
+
 def test_bf16_long_config_small_batch(torch_cuda, oracle):
     """`long` model (L = 128) on a small batch: parity + batch invariance across chunks."""
     from paper_2604_12891_b200 import Model
