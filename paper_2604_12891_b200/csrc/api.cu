@@ -294,6 +294,7 @@ static tcl_status ensure_workspace(tcl_model* m, int64_t chunk_n) {
     TAKE(dh2, chunk_n * d.dec_dims[1]);
     TAKE(dsc, chunk_n);
     TAKE(lens_mc, chunk_n);
+    TAKE(scan_ctr, 64);
     if (m->kb) {
         TAKE(Hk, rows * dm);
         TAKE(E1k, rows * d.enc_dims[0]);
@@ -729,6 +730,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
         ++nl;
         if (debug_sync("enc3", s) != TCL_OK) return TCL_ECUDA;
     }
+    CUDA_TRY(cudaMemsetAsync(w.scan_ctr, 0, sizeof(int) * (size_t)d.n_layer, s));   // k_scan work groups
     for (int l = 0; l < d.n_layer; ++l) {
         const LayerPtrs& q = m->wp.layers[l];
         {   // in_proj + SiLU(z) + conv + SiLU (inconv.cu): x never leaves the SM
@@ -757,7 +759,7 @@ static tcl_status forward_chunk_tc(tcl_model* m, const float* feats, const int32
             ScanBf16Args a{};
             a.Pk = w.Pk; a.GZ = w.GZb; a.G = w.Gb;
             a.A2 = m->A2 + (size_t)l * di * N; a.invA = m->invA + (size_t)l * di * N; a.Dv = q.Dv;
-            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.disc = d.disc;
+            a.cu = w.cu; a.n = n; a.DI = di; a.N = N; a.disc = d.disc; a.work_counter = w.scan_ctr + l;
             if ((e = launch_scan_bf16(a, m->num_sms, s)) != cudaSuccess) return cuda_error(e, "scan");
             ++nl;
             if (debug_sync("scan", s) != TCL_OK) return TCL_ECUDA;

@@ -119,6 +119,7 @@ struct Workspace {
     float* dh2 = nullptr;         // [cap_n][h2]  decoder hidden 2
     float* dsc = nullptr;         // [cap_n]      per-pass score (MC)
     int32_t* lens_mc = nullptr;   // [cap_n]      lengths of the batched MC passes (pass-major)
+    int* scan_ctr = nullptr;      // [kMaxLayers] k_scan work-group counters, zeroed per forward
     // bf16 tensor-core path
     __nv_bfloat16* Xb = nullptr;   // [rows][kXld]  packed features
     __nv_bfloat16* XZb = nullptr;  // [rows][max(2 di, e1 + e2)]  in_proj output / encoder hidden

@@ -70,11 +70,12 @@ __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.comm
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-// Candidate range of a persistent CTA over the packed rows: [c0, c1) balanced by rows (CTA b of G
-// owns the candidates whose first row lies in [P b / G, P (b + 1) / G)).
+// A candidate range [c0, c1) and its packed rows [r0, r_end) (a k_scan work group).
 struct RowRange {
     int64_t c0, c1, r0, r_end;
 };
+
+// Static partition: CTA b of G owns the candidates whose first row lies in [P b / G, P (b + 1) / G).
 __device__ __forceinline__ RowRange cta_rows(const int32_t* cu, int64_t n) {
     const int64_t P = cu[n];
     auto cand_at = [&](int64_t target) -> int64_t {   // first candidate i with cu[i] >= target

@@ -19,10 +19,10 @@
 // (10-bit mantissa: 8x finer than bf16; both are bounded: u is a SiLU of a 4-tap conv, Delta a
 // softplus), B and C in fp32.
 //
-// k_scan: persistent CTAs of DI threads, thread d owns channel d; each CTA owns the packed rows of a
-// contiguous candidate range (balanced by rows) and walks them in 16-row chunks that may span
-// candidates (SSM state reset at candidate starts, from a start-bit array built once per CTA in
-// shared memory).
+// k_scan: persistent CTAs of DI threads, thread d owns channel d; each CTA claims groups of
+// kScanItem whole candidates from a global counter and walks each group's packed rows in 16-row
+// chunks that may span candidates (SSM state reset at candidate starts, from a start-bit array
+// built per group in shared memory).
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 
@@ -38,6 +38,7 @@ namespace tcl {
 namespace mx {
 
 constexpr int kTC = 16;          // tokens per chunk (= mma.sync M)
+constexpr int kScanItem = 8;     // candidates per k_scan work group at large n (measured: 4 same, 16 slower)
 constexpr int kStartWords = 1024; // start bits for up to 2,048 chunks per CTA (else walk cu[])
 
 // Candidate-start bits of rows [r0, r_end) in shared memory (16 bits per chunk).
@@ -265,7 +266,31 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
         tc::fence_mbar_init();
     }
     __syncthreads();
-    const RowRange rr = cta_rows(a.cu, a.n);
+    __shared__ int s_item;
+    uint32_t parity = 0;
+    int buf = 0;
+    float2 s[N / 2];
+#pragma unroll
+    for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
+    // Work: groups of a.group whole candidates claimed from a global counter (dynamic: CTAs that
+    // run faster take more groups, so all finish together); a.group == 0 (small batches): one
+    // row-balanced candidate range per CTA, no claiming.  A candidate is always scanned by one CTA
+    // in row order: the result does not depend on the assignment.
+    for (int iter = 0;; ++iter) {
+    RowRange rr;
+    if (a.group == 0) {
+        if (iter > 0) break;
+        rr = cta_rows(a.cu, a.n);
+    } else {
+        if (d == 0) s_item = atomicAdd(a.work_counter, 1);
+        __syncthreads();
+        const int64_t c0 = (int64_t)s_item * a.group;
+        if (c0 >= a.n) break;
+        rr.c0 = c0;
+        rr.c1 = c0 + a.group < a.n ? c0 + a.group : a.n;
+        rr.r0 = a.cu[rr.c0];
+        rr.r_end = a.cu[rr.c1];
+    }
     const bool bits = build_start_bits(st_w, a.cu, rr, DI);
     int64_t k_next = rr.c0;
     auto issue = [&](int64_t r, int b) {
@@ -277,12 +302,8 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
         }
     };
 #pragma unroll
-    for (int b = 0; b < STAGES; ++b) issue(rr.r0 + (int64_t)b * kTC, b);
-    uint32_t parity = 0;
-    float2 s[N / 2];
-#pragma unroll
-    for (int n = 0; n < N / 2; ++n) s[n] = make_float2(0.f, 0.f);
-    int buf = 0, chunk = 0;
+    for (int b = 0; b < STAGES; ++b) issue(rr.r0 + (int64_t)b * kTC, (buf + b) % STAGES);
+    int chunk = 0;
     for (int64_t r0 = rr.r0; r0 < rr.r_end; r0 += kTC, ++chunk) {
         const int tc = (int)(rr.r_end - r0 < kTC ? rr.r_end - r0 : kTC);
         const uint32_t starts = chunk_starts(bits, st_w, chunk, a.cu, k_next, rr.c1, r0, tc);
@@ -360,6 +381,8 @@ __global__ void __launch_bounds__(DI, MINB) k_scan(ScanBf16Args a) {
         issue(r0 + (int64_t)STAGES * kTC, buf);
         if (++buf == STAGES) buf = 0;
     }
+    __syncthreads();       // s_item / the start bits are rewritten for the next group
+    }
 }
 
 // ============================================================================ launchers
@@ -391,7 +414,11 @@ static cudaError_t scan_launch(const ScanBf16Args& a, int num_sms, cudaStream_t 
     if (e != cudaSuccess) return e;
     int64_t grid = (int64_t)num_sms * bps;
     if (grid > a.n) grid = a.n;
-    kern<<<(unsigned)grid, DI, smem, s>>>(a);
+    // groups of kScanItem candidates claimed dynamically; small batches (fewer than 4 groups per
+    // CTA) take the static row-balanced partition (measured: claiming costs more than the tail there)
+    ScanBf16Args b = a;
+    b.group = a.n >= 4 * grid * kScanItem ? kScanItem : 0;
+    kern<<<(unsigned)grid, DI, smem, s>>>(b);
     return cudaGetLastError();
 }
 

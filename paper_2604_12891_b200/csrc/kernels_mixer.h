@@ -55,6 +55,8 @@ struct ScanBf16Args {
     const int32_t* cu;
     int64_t n;
     int DI, N, disc;
+    int* work_counter;                   // zeroed before the launch: candidate groups are claimed from it
+    int group;                           // candidates per claimed group; 0 = static partition (set by the launcher)
 };
 cudaError_t launch_scan_bf16(const ScanBf16Args& a, int num_sms, cudaStream_t s);
 
