@@ -231,6 +231,20 @@ def test_permutation_and_batch_invariance_bitexact(torch_cuda, name):
     assert np.array_equal(_gpu_score(torch_cuda, m2, f[250:750], l[250:750]), s[250:750])
 
 
+def test_scan_work_assignment_bitexact(torch_cuda):
+    """k_scan claims groups of 8 candidates dynamically at large batches (>= 4 groups per CTA) and
+    keeps the static row partition below: a 16,000-candidate batch (dynamic) and its 500-candidate
+    slices (static) score every candidate bit-identically, as does the batch permuted."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("large", n=16000)
+    m = Model(w, d)
+    s = _gpu_score(torch_cuda, m, f, l)
+    for a in (0, 7777, 15500):
+        assert np.array_equal(_gpu_score(torch_cuda, m, f[a:a + 500], l[a:a + 500]), s[a:a + 500])
+    perm = np.random.default_rng(5).permutation(len(l))
+    assert np.array_equal(_gpu_score(torch_cuda, m, f[perm], l[perm]), s[perm])
+
+
 @pytest.mark.parametrize("name,prec", [("tuning", inputs.PREC_FP32), ("large", inputs.PREC_BF16_PROJ)])
 def test_head_forms_bitexact(torch_cuda, name, prec):
     """The one-launch head (batches < 8,192) and the five-launch head (larger batches) compute each
