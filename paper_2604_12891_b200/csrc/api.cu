@@ -1071,6 +1071,8 @@ tcl_status tcl_reserve(tcl_model* m, int64_t n_max, int32_t mc_passes_max) {
     CUDA_TRY(cudaSetDevice(m->device));
     const int64_t cap = chunk_cap(m);
     // tcl_score_mc batches its passes: min(n, cap / p) * p <= min(n * p, cap) virtual candidates
+    // (n_max >= cap: the whole arena; otherwise n_max * p < 2^22 * 2^31 cannot overflow)
+    if (n_max >= cap) return ensure_workspace(m, cap);
     return ensure_workspace(m, std::min(n_max * std::max<int64_t>(1, mc_passes_max), cap));
 }
 
