@@ -623,3 +623,21 @@ def test_score_parity_fp32_tf32_bn32_kb8(torch_cuda, oracle):
     m = Model(w, d)
     got = _gpu_score(torch_cuda, m, f, l)
     _check_scores(got, oracle.score(d, w, f, l), d.precision)
+
+
+def test_reserve_then_score_and_mc(torch_cuda):
+    """tcl_reserve(n_max, mc_passes_max) pre-allocates for batched MC passes; results equal an
+    unreserved model bit for bit; an oversized n_max reserves the whole arena without overflow."""
+    from paper_2604_12891_b200 import Model
+    d, w, f, l = _setup("tuning", n=700)
+    m0 = Model(w, d)
+    mean0, var0 = _mc_gpu(torch_cuda, m0, f, l, 5, 11, index_base=3)
+    s0 = _gpu_score(torch_cuda, m0, f, l)
+    m = Model(w, d)
+    m.reserve(700, 5)
+    mean, var = _mc_gpu(torch_cuda, m, f, l, 5, 11, index_base=3)
+    assert np.array_equal(mean, mean0) and np.array_equal(var, var0)
+    assert np.array_equal(_gpu_score(torch_cuda, m, f, l), s0)
+    m2 = Model(w, d)
+    m2.reserve(1 << 40, 1 << 20)
+    assert np.array_equal(_gpu_score(torch_cuda, m2, f, l), s0)
